@@ -1,0 +1,167 @@
+/* hsz_b200.h -- C ABI of the B200-native HoSZp hot path (sm_100a).
+ *
+ * Drop-in boundary for the reference package `hoszp` 0.1.0
+ * (arxiv 2408.11971).  The reference is pure Python/numpy and has no FFI;
+ * its operator API is the module surface listed in SURVEY.md §8(b).  Each
+ * entry point below names the reference function it replaces (file:line
+ * relative to /root/reference/pkg/src/hoszp/).  The Python mirror of that
+ * API (paper_2408_11971_b200/codec.py, ops.py) binds these symbols through
+ * ctypes; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - every pointer argument is DEVICE memory unless stated; the caller owns
+ *    all buffers (torch tensors or cudaMalloc) and passes a cudaStream_t as
+ *    `void* stream` (NULL = legacy default stream);
+ *  - all calls are asynchronous on `stream`; data-dependent failures are
+ *    OR-ed into the device error word `*err` (HSZ_ERR_* bits) and surface
+ *    after the caller synchronizes -- the Python layer maps them onto the
+ *    reference's exception classes (errors.py:4-45);
+ *  - the return value reports argument / launch errors only (HSZ_OK = 0);
+ *  - a stream is described by four section buffers exactly as in
+ *    pkg/FORMAT.md:24-37 -- widths u8[B], outliers i32[B], sign planes,
+ *    payload -- plus a tile-offset cache: u64[2*(T+1)] holding the exclusive
+ *    (sign, payload) byte offset of every tile of HSZ_TILE_BLOCKS blocks,
+ *    T = hsz_tile_count(n, block_len); entry T is the section totals;
+ *  - section buffers must have HSZ_SECTION_SLACK zero bytes of slack past
+ *    their capacity (kernels read/write whole 32-bit words at the end);
+ *  - `ws` is a per-stream workspace of hsz_workspace_size() bytes, zeroed
+ *    once with hsz_workspace_init(); it is reused across calls on the same
+ *    CUDA stream (never concurrently from two streams).
+ */
+#ifndef HSZ_B200_H
+#define HSZ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HSZ_TILE_BLOCKS 128
+#define HSZ_SECTION_SLACK 16
+
+/* raw element type codes (FORMAT.md header byte 5) */
+#define HSZ_F32 0
+#define HSZ_F64 1
+
+/* decode output kinds */
+#define HSZ_OUT_F32 0   /* float32 values   (codec.py:112-115, f32 streams)   */
+#define HSZ_OUT_F64 1   /* float64 grid     (codec.py:107-109, 511-513)       */
+#define HSZ_OUT_BINS 2  /* int64 bins       (codec.py:517-520 decode_to_quant) */
+
+/* return codes */
+#define HSZ_OK 0
+#define HSZ_EINVAL (-1)
+#define HSZ_ECUDA (-2)
+
+/* device error-word bits */
+#define HSZ_ERR_NONFINITE (1u << 0)         /* ValueError      codec.py:52-53   */
+#define HSZ_ERR_QUANT_OVERFLOW (1u << 1)    /* QuantOverflow   codec.py:136-137 */
+#define HSZ_ERR_QUANT_RESOLUTION (1u << 2)  /* QuantOverflow   codec.py:150-154 */
+#define HSZ_ERR_PREFIX_OVERFLOW (1u << 3)   /* QuantOverflow   codec.py:259-260 */
+#define HSZ_ERR_RESCALE_OVERFLOW (1u << 4)  /* QuantOverflow   ops.py:201-202   */
+#define HSZ_ERR_OUTLIER_OVERFLOW (1u << 5)  /* OutlierOverflow model.py:182-191 */
+#define HSZ_ERR_CAPACITY (1u << 6)          /* output section buffer too small  */
+#define HSZ_ERR_OUTPUT_NONFINITE (1u << 7)  /* ValueError on decoded RawArray   */
+#define HSZ_ERR_BAD_WIDTH (1u << 8)         /* GeometryMismatch model.py:217    */
+
+/* ---- geometry / workspace ------------------------------------------------ */
+
+/* number of tiles of HSZ_TILE_BLOCKS blocks (QuantParams.block_count, model.py:81-84) */
+uint64_t hsz_tile_count(uint64_t n, uint32_t block_len);
+/* worst-case section sizes (bytes) for n elements: sign planes, payload */
+uint64_t hsz_sign_bound(uint64_t n, uint32_t block_len);
+uint64_t hsz_payload_bound(uint64_t n, uint32_t block_len);
+uint64_t hsz_workspace_size(uint64_t n, uint32_t block_len);
+int hsz_workspace_init(void* ws, uint64_t ws_bytes, void* stream);
+/* scratch (device bytes) hsz_scalar_mul needs besides ws (0 for block_len 32) */
+uint64_t hsz_scalar_mul_scratch_size(uint64_t n, uint32_t block_len);
+
+/* ---- K0: value range + finiteness -----------------------------------------
+ * Replaces the RawArray finite check (codec.py:52-53) and the two reductions
+ * of resolve_eps(mode="rel") (codec.py:96-99).  minmax = device double[2]
+ * (exact: every f32 widens exactly). */
+int hsz_minmax(const void* x, int dtype, uint64_t n, double* minmax, uint32_t* err,
+               void* ws, uint64_t ws_bytes, void* stream);
+
+/* ---- K1: compress ----------------------------------------------------------
+ * Replaces codec.compress (codec.py:495-498) = quantize (codec.py:118-155)
+ * + _split_residuals/_block_widths/_pack_stream (codec.py:178-225,393-416).
+ * Single pass: the input is read once, sections are placed by decoupled
+ * look-back.  tile_offsets[2*T], [2*T+1] receive the section totals.  If a
+ * section outgrows its capacity HSZ_ERR_CAPACITY is set (totals still valid)
+ * and the caller retries with exact capacities. */
+int hsz_compress(const void* x, int dtype, uint64_t n, uint32_t block_len, double eps,
+                 uint8_t* widths, int32_t* outliers, uint8_t* signs, uint64_t sign_cap,
+                 uint8_t* payload, uint64_t payload_cap, uint64_t* tile_offsets,
+                 uint32_t* err, void* ws, uint64_t ws_bytes, void* stream);
+
+/* Replaces codec.encode_from_quant (codec.py:523-525): int64 bins -> stream. */
+int hsz_encode_bins(const int64_t* bins, uint64_t n, uint32_t block_len, uint8_t* widths,
+                    int32_t* outliers, uint8_t* signs, uint64_t sign_cap, uint8_t* payload,
+                    uint64_t payload_cap, uint64_t* tile_offsets, uint32_t* err, void* ws,
+                    uint64_t ws_bytes, void* stream);
+
+/* Replaces codec.quantize (codec.py:118-155): raw values -> int64 bins. */
+int hsz_quantize(const void* x, int dtype, uint64_t n, double eps, int64_t* bins,
+                 uint32_t* err, void* stream);
+
+/* Replaces codec.dequantize (codec.py:158-160): int64 bins -> values
+ * (out_kind HSZ_OUT_F32 / HSZ_OUT_F64). */
+int hsz_dequantize(const int64_t* bins, uint64_t n, double eps, int out_kind, void* out,
+                   uint32_t* err, void* stream);
+
+/* ---- K2: tile offsets (section offsets of codec.py:298-301, per tile) ---- */
+int hsz_tile_offsets(const uint8_t* widths, uint64_t n, uint32_t block_len,
+                     uint64_t* tile_offsets, uint32_t* err, void* ws, uint64_t ws_bytes,
+                     void* stream);
+
+/* ---- K3: decode ------------------------------------------------------------
+ * Replaces codec.decompress (codec.py:501-514) and decode_to_quant
+ * (codec.py:517-520): unpack (codec.py:350-441) + prefix rebuild
+ * (codec.py:228-262) + dequantize (codec.py:107-115).  out_kind HSZ_OUT_*. */
+int hsz_decode(const uint8_t* widths, const int32_t* outliers, const uint8_t* signs,
+               const uint8_t* payload, const uint64_t* tile_offsets, uint64_t n,
+               uint32_t block_len, double eps, int out_kind, void* out, uint32_t* err,
+               void* stream);
+
+/* ---- K4: negate (ops.py:88-109) --------------------------------------------
+ * Flips every stored sign bit (padding untouched) and negates the outliers.
+ * widths / payload / tile offsets are shared with the input, as in the
+ * reference.  The sign-section length is read from tile_offsets[2*T]. */
+int hsz_negate(const uint8_t* widths, const int32_t* outliers_in, int32_t* outliers_out,
+               const uint8_t* signs_in, uint8_t* signs_out, const uint64_t* tile_offsets,
+               uint64_t n, uint32_t block_len, uint32_t* err, void* stream);
+
+/* ---- K5: scalar add / sub (ops.py:112-125): outliers + rs, int32 guard --- */
+int hsz_scalar_add(const int32_t* outliers_in, int32_t* outliers_out, uint64_t nblocks,
+                   int64_t rs, uint32_t* err, void* stream);
+
+/* ---- K6: scalar multiply (ops.py:199-225) ----------------------------------
+ * decode -> p = bin * rs (exact) -> RN(2eps * f64(p)) -> round half away ->
+ * re-encode, fused and placed by look-back.  `scratch` as sized by
+ * hsz_scalar_mul_scratch_size (may be NULL when that is 0). */
+int hsz_scalar_mul(const uint8_t* widths, const int32_t* outliers, const uint8_t* signs,
+                   const uint8_t* payload, const uint64_t* tile_offsets, uint64_t n,
+                   uint32_t block_len, double eps, int64_t rs, uint8_t* out_widths,
+                   int32_t* out_outliers, uint8_t* out_signs, uint64_t sign_cap,
+                   uint8_t* out_payload, uint64_t payload_cap, uint64_t* out_tile_offsets,
+                   void* scratch, uint32_t* err, void* ws, uint64_t ws_bytes, void* stream);
+
+/* ---- K7: exact moments (ops.py:249-357) -------------------------------------
+ * out (device u64[5]) = S as signed 128-bit (lo, hi) and, if want_sq,
+ * Q = sum(bins^2) as unsigned 192-bit (limb0, limb1, limb2).  The host
+ * finishes mean (ops.py:363) / variance (ops.py:386,393) with exact ints. */
+int hsz_moments(const uint8_t* widths, const int32_t* outliers, const uint8_t* signs,
+                const uint8_t* payload, const uint64_t* tile_offsets, uint64_t n,
+                uint32_t block_len, int want_sq, uint64_t* out, uint32_t* err, void* ws,
+                uint64_t ws_bytes, void* stream);
+
+/* library identification (for the loader's sanity check) */
+const char* hsz_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HSZ_B200_H */

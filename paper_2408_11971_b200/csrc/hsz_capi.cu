@@ -1,0 +1,544 @@
+// C ABI of the B200 hot path (see include/hsz_b200.h) + the streaming ops
+// (value range, negate, scalar add) that need no block decoding.
+//
+// Build (done by __graft_entry__.build / paper_2408_11971_b200/build.py):
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared
+//        -Xcompiler -fPIC -o paper_2408_11971_b200/_lib/libhsz_b200.so hsz_capi.cu
+
+#include <cstdio>
+
+#include "hsz_common.cuh"
+#include "hsz_generic.cuh"
+#include "hsz_k32.cuh"
+#include "hsz_quant.cuh"
+
+namespace hsz {
+namespace ops {
+
+constexpr int kThreads = 256;
+constexpr int kMinmaxCtas = static_cast<int>(kMinmaxCtasMax);
+
+// ---- K0: min / max / finiteness (codec.py:52-53, 96-99) -------------------
+template <typename T>
+__global__ void __launch_bounds__(kThreads) minmax_kernel(const T* x, uint64_t n, double* out,
+                                                          uint32_t* err, void* ws) {
+  double lo = INFINITY, hi = -INFINITY;
+  bool bad = false;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if constexpr (sizeof(T) == 4) {
+    const bool vec = (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
+    const uint64_t nv = vec ? n / 4 : 0;
+    const float4* xv = reinterpret_cast<const float4*>(x);
+    float flo = INFINITY, fhi = -INFINITY;
+    for (uint64_t i = tid; i < nv; i += stride) {
+      const float4 v = __ldcs(xv + i);
+      bad |= !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
+      flo = fminf(fminf(flo, v.x), fminf(fminf(v.y, v.z), v.w));
+      fhi = fmaxf(fmaxf(fhi, v.x), fmaxf(fmaxf(v.y, v.z), v.w));
+    }
+    for (uint64_t i = nv * 4 + tid; i < n; i += stride) {
+      const float v = x[i];
+      bad |= !isfinite(v);
+      flo = fminf(flo, v);
+      fhi = fmaxf(fhi, v);
+    }
+    lo = flo;
+    hi = fhi;
+  } else {
+    for (uint64_t i = tid; i < n; i += stride) {
+      const double v = x[i];
+      bad |= !isfinite(v);
+      lo = fmin(lo, v);
+      hi = fmax(hi, v);
+    }
+  }
+  for (int m = 16; m > 0; m >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(kFull, lo, m));
+    hi = fmax(hi, __shfl_xor_sync(kFull, hi, m));
+  }
+  if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(err, HSZ_ERR_NONFINITE);
+  __shared__ double s_lo[kThreads / 32], s_hi[kThreads / 32];
+  __shared__ bool s_last;
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_lo[warp] = lo;
+    s_hi[warp] = hi;
+  }
+  __syncthreads();
+  uint64_t* base = static_cast<uint64_t*>(ws);
+  uint64_t* done = base + 3;
+  double* part = reinterpret_cast<double*>(base + kWsMinmaxOff);
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < kThreads / 32; ++i) {
+      lo = fmin(lo, s_lo[i]);
+      hi = fmax(hi, s_hi[i]);
+    }
+    part[2 * blockIdx.x] = lo;
+    part[2 * blockIdx.x + 1] = hi;
+    __threadfence();
+    s_last = atom_add_acq_rel(done, 1) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence();
+  for (unsigned i = 0; i < gridDim.x; ++i) {
+    lo = fmin(lo, __longlong_as_double(ld_relaxed(reinterpret_cast<uint64_t*>(part + 2 * i))));
+    hi = fmax(hi, __longlong_as_double(ld_relaxed(reinterpret_cast<uint64_t*>(part + 2 * i + 1))));
+  }
+  out[0] = lo;
+  out[1] = hi;
+  st_relaxed(done, 0);
+}
+
+// ---- K4: negate (ops.py:88-109) --------------------------------------------
+// Every stored sign bit flips; padding bits of a block's last sign byte stay
+// 0.  Full non-constant blocks all contribute sk = ceil(k/8) bytes, so the
+// mask of byte j depends only on j % sk -- except for a partial tail block,
+// which always sits at the very end of the section.
+__global__ void __launch_bounds__(kThreads) negate_kernel(
+    const uint8_t* widths, const int32_t* oin, int32_t* oout, const uint8_t* sin, uint8_t* sout,
+    const uint64_t* toff, uint64_t ntiles, uint64_t n, uint32_t k, uint64_t nblocks,
+    uint32_t* err) {
+  const uint64_t S = toff[2 * ntiles];
+  const uint32_t r = static_cast<uint32_t>(n % k);
+  const bool tail_part = r != 0 && widths[nblocks - 1] > 0;
+  const uint64_t tail_bytes = tail_part ? (r + 7) / 8 : 0;
+  const uint64_t per_end = S - tail_bytes;
+  const uint32_t sk = (k + 7) / 8, kr = k & 7;
+  const uint8_t kmask = static_cast<uint8_t>((0xFFu << (8 - kr)) & 0xFFu);
+  const uint8_t tmask = static_cast<uint8_t>((0xFFu << (8 - (r & 7))) & 0xFFu);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  // sign planes, 16 bytes per thread step
+  const uint64_t nchunks = (S + 15) / 16;
+  for (uint64_t c = tid; c < nchunks; c += stride) {
+    const uint64_t j0 = c * 16;
+    if (kr == 0 && j0 + 16 <= per_end) {
+      uint4 v = *reinterpret_cast<const uint4*>(sin + j0);
+      v.x = ~v.x;
+      v.y = ~v.y;
+      v.z = ~v.z;
+      v.w = ~v.w;
+      *reinterpret_cast<uint4*>(sout + j0) = v;
+      continue;
+    }
+    const uint64_t j1 = (j0 + 16 < S) ? j0 + 16 : S;
+    for (uint64_t j = j0; j < j1; ++j) {
+      uint8_t m = 0xFF;
+      if (j < per_end) {
+        if (kr && (j % sk) == sk - 1) m = kmask;
+      } else if (j == S - 1 && (r & 7)) {
+        m = tmask;
+      }
+      sout[j] = sin[j] ^ m;
+    }
+  }
+  // outliers
+  uint32_t flags = 0;
+  for (uint64_t i = tid; i < nblocks; i += stride) {
+    const int64_t v = -static_cast<int64_t>(oin[i]);
+    if (v > INT32_MAX) flags |= HSZ_ERR_OUTLIER_OVERFLOW;
+    oout[i] = static_cast<int32_t>(v);
+  }
+  if (flags) atomicOr(err, flags);
+}
+
+// ---- K5: scalar add (ops.py:112-118) -----------------------------------------
+__global__ void __launch_bounds__(kThreads) sadd_kernel(const int32_t* oin, int32_t* oout,
+                                                        uint64_t nblocks, int64_t rs,
+                                                        uint32_t* err) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint32_t flags = 0;
+  auto one = [&](int32_t o) -> int32_t {
+    // numpy int64 addition wraps; any wrapped or true sum outside int32 is
+    // rejected by the int32 guard, so the exact test is equivalent
+    const __int128 v = static_cast<__int128>(o) + rs;
+    if (v < INT32_MIN || v > INT32_MAX) flags |= HSZ_ERR_OUTLIER_OVERFLOW;
+    return static_cast<int32_t>(static_cast<int64_t>(v));
+  };
+  const bool vec = ((reinterpret_cast<uintptr_t>(oin) | reinterpret_cast<uintptr_t>(oout)) & 15u) == 0;
+  const uint64_t nv = vec ? nblocks / 4 : 0;
+  for (uint64_t i = tid; i < nv; i += stride) {
+    int4 v = reinterpret_cast<const int4*>(oin)[i];
+    v.x = one(v.x);
+    v.y = one(v.y);
+    v.z = one(v.z);
+    v.w = one(v.w);
+    reinterpret_cast<int4*>(oout)[i] = v;
+  }
+  for (uint64_t i = nv * 4 + tid; i < nblocks; i += stride) oout[i] = one(oin[i]);
+  if (flags) atomicOr(err, flags);
+}
+
+}  // namespace ops
+
+// ---------------------------------------------------------------------------
+// launch helpers
+
+static inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+static inline int launch_status() {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "hsz_b200: CUDA launch failed: %s\n", cudaGetErrorString(e));
+    return HSZ_ECUDA;
+  }
+  return HSZ_OK;
+}
+
+template <typename Kern>
+static inline void allow_smem(Kern kern, int bytes) {
+  static int configured_device = -1;   // one static per kernel instantiation
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (bytes > 48 * 1024 && configured_device != dev) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    configured_device = dev;
+  }
+}
+
+static inline uint64_t grid_for(uint64_t items, uint64_t per_thread, int threads, uint64_t cap) {
+  uint64_t g = ceil_div(ceil_div(items, per_thread), threads);
+  if (g < 1) g = 1;
+  return g < cap ? g : cap;
+}
+
+static inline uint32_t tail_len_of(uint64_t n, uint32_t k) {
+  const uint32_t r = static_cast<uint32_t>(n % k);
+  return r ? r : k;
+}
+
+template <class Src>
+static int launch_encode32(Src src, const k32::EncodeOut& out, uint64_t n, cudaStream_t st) {
+  const uint64_t nb = ceil_div(n, 32);
+  const uint64_t nt = ceil_div(nb, kTileBlocks);
+  constexpr bool kDec = std::is_same<Src, k32::SrcSmul>::value;
+  auto kern = k32::encode_kernel<Src, kDec>;
+  constexpr int smem = k32::EncodeSmem<Src>::kBytes;
+  allow_smem(kern, smem);
+  kern<<<static_cast<unsigned>(nt), k32::kThreads, smem, st>>>(src, out, nb, nt, tail_len_of(n, 32));
+  return launch_status();
+}
+
+template <class G>
+static int launch_encode_generic(G src, uint64_t n, uint32_t k, uint8_t* widths,
+                                 int32_t* outliers, uint8_t* signs, uint64_t sign_cap,
+                                 uint8_t* payload, uint64_t payload_cap, uint64_t* toff,
+                                 uint32_t* err, void* ws, cudaStream_t st) {
+  const uint64_t nb = ceil_div(n, k);
+  const uint64_t nt = ceil_div(nb, kTileBlocks);
+  gen::widths_kernel<G><<<static_cast<unsigned>(ceil_div(nb, gen::kThreads)), gen::kThreads, 0, st>>>(
+      src, n, k, nb, widths, outliers, err);
+  gen::tile_offsets_kernel<<<static_cast<unsigned>(nt), gen::kThreads, 0, st>>>(widths, n, k, nb, nt,
+                                                                               toff, err, ws);
+  gen::pack_kernel<G><<<static_cast<unsigned>(nt), gen::kThreads, 0, st>>>(
+      src, n, k, nb, nt, widths, toff, signs, sign_cap, payload, payload_cap, err);
+  return launch_status();
+}
+
+namespace ops {
+template <typename T>
+__global__ void quantize_kernel(const T* x, uint64_t n, QuantConst c, int64_t* bins, uint32_t* err) {
+  uint32_t flags = 0;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    bins[i] = quantize1(static_cast<double>(x[i]), c, &flags);
+  if (flags) atomicOr(err, flags);
+}
+}  // namespace ops
+
+namespace ops {
+struct SinkAcc {
+  k32::Acc acc;
+  bool want_sq;
+  __device__ __forceinline__ void put(uint64_t, int64_t bin, uint32_t*) { acc.add(bin, want_sq); }
+};
+
+__global__ void __launch_bounds__(gen::kThreads) gen_moments_kernel(gen::GStream s, int want_sq,
+                                                                    uint64_t* out, uint32_t* err,
+                                                                    void* ws) {
+  uint32_t flags = 0;
+  SinkAcc sink;
+  sink.acc.s = 0;
+  sink.acc.q = 0;
+  sink.acc.q2 = 0;
+  sink.want_sq = want_sq != 0;
+  const uint64_t tile = blockIdx.x;
+  gen::decode_one_block(s, tile, tile * gen::kThreads + threadIdx.x, sink, &flags);
+  if (flags) atomicOr(err, flags);
+  k32::finish_moments(sink.acc, gridDim.x, ws, out);
+}
+}  // namespace ops
+
+namespace ops {
+template <class Sink>
+__global__ void dequant_kernel(const int64_t* bins, uint64_t n, Sink sink, uint32_t* err) {
+  uint32_t flags = 0;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    sink.put(i, bins[i], &flags);
+  if (flags) atomicOr(err, flags);
+}
+}  // namespace ops
+
+}  // namespace hsz
+
+using namespace hsz;
+
+// ===========================================================================
+extern "C" {
+
+const char* hsz_version(void) { return "hsz_b200 1.0 sm_100a"; }
+
+uint64_t hsz_tile_count(uint64_t n, uint32_t k) {
+  if (k == 0) return 0;
+  return ceil_div(ceil_div(n, k), kTileBlocks);
+}
+
+uint64_t hsz_sign_bound(uint64_t n, uint32_t k) {
+  if (k == 0) return 0;
+  return ceil_div(n, k) * ((k + 7) / 8);
+}
+
+uint64_t hsz_payload_bound(uint64_t n, uint32_t k) {
+  if (k == 0) return 0;
+  return ceil_div(n, k) * (static_cast<uint64_t>(k) * 8);
+}
+
+uint64_t hsz_workspace_size(uint64_t n, uint32_t k) {
+  const uint64_t nt = hsz_tile_count(n, k) + 1;
+  // header + minmax partials, then flags[nt] and vals[6*nt]
+  return 8 * (kWsFlagsOff + nt + 6 * nt);
+}
+
+int hsz_workspace_init(void* ws, uint64_t ws_bytes, void* stream) {
+  if (!ws) return HSZ_EINVAL;
+  return cudaMemsetAsync(ws, 0, ws_bytes, static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? HSZ_OK
+             : HSZ_ECUDA;
+}
+
+uint64_t hsz_scalar_mul_scratch_size(uint64_t n, uint32_t k) { return k == 32 ? 0 : 8 * n; }
+
+int hsz_minmax(const void* x, int dtype, uint64_t n, double* minmax, uint32_t* err, void* ws,
+               uint64_t ws_bytes, void* stream) {
+  if (!x || !minmax || !err || !ws || n == 0) return HSZ_EINVAL;
+  if (ws_bytes < 8 * kWsFlagsOff) return HSZ_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const unsigned g = static_cast<unsigned>(grid_for(n, dtype == HSZ_F32 ? 16 : 8, ops::kThreads, ops::kMinmaxCtas));
+  if (dtype == HSZ_F32)
+    ops::minmax_kernel<float><<<g, ops::kThreads, 0, st>>>(static_cast<const float*>(x), n, minmax, err, ws);
+  else if (dtype == HSZ_F64)
+    ops::minmax_kernel<double><<<g, ops::kThreads, 0, st>>>(static_cast<const double*>(x), n, minmax, err, ws);
+  else
+    return HSZ_EINVAL;
+  return launch_status();
+}
+
+int hsz_compress(const void* x, int dtype, uint64_t n, uint32_t k, double eps, uint8_t* widths,
+                 int32_t* outliers, uint8_t* signs, uint64_t sign_cap, uint8_t* payload,
+                 uint64_t payload_cap, uint64_t* toff, uint32_t* err, void* ws,
+                 uint64_t ws_bytes, void* stream) {
+  if (!x || !widths || !outliers || !signs || !payload || !toff || !err || !ws || n == 0 || k == 0)
+    return HSZ_EINVAL;
+  if (ws_bytes < hsz_workspace_size(n, k)) return HSZ_EINVAL;
+  if (dtype != HSZ_F32 && dtype != HSZ_F64) return HSZ_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const QuantConst c = make_quant_const(eps);
+  if (k == 32) {
+    const k32::EncodeOut out{widths, outliers, signs, sign_cap, payload, payload_cap, toff, err, ws};
+    if (dtype == HSZ_F32) return launch_encode32(k32::SrcQuant<float>{static_cast<const float*>(x), n, c}, out, n, st);
+    return launch_encode32(k32::SrcQuant<double>{static_cast<const double*>(x), n, c}, out, n, st);
+  }
+  if (dtype == HSZ_F32)
+    return launch_encode_generic(gen::GQuant<float>{static_cast<const float*>(x), c}, n, k, widths, outliers,
+                                 signs, sign_cap, payload, payload_cap, toff, err, ws, st);
+  return launch_encode_generic(gen::GQuant<double>{static_cast<const double*>(x), c}, n, k, widths, outliers,
+                               signs, sign_cap, payload, payload_cap, toff, err, ws, st);
+}
+
+int hsz_encode_bins(const int64_t* bins, uint64_t n, uint32_t k, uint8_t* widths, int32_t* outliers,
+                    uint8_t* signs, uint64_t sign_cap, uint8_t* payload, uint64_t payload_cap,
+                    uint64_t* toff, uint32_t* err, void* ws, uint64_t ws_bytes, void* stream) {
+  if (!bins || !widths || !outliers || !signs || !payload || !toff || !err || !ws || n == 0 || k == 0)
+    return HSZ_EINVAL;
+  if (ws_bytes < hsz_workspace_size(n, k)) return HSZ_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (k == 32) {
+    const k32::EncodeOut out{widths, outliers, signs, sign_cap, payload, payload_cap, toff, err, ws};
+    return launch_encode32(k32::SrcBins{bins, n}, out, n, st);
+  }
+  return launch_encode_generic(gen::GBins{bins}, n, k, widths, outliers, signs, sign_cap, payload,
+                               payload_cap, toff, err, ws, st);
+}
+
+
+int hsz_quantize(const void* x, int dtype, uint64_t n, double eps, int64_t* bins, uint32_t* err,
+                 void* stream) {
+  if (!x || !bins || !err || n == 0) return HSZ_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const QuantConst c = make_quant_const(eps);
+  const unsigned g = static_cast<unsigned>(grid_for(n, 4, 256, 148 * 16));
+  if (dtype == HSZ_F32)
+    ops::quantize_kernel<float><<<g, 256, 0, st>>>(static_cast<const float*>(x), n, c, bins, err);
+  else if (dtype == HSZ_F64)
+    ops::quantize_kernel<double><<<g, 256, 0, st>>>(static_cast<const double*>(x), n, c, bins, err);
+  else
+    return HSZ_EINVAL;
+  return launch_status();
+}
+
+int hsz_dequantize(const int64_t* bins, uint64_t n, double eps, int out_kind, void* out,
+                   uint32_t* err, void* stream) {
+  if (!bins || !out || !err || n == 0) return HSZ_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const unsigned g = static_cast<unsigned>(grid_for(n, 4, 256, 148 * 16));
+  const double d = 2.0 * eps;
+  if (out_kind == HSZ_OUT_F32)
+    ops::dequant_kernel<<<g, 256, 0, st>>>(bins, n, k32::SinkF32{static_cast<float*>(out), d}, err);
+  else if (out_kind == HSZ_OUT_F64)
+    ops::dequant_kernel<<<g, 256, 0, st>>>(bins, n, k32::SinkF64{static_cast<double*>(out), d}, err);
+  else
+    return HSZ_EINVAL;
+  return launch_status();
+}
+
+int hsz_tile_offsets(const uint8_t* widths, uint64_t n, uint32_t k, uint64_t* toff, uint32_t* err,
+                     void* ws, uint64_t ws_bytes, void* stream) {
+  if (!widths || !toff || !err || !ws || n == 0 || k == 0) return HSZ_EINVAL;
+  if (ws_bytes < hsz_workspace_size(n, k)) return HSZ_EINVAL;
+  const uint64_t nb = ceil_div(n, k);
+  const uint64_t nt = ceil_div(nb, kTileBlocks);
+  gen::tile_offsets_kernel<<<static_cast<unsigned>(nt), gen::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      widths, n, k, nb, nt, toff, err, ws);
+  return launch_status();
+}
+
+int hsz_decode(const uint8_t* widths, const int32_t* outliers, const uint8_t* signs,
+               const uint8_t* payload, const uint64_t* toff, uint64_t n, uint32_t k, double eps,
+               int out_kind, void* out, uint32_t* err, void* stream) {
+  if (!widths || !outliers || !signs || !payload || !toff || !out || !err || n == 0 || k == 0)
+    return HSZ_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t nb = ceil_div(n, k);
+  const uint64_t nt = ceil_div(nb, kTileBlocks);
+  const double d = 2.0 * eps;
+  if (k == 32) {
+    const k32::StreamIn s{widths, outliers, signs, payload, toff, n, nb, tail_len_of(n, 32)};
+    constexpr int smem = k32::TileIn::kBytes;
+    switch (out_kind) {
+      case HSZ_OUT_F32:
+        k32::decode_kernel<k32::SinkF32><<<static_cast<unsigned>(nt), k32::kThreads, smem, st>>>(
+            s, k32::SinkF32{static_cast<float*>(out), d}, err);
+        break;
+      case HSZ_OUT_F64:
+        k32::decode_kernel<k32::SinkF64><<<static_cast<unsigned>(nt), k32::kThreads, smem, st>>>(
+            s, k32::SinkF64{static_cast<double*>(out), d}, err);
+        break;
+      case HSZ_OUT_BINS:
+        k32::decode_kernel<k32::SinkBins><<<static_cast<unsigned>(nt), k32::kThreads, smem, st>>>(
+            s, k32::SinkBins{static_cast<int64_t*>(out)}, err);
+        break;
+      default:
+        return HSZ_EINVAL;
+    }
+    return launch_status();
+  }
+  const gen::GStream s{widths, outliers, signs, payload, toff, n, k, nb};
+  switch (out_kind) {
+    case HSZ_OUT_F32:
+      gen::decode_kernel<k32::SinkF32><<<static_cast<unsigned>(nt), gen::kThreads, 0, st>>>(
+          s, k32::SinkF32{static_cast<float*>(out), d}, err);
+      break;
+    case HSZ_OUT_F64:
+      gen::decode_kernel<k32::SinkF64><<<static_cast<unsigned>(nt), gen::kThreads, 0, st>>>(
+          s, k32::SinkF64{static_cast<double*>(out), d}, err);
+      break;
+    case HSZ_OUT_BINS:
+      gen::decode_kernel<k32::SinkBins><<<static_cast<unsigned>(nt), gen::kThreads, 0, st>>>(
+          s, k32::SinkBins{static_cast<int64_t*>(out)}, err);
+      break;
+    default:
+      return HSZ_EINVAL;
+  }
+  return launch_status();
+}
+
+int hsz_negate(const uint8_t* widths, const int32_t* oin, int32_t* oout, const uint8_t* sin,
+               uint8_t* sout, const uint64_t* toff, uint64_t n, uint32_t k, uint32_t* err,
+               void* stream) {
+  if (!widths || !oin || !oout || !sin || !sout || !toff || !err || n == 0 || k == 0) return HSZ_EINVAL;
+  const uint64_t nb = ceil_div(n, k);
+  const uint64_t nt = ceil_div(nb, kTileBlocks);
+  const uint64_t sign_bound = hsz_sign_bound(n, k);
+  const uint64_t items = (sign_bound / 16 > nb) ? sign_bound / 16 : nb;
+  const unsigned g = static_cast<unsigned>(grid_for(items, 2, ops::kThreads, 148 * 16));
+  ops::negate_kernel<<<g, ops::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      widths, oin, oout, sin, sout, toff, nt, n, k, nb, err);
+  return launch_status();
+}
+
+int hsz_scalar_add(const int32_t* oin, int32_t* oout, uint64_t nblocks, int64_t rs, uint32_t* err,
+                   void* stream) {
+  if (!oin || !oout || !err || nblocks == 0) return HSZ_EINVAL;
+  const unsigned g = static_cast<unsigned>(grid_for(nblocks, 8, ops::kThreads, 148 * 16));
+  ops::sadd_kernel<<<g, ops::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(oin, oout, nblocks, rs, err);
+  return launch_status();
+}
+
+int hsz_scalar_mul(const uint8_t* widths, const int32_t* outliers, const uint8_t* signs,
+                   const uint8_t* payload, const uint64_t* toff, uint64_t n, uint32_t k, double eps,
+                   int64_t rs, uint8_t* ow, int32_t* oo, uint8_t* os, uint64_t sign_cap, uint8_t* op,
+                   uint64_t payload_cap, uint64_t* otoff, void* scratch, uint32_t* err, void* ws,
+                   uint64_t ws_bytes, void* stream) {
+  if (!widths || !outliers || !signs || !payload || !toff || !ow || !oo || !os || !op || !otoff ||
+      !err || !ws || n == 0 || k == 0)
+    return HSZ_EINVAL;
+  if (ws_bytes < hsz_workspace_size(n, k)) return HSZ_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t nb = ceil_div(n, k);
+  const uint64_t nt = ceil_div(nb, kTileBlocks);
+  const double d = 2.0 * eps;
+  if (k == 32) {
+    k32::SrcSmul src;
+    src.in = k32::StreamIn{widths, outliers, signs, payload, toff, n, nb, tail_len_of(n, 32)};
+    src.rs = rs;
+    src.d = d;
+    const k32::EncodeOut out{ow, oo, os, sign_cap, op, payload_cap, otoff, err, ws};
+    return launch_encode32(src, out, n, st);
+  }
+  if (!scratch) return HSZ_EINVAL;
+  int64_t* bins = static_cast<int64_t*>(scratch);
+  const gen::GStream s{widths, outliers, signs, payload, toff, n, k, nb};
+  gen::decode_kernel<gen::SinkSmul><<<static_cast<unsigned>(nt), gen::kThreads, 0, st>>>(
+      s, gen::SinkSmul{bins, rs, d}, err);
+  return launch_encode_generic(gen::GBins{bins}, n, k, ow, oo, os, sign_cap, op, payload_cap, otoff,
+                               err, ws, st);
+}
+
+int hsz_moments(const uint8_t* widths, const int32_t* outliers, const uint8_t* signs,
+                const uint8_t* payload, const uint64_t* toff, uint64_t n, uint32_t k, int want_sq,
+                uint64_t* out, uint32_t* err, void* ws, uint64_t ws_bytes, void* stream) {
+  if (!widths || !outliers || !signs || !payload || !toff || !out || !err || !ws || n == 0 || k == 0)
+    return HSZ_EINVAL;
+  if (ws_bytes < hsz_workspace_size(n, k)) return HSZ_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t nb = ceil_div(n, k);
+  const uint64_t nt = ceil_div(nb, kTileBlocks);
+  if (k == 32) {
+    const k32::StreamIn s{widths, outliers, signs, payload, toff, n, nb, tail_len_of(n, 32)};
+    constexpr int smem = k32::TileIn::kBytes;
+    if (want_sq)
+      k32::moments_kernel<true><<<static_cast<unsigned>(nt), k32::kThreads, smem, st>>>(s, out, err, ws);
+    else
+      k32::moments_kernel<false><<<static_cast<unsigned>(nt), k32::kThreads, smem, st>>>(s, out, err, ws);
+    return launch_status();
+  }
+  const gen::GStream s{widths, outliers, signs, payload, toff, n, k, nb};
+  ops::gen_moments_kernel<<<static_cast<unsigned>(nt), gen::kThreads, 0, st>>>(s, want_sq, out, err, ws);
+  return launch_status();
+}
+
+}  // extern "C"

@@ -1,0 +1,251 @@
+// Shared device helpers for the HoSZp B200 hot path (sm_100a).
+//
+// * error word bits (HSZ_ERR_*, same values as include/hsz_b200.h)
+// * big-endian / bit-reversal helpers for the MSB-first sign planes and
+//   element-major payload fields of pkg/FORMAT.md:24-37
+// * TMA bulk copy (cp.async.bulk) + mbarrier wrappers
+// * the single-pass decoupled look-back used to place variable-length
+//   blocks (sign planes, payload) at their global byte offsets
+#pragma once
+
+#include <cstdint>
+#include <type_traits>
+#include <cuda_runtime.h>
+
+#include "../../include/hsz_b200.h"
+
+namespace hsz {
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+// Tile geometry shared by every kernel and by the tile-offset cache of a
+// device stream: a tile is kTileBlocks consecutive blocks.
+constexpr int kTileBlocks = HSZ_TILE_BLOCKS;   // 128
+constexpr int kCtaWarps = 8;                    // 256-thread CTAs
+constexpr int kBlocksPerWarp = kTileBlocks / kCtaWarps;  // 16
+
+static_assert(kTileBlocks % kCtaWarps == 0, "tile must split evenly over warps");
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
+
+__device__ __forceinline__ void set_err(uint32_t* err, uint32_t bits) {
+  if (bits) atomicOr(err, bits);
+}
+
+// ---------------------------------------------------------------------------
+// shared-memory addresses, mbarrier and bulk async copy (TMA engine)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// global -> shared bulk copy; dst/src 16-byte aligned, bytes % 16 == 0
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// gpu-scope acquire / release accesses for the look-back protocol
+
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t atom_add_acq_rel(uint64_t* p, uint64_t v) {
+  uint64_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v)
+               : "memory");
+  return old;
+}
+
+// Workspace layout (u64 words; see hsz_workspace_size):
+//   [0]      ticket          [1] epoch       [2] moments done-counter
+//   [3]      minmax done-counter             [4..64) reserved
+//   [64 .. 64 + 2*kMinmaxCtasMax)            minmax per-CTA partials
+//   flags[ntiles]   at kWsFlagsOff            (epoch << 2 | state)
+//   vals[ntiles][6] right after the flags     (agg_sign, agg_pay, inc_sign,
+//                                              inc_pay | moments partials)
+constexpr uint64_t kMinmaxCtasMax = 148 * 4;
+constexpr uint64_t kWsMinmaxOff = 64;
+constexpr uint64_t kWsFlagsOff = kWsMinmaxOff + 2 * kMinmaxCtasMax;
+
+struct LookbackWs {
+  uint64_t* ticket;
+  uint64_t* epoch;
+  uint64_t* flags;
+  uint64_t* vals;
+  __device__ static LookbackWs bind(void* ws, uint64_t ntiles) {
+    LookbackWs w;
+    uint64_t* base = static_cast<uint64_t*>(ws);
+    w.ticket = base;
+    w.epoch = base + 1;
+    w.flags = base + kWsFlagsOff;
+    w.vals = base + kWsFlagsOff + ntiles;
+    return w;
+  }
+};
+
+constexpr uint64_t kStAgg = 1, kStInc = 2;
+
+// Called by thread 0: draw the launch epoch and a tile ticket (tickets are
+// handed out in order, so every predecessor of a tile is resident or done,
+// which makes the spin in lookback() deadlock-free).  The CTA drawing the
+// last ticket rearms the counter and advances the epoch for the next launch.
+__device__ __forceinline__ void draw_ticket(LookbackWs& w, uint64_t ntiles, uint64_t* tile,
+                                            uint64_t* epoch) {
+  uint64_t e = ld_acquire(w.epoch);
+  uint64_t t = atom_add_acq_rel(w.ticket, 1);
+  if (t == ntiles - 1) {
+    st_relaxed(w.ticket, 0);
+    st_release(w.epoch, e + 1);
+  }
+  *tile = t;
+  *epoch = e;
+}
+
+// Decoupled look-back over (sign bytes, payload bytes), executed by one
+// full warp.  Publishes the tile's aggregate, sums predecessors (32 at a
+// time) until an inclusive prefix is found, then publishes the inclusive
+// prefix.  Returns the exclusive prefix of this tile.
+__device__ __forceinline__ void lookback(LookbackWs& w, uint64_t tile, uint64_t epoch,
+                                         uint64_t agg_s, uint64_t agg_p, uint64_t* excl_s,
+                                         uint64_t* excl_p) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t tag = epoch << 2;
+  if (tile == 0) {
+    if (lane == 0) {
+      w.vals[2] = agg_s;   // inclusive slots of tile 0
+      w.vals[3] = agg_p;
+      st_release(&w.flags[0], tag | kStInc);
+    }
+    *excl_s = 0;
+    *excl_p = 0;
+    return;
+  }
+  if (lane == 0) {
+    w.vals[tile * 4 + 0] = agg_s;
+    w.vals[tile * 4 + 1] = agg_p;
+    st_release(&w.flags[tile], tag | kStAgg);
+  }
+  uint64_t sum_s = 0, sum_p = 0;
+  int64_t base = static_cast<int64_t>(tile) - 1;
+  while (true) {
+    const int64_t idx = base - lane;
+    uint64_t st = kStInc;       // virtual inclusive zero before tile 0
+    if (idx >= 0) {
+      const uint64_t f = ld_acquire(&w.flags[idx]);
+      st = ((f >> 2) == epoch) ? (f & 3) : 0;
+    }
+    const unsigned inv = __ballot_sync(kFull, st == 0);
+    const unsigned inc = __ballot_sync(kFull, st == kStInc);
+    const int first = inc ? (__ffs(inc) - 1) : 32;
+    const unsigned below = (first >= 32) ? kFull : ((1u << first) - 1u) | (1u << first);
+    if (inv & below) {          // a needed predecessor has not published yet
+      __nanosleep(32);
+      continue;
+    }
+    uint64_t vs = 0, vp = 0;
+    if (idx >= 0) {
+      if (lane < first) {
+        vs = ld_relaxed(&w.vals[idx * 4 + 0]);
+        vp = ld_relaxed(&w.vals[idx * 4 + 1]);
+      } else if (lane == first) {
+        vs = ld_relaxed(&w.vals[idx * 4 + 2]);
+        vp = ld_relaxed(&w.vals[idx * 4 + 3]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      vs += __shfl_xor_sync(kFull, vs, o);
+      vp += __shfl_xor_sync(kFull, vp, o);
+    }
+    sum_s += vs;
+    sum_p += vp;
+    if (first < 32) break;
+    base -= 32;
+  }
+  if (lane == 0) {
+    w.vals[tile * 4 + 2] = sum_s + agg_s;
+    w.vals[tile * 4 + 3] = sum_p + agg_p;
+    st_release(&w.flags[tile], tag | kStInc);
+  }
+  *excl_s = sum_s;
+  *excl_p = sum_p;
+}
+
+// ---------------------------------------------------------------------------
+// exact integer helpers
+
+// 64-bit signed difference a - b as (magnitude, negative) -- exact for any
+// pair with |a|,|b| <= 2^63 - 1 (magnitude < 2^64).
+__device__ __forceinline__ uint64_t absdiff64(int64_t a, int64_t b, bool* neg) {
+  *neg = a < b;
+  return a >= b ? static_cast<uint64_t>(a) - static_cast<uint64_t>(b)
+                : static_cast<uint64_t>(b) - static_cast<uint64_t>(a);
+}
+
+// Round-to-nearest-even conversion of a signed 128-bit integer to double
+// (what numpy / CPython do for the exact product p = bin * rs).
+__device__ __forceinline__ double i128_to_double_rn(__int128 v) {
+  const bool neg = v < 0;
+  unsigned __int128 m = neg ? (unsigned __int128)(-(v + 1)) + 1u : (unsigned __int128)v;
+  const uint64_t hi = static_cast<uint64_t>(m >> 64);
+  double r;
+  if (hi == 0) {
+    r = __ull2double_rn(static_cast<uint64_t>(m));
+  } else {
+    const int lz = __clzll(hi);            // 0..63
+    const int sh = 64 - lz;                // bits to drop so the value fits 64 bits
+    const uint64_t top = static_cast<uint64_t>(m >> sh);
+    const bool sticky = (m & ((((unsigned __int128)1) << sh) - 1u)) != 0;
+    // the sticky bit sits far below the rounding position of a 53-bit
+    // mantissa, so RN of (top | sticky) equals RN of the full value
+    r = ldexp(__ull2double_rn(top | (sticky ? 1u : 0u)), sh);
+  }
+  return neg ? -r : r;
+}
+
+}  // namespace hsz

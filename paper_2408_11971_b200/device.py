@@ -1,0 +1,292 @@
+"""Device-resident stream and the per-CUDA-stream execution context.
+
+:class:`DeviceStream` is the HBM twin of :class:`model.CompressedStream`:
+the four FORMAT.md sections live in device buffers (torch tensors used as
+plain allocations) plus a cached tile-offset table (the exclusive byte
+offsets of every HSZ_TILE_BLOCKS-block tile, written for free by the
+encoders' look-back).  Operations on DeviceStreams are asynchronous on the
+current CUDA stream; failures are accumulated in a sticky device error word
+that is checked (and raised as the reference's exception class) whenever a
+result is materialised on the host (``to_host()``, a reduction's float,
+``check()``).
+
+Memory layout in HBM per stream (N elements, B blocks, T tiles):
+  widths u8[B] | outliers i32[B] | signs u8[cap_s + 16] | payload u8[cap_p + 16]
+  | tile offsets u64[2(T+1)]
+negate / scalar_add share the untouched sections (widths, payload, tile
+offsets; and signs for scalar_add) with their input, exactly like the
+reference shares the numpy arrays / bytes objects (ops.py:106-118).
+"""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+
+from . import _native as N
+from .errors import CapacityExceeded, raise_for_flags
+from .model import CompressedStream, QuantParams
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+
+        _torch = t
+    return _torch
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise RuntimeError("paper_2408_11971_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    return t
+
+
+def ptr(t) -> int:
+    return int(t.data_ptr())
+
+
+DTYPE_CODE = {"f32": N.HSZ_F32, "f64": N.HSZ_F64}
+
+# payload capacity policy: the exact worst case (8 bytes/element) when it is
+# affordable, else 4 bytes/element with an exact-size retry on overflow
+_PAYLOAD_BOUND_LIMIT = 16 << 30
+
+
+class Context:
+    """Workspace, error word and scratch for one (device, CUDA stream)."""
+
+    def __init__(self, device_index: int, stream):
+        t = require_cuda()
+        self.lib = N.load()
+        self.device = t.device("cuda", device_index)
+        self.stream = stream
+        self.handle = int(stream.cuda_stream)
+        self.ws = None
+        self.ws_bytes = 0
+        with t.cuda.device(self.device):
+            self.err = t.zeros(4, dtype=t.int32, device=self.device)
+        self.err_ptr = ptr(self.err)
+
+    def workspace(self, n: int, k: int):
+        need = int(self.lib.hsz_workspace_size(n, k))
+        if need > self.ws_bytes:
+            t = torch()
+            need = max(need, 2 * self.ws_bytes)
+            self.ws = t.empty(need, dtype=t.uint8, device=self.device)
+            N.check(self.lib.hsz_workspace_init(ptr(self.ws), need, self.handle), "workspace init")
+            self.ws_bytes = need
+        return ptr(self.ws), self.ws_bytes
+
+    def synchronize(self):
+        self.stream.synchronize()
+
+    def read_flags(self) -> int:
+        """Synchronize, read and clear the sticky error word."""
+        self.stream.synchronize()
+        v = int(self.err[0].item())
+        if v:
+            self.err.zero_()
+            self.stream.synchronize()
+        return v
+
+    def check(self, what: str = "") -> None:
+        raise_for_flags(self.read_flags(), what)
+
+    def empty(self, n, dtype):
+        t = torch()
+        return t.empty(int(n), dtype=dtype, device=self.device)
+
+
+_CTX = {}
+_CTX_LOCK = threading.Lock()
+
+
+def context(device=None) -> Context:
+    """Context of the current CUDA stream on ``device`` (default: current)."""
+    t = require_cuda()
+    if device is None:
+        idx = t.cuda.current_device()
+    else:
+        idx = t.device(device).index
+        if idx is None:
+            idx = t.cuda.current_device()
+    stream = t.cuda.current_stream(idx)
+    key = (idx, int(stream.cuda_stream))
+    with _CTX_LOCK:
+        ctx = _CTX.get(key)
+        if ctx is None:
+            ctx = Context(idx, stream)
+            _CTX[key] = ctx
+    return ctx
+
+
+def payload_capacity(lib, n: int, k: int) -> int:
+    bound = int(lib.hsz_payload_bound(n, k))
+    if bound <= _PAYLOAD_BOUND_LIMIT:
+        return bound
+    return max(4 * n, 1 << 20)
+
+
+class DeviceStream:
+    """A compressed stream resident in HBM (see module docstring)."""
+
+    __slots__ = ("params", "widths", "outliers", "signs", "payload", "toff", "ctx",
+                 "sign_cap", "payload_cap", "_totals")
+
+    def __init__(self, params: QuantParams, widths, outliers, signs, payload, toff, ctx: Context,
+                 sign_cap: int, payload_cap: int):
+        self.params = params
+        self.widths = widths
+        self.outliers = outliers
+        self.signs = signs
+        self.payload = payload
+        self.toff = toff
+        self.ctx = ctx
+        self.sign_cap = int(sign_cap)
+        self.payload_cap = int(payload_cap)
+        self._totals = None
+
+    # -- geometry ---------------------------------------------------------
+    @property
+    def n(self) -> int:
+        return self.params.element_count
+
+    @property
+    def k(self) -> int:
+        return self.params.block_len
+
+    @property
+    def ntiles(self) -> int:
+        return int(self.ctx.lib.hsz_tile_count(self.n, self.k))
+
+    def pointers(self):
+        return (ptr(self.widths), ptr(self.outliers), ptr(self.signs), ptr(self.payload),
+                ptr(self.toff))
+
+    # -- host materialisation ------------------------------------------------
+    def check(self) -> "DeviceStream":
+        """Synchronize and raise any pending device error."""
+        self.ctx.check()
+        return self
+
+    def totals(self):
+        """(sign bytes, payload bytes) -- synchronizes."""
+        if self._totals is None:
+            self.ctx.check()
+            T = self.ntiles
+            tt = self.toff[2 * T:2 * T + 2].cpu().numpy().view(np.uint64)
+            self._totals = (int(tt[0]), int(tt[1]))
+        return self._totals
+
+    @property
+    def serialized_size(self) -> int:
+        s, p = self.totals()
+        from .model import HEADER
+        return HEADER.size + 8 * len(self.params.dims) + 5 * self.params.block_count + s + p
+
+    @property
+    def compression_ratio(self) -> float:
+        return self.params.raw_nbytes / self.serialized_size
+
+    def to_host(self) -> CompressedStream:
+        self.ctx.check()
+        s, p = self.totals()
+        w = self.widths.cpu().numpy()
+        o = self.outliers.cpu().numpy()
+        sg = self.signs[:s].cpu().numpy().tobytes()
+        py = self.payload[:p].cpu().numpy().tobytes()
+        return CompressedStream(self.params, w, o, sg, py)
+
+    @classmethod
+    def from_host(cls, cs: CompressedStream, ctx: Context = None) -> "DeviceStream":
+        """Upload a host stream and rebuild its tile-offset cache on device."""
+        t = require_cuda()
+        ctx = ctx or context()
+        p = cs.params
+        n, k = p.element_count, p.block_len
+        lib = ctx.lib
+        dev = ctx.device
+
+        def up(arr_u8, extra=0):
+            host = t.from_numpy(np.frombuffer(arr_u8, dtype=np.uint8).copy())
+            out = t.empty(host.numel() + extra, dtype=t.uint8, device=dev)
+            if host.numel():
+                out[:host.numel()].copy_(host, non_blocking=False)
+            return out
+
+        widths = up(cs.widths.tobytes())
+        outliers = up(cs.outliers.astype("<i4").tobytes()).view(t.int32)
+        signs = up(cs.sign_planes, N.HSZ_SECTION_SLACK)
+        payload = up(cs.payload, N.HSZ_SECTION_SLACK)
+        T = int(lib.hsz_tile_count(n, k))
+        toff = t.empty(2 * (T + 1), dtype=t.int64, device=dev)
+        wsp, wsb = ctx.workspace(n, k)
+        N.check(lib.hsz_tile_offsets(ptr(widths), n, k, ptr(toff), ctx.err_ptr, wsp, wsb,
+                                     ctx.handle), "hsz_tile_offsets")
+        ds = cls(p, widths, outliers, signs, payload, toff, ctx, len(cs.sign_planes),
+                 len(cs.payload))
+        ds._totals = (len(cs.sign_planes), len(cs.payload))
+        return ds
+
+    def __eq__(self, other):
+        if isinstance(other, DeviceStream):
+            other = other.to_host()
+        if not isinstance(other, CompressedStream):
+            return NotImplemented
+        return self.to_host() == other
+
+    __hash__ = None
+
+    def __repr__(self):
+        return f"DeviceStream({self.params}, device={self.ctx.device})"
+
+
+def new_stream_buffers(ctx: Context, params: QuantParams, payload_cap: int = None):
+    """Allocate output sections for an encoder writing `params`-shaped data."""
+    t = torch()
+    n, k = params.element_count, params.block_len
+    lib = ctx.lib
+    B = params.block_count
+    T = int(lib.hsz_tile_count(n, k))
+    scap = int(lib.hsz_sign_bound(n, k))
+    pcap = payload_capacity(lib, n, k) if payload_cap is None else int(payload_cap)
+    widths = ctx.empty(B, t.uint8)
+    outliers = ctx.empty(B, t.int32)
+    signs = ctx.empty(scap + N.HSZ_SECTION_SLACK, t.uint8)
+    payload = ctx.empty(pcap + N.HSZ_SECTION_SLACK, t.uint8)
+    toff = ctx.empty(2 * (T + 1), t.int64)
+    return widths, outliers, signs, payload, toff, scap, pcap
+
+
+def run_encoder(ctx: Context, params: QuantParams, launch) -> DeviceStream:
+    """Run an encoder launch(widths, outliers, signs, scap, payload, pcap, toff);
+    retry once with the exact payload size if the capacity policy undershot."""
+    lib = ctx.lib
+    n, k = params.element_count, params.block_len
+    w, o, s, p, toff, scap, pcap = new_stream_buffers(ctx, params)
+    launch(w, o, s, scap, p, pcap, toff)
+    ds = DeviceStream(params, w, o, s, p, toff, ctx, scap, pcap)
+    if pcap >= int(lib.hsz_payload_bound(n, k)):
+        return ds                       # overflow impossible: stay asynchronous
+    flags = ctx.read_flags()
+    if flags & ~(1 << 6):
+        raise_for_flags(flags & ~(1 << 6))
+    if flags & (1 << 6):
+        T = int(lib.hsz_tile_count(n, k))
+        need = int(toff[2 * T + 1].item())
+        w, o, s, p, toff, scap, pcap = new_stream_buffers(ctx, params, payload_cap=need)
+        launch(w, o, s, scap, p, pcap, toff)
+        ds = DeviceStream(params, w, o, s, p, toff, ctx, scap, pcap)
+        flags = ctx.read_flags()
+        if flags:
+            if flags & (1 << 6):
+                raise CapacityExceeded("payload capacity retry failed")
+            raise_for_flags(flags)
+    return ds

@@ -1,0 +1,257 @@
+"""Homomorphic operations -- drop-in for the reference's ``hoszp.ops`` hot path.
+
+==================  =====================  =================================
+this module         reference              CUDA entry point
+==================  =====================  =================================
+ScalarBin           ops.py:51-74           (host: exact Python float/int)
+negate              ops.py:88-109          hsz_negate
+scalar_add / _sub   ops.py:112-125         hsz_scalar_add
+scalar_mul          ops.py:199-225         hsz_scalar_mul (fused decode/encode)
+mean                ops.py:360-363         hsz_moments + host finalize
+variance / stddev   ops.py:382-397         hsz_moments(want_sq) + finalize
+apply_stream_op     ops.py:520-538         dispatch
+apply_reduction     ops.py:541-552         dispatch
+==================  =====================  =================================
+
+Reductions are exact: the kernel returns S = sum(bins) (int128) and
+Q = sum(bins^2) (uint192) and the final float64 arithmetic is the
+reference's own Python expression on Python ints, so mean / variance are
+bit-identical to the reference, not merely within tolerance.
+
+The bivariate operations of the reference (elementwise add/sub, hadamard,
+covariance, ssim) are not on this hot path; the dispatch
+tables keep their names and report them as not implemented here.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .codec import _as_device_stream
+from .device import DeviceStream, ptr, run_encoder, torch
+from .errors import QuantOverflow
+from .model import CompressedStream
+
+_I64_MAX = 2 ** 63 - 1
+
+#: stream-returning operations: name -> (operand streams, takes a scalar)  (ops.py:37-45)
+STREAM_OPS = {
+    "neg": (1, False),
+    "sadd": (1, True),
+    "ssub": (1, True),
+    "smul": (1, True),
+    "eadd": (2, False),
+    "esub": (2, False),
+    "hadamard": (2, False),
+}
+
+#: scalar-returning reductions: name -> operand streams  (ops.py:48)
+REDUCTIONS = {"mean": 1, "variance": 1, "stddev": 1, "covariance": 2, "ssim": 2}
+
+#: the subset implemented by this B200 hot path
+HOT_STREAM_OPS = ("neg", "sadd", "ssub", "smul")
+HOT_REDUCTIONS = ("mean", "variance", "stddev")
+
+
+@dataclass(frozen=True)
+class ScalarBin:
+    """A scalar on a stream's bin grid: ``trunc(s / 2eps)`` toward zero
+    (reference: ops.py:51-74)."""
+
+    value: float
+    eps: float
+    bin: int
+
+    @classmethod
+    def of(cls, value: float, eps: float) -> "ScalarBin":
+        q = float(value) / (2.0 * eps)
+        if not math.isfinite(q) or abs(q) >= 2.0 ** 63:
+            raise QuantOverflow(f"scalar {value} overflows the bin grid at eps={eps}")
+        return cls(float(value), float(eps), math.trunc(q))
+
+    @property
+    def quantized_value(self) -> float:
+        return 2.0 * self.eps * self.bin
+
+
+def _finish(stream, ds: DeviceStream, what: str):
+    if isinstance(stream, DeviceStream):
+        return ds
+    return ds.to_host()
+
+
+# ---------------------------------------------------------------------------
+# fully-compressed-space operations
+
+def negate(c):
+    """Flip every stored sign bit, negate every outlier; widths, payload and
+    the tile-offset cache are shared with the input (ops.py:102-109)."""
+    ds = _as_device_stream(c)
+    ctx = ds.ctx
+    t = torch()
+    outl = ctx.empty(ds.outliers.numel(), t.int32)
+    signs = ctx.empty(ds.signs.numel(), t.uint8)
+    p = ds.params
+    N.check(ctx.lib.hsz_negate(ptr(ds.widths), ptr(ds.outliers), ptr(outl), ptr(ds.signs),
+                               ptr(signs), ptr(ds.toff), p.element_count, p.block_len,
+                               ctx.err_ptr, ctx.handle), "hsz_negate")
+    out = DeviceStream(p, ds.widths, outl, signs, ds.payload, ds.toff, ctx, ds.sign_cap,
+                       ds.payload_cap)
+    out._totals = ds._totals
+    return _finish(c, out, "negate")
+
+
+def _shift_outliers(c, rs: int, what: str):
+    ds = _as_device_stream(c)
+    ctx = ds.ctx
+    t = torch()
+    outl = ctx.empty(ds.outliers.numel(), t.int32)
+    N.check(ctx.lib.hsz_scalar_add(ptr(ds.outliers), ptr(outl), ds.params.block_count, rs,
+                                   ctx.err_ptr, ctx.handle), "hsz_scalar_add")
+    out = DeviceStream(ds.params, ds.widths, outl, ds.signs, ds.payload, ds.toff, ctx,
+                       ds.sign_cap, ds.payload_cap)
+    out._totals = ds._totals
+    return _finish(c, out, what)
+
+
+def scalar_add(c, s: float):
+    """Shift every outlier by the scalar's bin (ops.py:112-118)."""
+    eps = c.params.eps
+    return _shift_outliers(c, ScalarBin.of(s, eps).bin, "scalar_add")
+
+
+def scalar_sub(c, s: float):
+    """ops.py:121-125."""
+    eps = c.params.eps
+    return _shift_outliers(c, -ScalarBin.of(s, eps).bin, "scalar_sub")
+
+
+# ---------------------------------------------------------------------------
+# quantized-space operations
+
+def scalar_mul(c, s: float, threads: int = 1):
+    """bins * rs, re-centred with nearest-ties-away rounding, re-encoded --
+    one fused single-pass kernel for block_len 32 (ops.py:211-225)."""
+    p = c.params
+    rs = ScalarBin.of(s, p.eps).bin
+    ds = _as_device_stream(c)
+    ctx = ds.ctx
+    lib = ctx.lib
+    n, k = p.element_count, p.block_len
+    wsp, wsb = ctx.workspace(n, k)
+    scratch_bytes = int(lib.hsz_scalar_mul_scratch_size(n, k))
+    scratch = ctx.empty(scratch_bytes, torch().uint8) if scratch_bytes else None
+    sp = ptr(scratch) if scratch is not None else None
+    w, o, sg, py, toff = ds.pointers()
+
+    def launch(ow, oo, os_, scap, op, pcap, otoff):
+        N.check(lib.hsz_scalar_mul(w, o, sg, py, toff, n, k, p.eps, rs, ptr(ow), ptr(oo),
+                                   ptr(os_), scap, ptr(op), pcap, ptr(otoff), sp, ctx.err_ptr,
+                                   wsp, wsb, ctx.handle), "hsz_scalar_mul")
+
+    out = run_encoder(ctx, p, launch)
+    return _finish(c, out, "scalar_mul")
+
+
+# ---------------------------------------------------------------------------
+# reductions
+
+def moments_device(ds: DeviceStream, want_sq: bool):
+    """Launch the exact-moment kernel; returns the device u64[5] result."""
+    ctx = ds.ctx
+    p = ds.params
+    n, k = p.element_count, p.block_len
+    wsp, wsb = ctx.workspace(n, k)
+    out = ctx.empty(5, torch().int64)
+    w, o, sg, py, toff = ds.pointers()
+    N.check(ctx.lib.hsz_moments(w, o, sg, py, toff, n, k, 1 if want_sq else 0, ptr(out),
+                                ctx.err_ptr, wsp, wsb, ctx.handle), "hsz_moments")
+    return out
+
+
+def unpack_moments(limbs) -> tuple:
+    """u64[5] -> (S: signed 128-bit, Q: unsigned 192-bit) as Python ints."""
+    v = [int(x) for x in np.asarray(limbs).view(np.uint64)]
+    S = v[0] | (v[1] << 64)
+    if S >= 1 << 127:
+        S -= 1 << 128
+    Q = v[2] | (v[3] << 64) | (v[4] << 128)
+    return S, Q
+
+
+def exact_moments(c, want_sq: bool = True):
+    """Exact (sum(bins), sum(bins^2)) of a stream (ops.py:313-357)."""
+    ds = _as_device_stream(c)
+    out = moments_device(ds, want_sq)
+    ds.ctx.check("moments")
+    return unpack_moments(out.cpu().numpy())
+
+
+def mean_from(S: int, n: int, eps: float) -> float:
+    """ops.py:363, evaluated with the reference's Python operators."""
+    return (2.0 * eps * S) / n
+
+
+def variance_from(S: int, Q: int, n: int, eps: float) -> float:
+    """ops.py:386 and 393."""
+    spread = float(n * Q - S * S) / (n * n)
+    return (2.0 * eps) ** 2 * spread
+
+
+def mean(c, *, shortcut: bool = True, threads: int = 1) -> float:
+    S, _ = exact_moments(c, want_sq=False)
+    return mean_from(S, c.params.element_count, c.params.eps)
+
+
+def variance(c, *, shortcut: bool = True, threads: int = 1) -> float:
+    S, Q = exact_moments(c, want_sq=True)
+    return variance_from(S, Q, c.params.element_count, c.params.eps)
+
+
+def stddev(c, *, shortcut: bool = True, threads: int = 1) -> float:
+    return math.sqrt(variance(c, shortcut=shortcut, threads=threads))
+
+
+# ---------------------------------------------------------------------------
+# dispatch (ops.py:520-552)
+
+def apply_stream_op(name: str, streams, scalar=None, threads: int = 1):
+    arity, needs_scalar = STREAM_OPS[name]
+    if len(streams) != arity:
+        raise ValueError(f"{name} takes {arity} stream operand(s), got {len(streams)}")
+    if needs_scalar and scalar is None:
+        raise ValueError(f"{name} needs a scalar operand")
+    if name == "neg":
+        return negate(streams[0])
+    if name == "sadd":
+        return scalar_add(streams[0], scalar)
+    if name == "ssub":
+        return scalar_sub(streams[0], scalar)
+    if name == "smul":
+        return scalar_mul(streams[0], scalar, threads)
+    raise NotImplementedError(f"stream op {name!r} is outside the B200 hot path "
+                              f"(implemented: {', '.join(HOT_STREAM_OPS)})")
+
+
+def apply_reduction(name: str, streams, threads: int = 1) -> float:
+    if len(streams) != REDUCTIONS[name]:
+        raise ValueError(f"{name} takes {REDUCTIONS[name]} stream operand(s)")
+    if name == "mean":
+        return mean(streams[0], threads=threads)
+    if name == "variance":
+        return variance(streams[0], threads=threads)
+    if name == "stddev":
+        return stddev(streams[0], threads=threads)
+    raise NotImplementedError(f"reduction {name!r} is outside the B200 hot path "
+                              f"(implemented: {', '.join(HOT_REDUCTIONS)})")
+
+
+__all__ = [
+    "STREAM_OPS", "REDUCTIONS", "ScalarBin", "negate", "scalar_add", "scalar_sub", "scalar_mul",
+    "mean", "variance", "stddev", "exact_moments", "apply_stream_op", "apply_reduction",
+    "CompressedStream",
+]
