@@ -1,0 +1,547 @@
+"""Benchmark of the HoSZp hot path on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2|4]
+    python bench.py --impl reference ...       # CPU oracle arm (rank 0 only)
+
+Workload (BASELINE.json configs[1] = config 2): a 100x500x500 float32 GRF
+field (P(k) ~ k^-11/3, mean 280, std 15; seeded synthetic -- SDRBench data is
+not available offline), relative error bound 1e-4, block_len 32.  One step is
+the whole op chain of the path on that field:
+
+    value range (K0) -> resolve rel eps -> compress (K1) -> negate (K4)
+    -> scalar_add 3.5 (K5) -> scalar_mul -1.25 (K6) -> mean (K7)
+    -> variance (K7) -> decompress (K3)
+
+``value`` = 7 ops x 4N uncompressed bytes / device step time (the chain
+aggregate of the per-op "uncompressed GB/s" metric; per-op numbers are in
+``ops``).  Inputs are resident in HBM; L2 (126 MB > the 100 MB field) is
+flushed with a 512 MB write between steps and excluded from the timing.  At
+N > 1 every rank owns one config-2-sized shard of a field partitioned by
+contiguous block ranges (weak scaling) and the step adds the collectives C1
+(global value range), C2 (global section offsets) and C3 (exact moments).
+
+``e2e`` runs the same chain through the public API starting from the field in
+pinned HOST memory (H2D inside the timed region) and ends with a D2H read of
+the resulting stream sections, the decompressed field and mean / variance.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+OPS = ("compress", "negate", "scalar_add", "scalar_mul", "mean", "variance", "decompress")
+METRIC = "uncompressed GB/s per op (compress/decompress/homomorphic) & % HBM roofline"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region (nvidia-smi, like the recipe)
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# the B200 arm
+
+def _dist_init():
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def _field(config: int, rank: int, device):
+    from paper_2408_11971_b200 import workloads as W
+
+    if config == 2:
+        seed = 1 if rank == 0 else (1, rank)
+        if rank == 0:
+            import torch
+
+            return torch.from_numpy(W.config2()).to(device)
+        x = W.grf_device(W.CONFIGS[2]["dims"], 11.0 / 3.0, seed, device) * 15.0 + 280.0
+        return x.reshape(-1).float()
+    if config == 4:
+        return W.config4(seed=3 if rank == 0 else 3 + 1000 * rank, device=device)
+    raise ValueError("bench supports --config 2 or 4")
+
+
+class Chain:
+    """One step of the op chain through the public (device) API."""
+
+    def __init__(self, H, cfg, coll):
+        self.H = H
+        self.cfg = cfg
+        self.coll = coll
+
+    def run(self, x, events=None, host_out=False):
+        H, cfg = self.H, self.cfg
+        mark = (lambda i: events[i].record()) if events is not None else (lambda i: None)
+        mark(0)
+        raw = H.RawArray(x, cfg["dims"], "f32")               # K0: range + finite check
+        lo, hi = raw.value_range()
+        if self.coll is not None:
+            lo, hi = self.coll.global_range(lo, hi)            # C1
+        eps = float(cfg["rel_eps"]) * (hi - lo)
+        p = H.QuantParams(eps, cfg["dims"], 32, "f32")
+        s = H.compress(raw, p)                                 # K1
+        if self.coll is not None:
+            sb, pb = s.totals()
+            self.coll.global_offsets(0, sb, pb)                # C2
+        mark(1)
+        z = H.negate(s)                                        # K4
+        mark(2)
+        z = H.scalar_add(z, cfg["sadd"])                       # K5
+        mark(3)
+        z = H.scalar_mul(z, cfg["smul"])                       # K6
+        mark(4)
+        mean = _global_mean(H, z, self.coll)                   # K7
+        mark(5)
+        var = _global_var(H, z, self.coll)                     # K7 (+ squares)
+        mark(6)
+        out = H.decompress(z)                                  # K3
+        mark(7)
+        if host_out:
+            hz = z.to_host()
+            vals = out.values.cpu()
+            return hz, vals, mean, var
+        return z, out, mean, var
+
+
+def _global_mean(H, z, coll):
+    from paper_2408_11971_b200 import ops
+
+    S, Q = ops.exact_moments(z, want_sq=False)
+    n = z.params.element_count
+    if coll is not None:
+        S, Q = coll.global_moments(S, 0)
+        n *= coll.world
+    return ops.mean_from(S, n, z.params.eps)
+
+
+def _global_var(H, z, coll):
+    from paper_2408_11971_b200 import ops
+
+    S, Q = ops.exact_moments(z, want_sq=True)
+    n = z.params.element_count
+    if coll is not None:
+        S, Q = coll.global_moments(S, Q)
+        n *= coll.world
+    return ops.variance_from(S, Q, n, z.params.eps)
+
+
+def _algorithmic_bytes(H, cfg, x):
+    """Per-op algorithmic bytes for this field."""
+    raw = H.RawArray(x, cfg["dims"], "f32")
+    lo, hi = raw.value_range()
+    eps = float(cfg["rel_eps"]) * (hi - lo)
+    p = H.QuantParams(eps, cfg["dims"], 32, "f32")
+    s = H.compress(raw, p)
+    z = H.scalar_mul(H.scalar_add(H.negate(s), cfg["sadd"]), cfg["smul"])
+    n = p.element_count
+    B = p.block_count
+    hs = s.to_host()
+    hz = z.to_host()
+    C_in = B + 4 * B + len(hs.sign_planes) + len(hs.payload)
+    C_z = B + 4 * B + len(hz.sign_planes) + len(hz.payload)
+    nc = int((hs.widths > 0).sum())
+    return {
+        "minmax": 4 * n,
+        "compress": 4 * n + C_in,
+        "negate": 2 * (4 * nc + 4 * B),
+        "scalar_add": 2 * 4 * B,
+        "scalar_mul": C_in + C_z,
+        "mean": C_z,
+        "variance": C_z,
+        "decompress": C_z + 4 * n,
+        "_C": C_in, "_C_chain": C_z, "_ratio": p.raw_nbytes / hs.serialized_size,
+        "_eps": eps,
+    }
+
+
+def run_b200(args):
+    import torch
+
+    world, rank, local = _dist_init()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2408_11971_b200 as H
+    from paper_2408_11971_b200 import workloads as W
+    from paper_2408_11971_b200.sharding import Collectives
+
+    coll = Collectives() if world > 1 else None
+    cfg = dict(W.CONFIGS[args.config])
+    x = _field(args.config, rank, dev).contiguous()
+    n = x.numel()
+    chain = Chain(H, cfg, coll)
+    abytes = _algorithmic_bytes(H, cfg, x)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    for _ in range(max(args.warmup, 3)):
+        chain.run(x)
+    torch.cuda.synchronize()
+
+    nev = 8
+    per_step = []
+    per_op = {op: [] for op in OPS}
+    sampler = ClockSampler(local)
+    sampler.start()
+    if coll is not None:
+        coll.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        flush.fill_(1)                                  # evict L2 (excluded from timing)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
+        chain.run(x, evs)
+        torch.cuda.synchronize()
+        per_step.append(evs[0].elapsed_time(evs[7]))
+        for i, op in enumerate(OPS):
+            per_op[op].append(evs[i].elapsed_time(evs[i + 1]))
+    torch.cuda.synchronize()
+    if coll is not None:
+        coll.barrier()
+    wall = time.perf_counter() - wall0
+    clocks = sampler.stop()
+
+    step_ms = sum(per_step) / len(per_step)
+    if coll is not None:
+        step_ms = coll.max_over_ranks(step_ms)
+    # whole job: 7 ops over every rank's N elements
+    value = len(OPS) * 4.0 * n * world / (step_ms * 1e-3) / 1e9
+
+    # ---- per-kernel timing (each op alone, L2 flushed first) for the roofline
+    kern = _kernel_times(H, cfg, x, flush, reps=max(5, min(args.steps, 20)))
+    peak, peak_kind = _peaks()
+    ops_json = {}
+    for op in OPS:
+        t_ms = statistics.median(per_op[op])
+        ops_json[op] = {
+            "ms_in_chain": round(t_ms, 4),
+            "gbps_uncompressed_in_chain": round(4.0 * n / (t_ms * 1e-3) / 1e9, 2),
+            "kernel_ms": round(kern[op], 4),
+            "kernel_gbps_uncompressed": round(4.0 * n / (kern[op] * 1e-3) / 1e9, 2),
+            "algorithmic_bytes": int(abytes[op]),
+            "roofline_frac": round(abytes[op] / (kern[op] * 1e-3) / 1e9 / peak, 4),
+        }
+    ops_json["minmax"] = {"kernel_ms": round(kern["minmax"], 4),
+                          "algorithmic_bytes": int(abytes["minmax"]),
+                          "roofline_frac": round(abytes["minmax"] / (kern["minmax"] * 1e-3) / 1e9 / peak, 4)}
+    dom = max(OPS, key=lambda o: kern[o])
+    achieved = abytes[dom] / (kern[dom] * 1e-3) / 1e9
+
+    # ---- e2e through the public API from pinned host memory
+    e2e = _e2e(H, chain, x, flush, steps=max(3, min(args.steps, 10)), coll=coll)
+
+    line = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(step_ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64 quantize / int64 bins (f32 input)",
+        "data": "synthetic (seeded GRF stand-in for SDRBench; see DESIGN.md)",
+        "config": {
+            "workload": f"config {args.config}: {'x'.join(map(str, cfg['dims']))} f32, rel eps "
+                        f"{cfg['rel_eps']}, block_len 32, op chain {'>'.join(OPS)}",
+            "elements_per_gpu": n,
+            "global_elements": n * world,
+            "eps": abytes["_eps"],
+            "compression_ratio": round(abytes["_ratio"], 3),
+            "stream_bytes": int(abytes["_C"]),
+            "value_definition": "7 ops x 4N bytes (all ranks) / device step time",
+            "l2": "512 MB write between steps (field 100 MB < 126 MB L2), excluded from timing",
+            "parallelism": f"{world} rank(s), contiguous block ranges, NCCL C1/C2/C3" if world > 1
+            else "1 GPU",
+            "wall_s_timed_region": round(wall, 3),
+        },
+        "ops": ops_json,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None},
+        "e2e": e2e,
+        "gpu_launches": 8 * args.steps,
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = _cpu_baseline(x.cpu().numpy(), cfg, budget_s=args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if coll is not None:
+        coll.barrier()
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def _kernel_times(H, cfg, x, flush, reps=10):
+    """Median device time of each op launched alone after an L2 flush."""
+    import torch
+    from paper_2408_11971_b200 import ops as O
+
+    raw = H.RawArray(x, cfg["dims"], "f32")
+    lo, hi = raw.value_range()
+    p = H.QuantParams(float(cfg["rel_eps"]) * (hi - lo), cfg["dims"], 32, "f32")
+    s = H.compress(raw, p)
+    z0 = H.scalar_add(H.negate(s), cfg["sadd"])
+    z = H.scalar_mul(z0, cfg["smul"])
+    fns = {
+        "minmax": lambda: H.RawArray(x, cfg["dims"], "f32", _validated=True)._validate(),
+        "compress": lambda: H.compress(raw, p),
+        "negate": lambda: H.negate(s),
+        "scalar_add": lambda: H.scalar_add(s, cfg["sadd"]),
+        "scalar_mul": lambda: H.scalar_mul(z0, cfg["smul"]),
+        "mean": lambda: O.moments_device(z, False),
+        "variance": lambda: O.moments_device(z, True),
+        "decompress": lambda: H.decompress(z),
+    }
+    out = {}
+    for name, fn in fns.items():
+        ts = []
+        for _ in range(reps + 1):
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        out[name] = statistics.median(ts[1:])
+    z.check()
+    return out
+
+
+def _e2e(H, chain, x, flush, steps, coll):
+    import torch
+
+    host = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+    host.copy_(x.cpu())
+    n = x.numel()
+    ts = []
+    bo = 0
+    for _ in range(steps + 1):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        xd = host.to(x.device, non_blocking=True)
+        hz, vals, mean, var = chain.run(xd, host_out=True)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+        bo = len(hz.sign_planes) + len(hz.payload) + 5 * hz.params.block_count + vals.numel() * 4 + 16
+    t = statistics.median(ts[1:])
+    if coll is not None:
+        t = coll.max_over_ranks(t)
+    world = coll.world if coll is not None else 1
+    return {"value": round(len(OPS) * 4.0 * n * world / t / 1e9, 3), "unit": "GB/s",
+            "ms_per_step": round(t * 1e3, 3), "h2d_bytes_per_step": 4 * n,
+            "d2h_bytes_per_step": int(bo),
+            "path": "pinned host field -> H2D -> public API chain -> D2H stream + values"}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle arm (cpu_baseline and --impl reference)
+
+_POOL_X = None
+
+
+def _cpu_chain_slice(args):
+    """Oracle op chain on one block-aligned slice [e0, e1) (fork-shared array)."""
+    import hoszp_oracle as O
+
+    e0, e1, eps, sadd, smul = args
+    xs = _POOL_X[e0:e1]
+    s = O.compress(xs, eps, (xs.size,), 32, "f32")
+    z = O.scalar_mul(O.scalar_add(O.negate(s), sadd), smul)
+    S, Q = O.moments(z)
+    S2, _ = O.moments(z)           # mean and variance are separate passes in the reference
+    O.decompress(z)
+    return len(s["payload"]), S, Q
+
+
+def _cpu_run(x, cfg, procs):
+    """One chain over `x` with `procs` worker processes (block-range slices)."""
+    import multiprocessing as mp
+
+    global _POOL_X
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import hoszp_oracle as O
+
+    _POOL_X = x
+    t0 = time.perf_counter()
+    eps = O.resolve_eps(x, cfg["rel_eps"], "rel")
+    nb = -(-x.size // 32)
+    from paper_2408_11971_b200.sharding import block_range
+
+    jobs = []
+    for r in range(procs):
+        b0, b1 = block_range(nb, r, procs)
+        jobs.append((b0 * 32, min(b1 * 32, x.size), eps, cfg["sadd"], cfg["smul"]))
+    if procs == 1:
+        res = [_cpu_chain_slice(j) for j in jobs]
+    else:
+        with mp.get_context("fork").Pool(procs) as pool:
+            res = pool.map(_cpu_chain_slice, jobs)
+    dt = time.perf_counter() - t0
+    return dt, res
+
+
+def _cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def _cpu_baseline(x, cfg, budget_s=20.0):
+    """Oracle chain on a bounded prefix sample of the same field, all cores."""
+    procs = _cpu_cores()
+    sample = min(x.size, max(32 * procs, 1 << 21))
+    # grow the sample while the run stays inside the budget
+    while True:
+        dt, _ = _cpu_run(x[:sample], cfg, procs)
+        if dt * 2.5 > budget_s or sample >= x.size:
+            break
+        sample = min(x.size, sample * 2)
+    return {"value": round(len(OPS) * 4.0 * sample / dt / 1e9, 4), "unit": "GB/s",
+            "cores": procs, "kind": "port",
+            "sample": f"first {sample} of {x.size} values of the bench field, whole op chain, "
+                      f"{procs} processes over block ranges ({dt:.2f} s)"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2408_11971_b200 import workloads as W
+
+    cfg = dict(W.CONFIGS[args.config])
+    if args.config == 2:
+        x = W.config2()
+    else:
+        x = W.config4()
+    procs = _cpu_cores()
+    sample = min(x.size, 1 << 21)
+    xs = x[:sample]
+    for _ in range(args.warmup):
+        _cpu_run(xs, cfg, procs)
+    times = []
+    for _ in range(args.steps):
+        dt, _ = _cpu_run(xs, cfg, procs)
+        times.append(dt)
+    t = sum(times) / len(times)
+    value = len(OPS) * 4.0 * sample / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64 quantize / int64 bins (f32 input)",
+        "data": "synthetic (seeded GRF stand-in for SDRBench)",
+        "config": {"workload": f"config {args.config}, op chain {'>'.join(OPS)}",
+                   "sample_elements": sample},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": procs, "kind": "port",
+                         "sample": f"first {sample} values of the config-{args.config} field per "
+                                   f"step, numpy oracle over {procs} processes"},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -214,8 +214,7 @@ template <class Src>
 static int launch_encode32(Src src, const k32::EncodeOut& out, uint64_t n, cudaStream_t st) {
   const uint64_t nb = ceil_div(n, 32);
   const uint64_t nt = ceil_div(nb, kTileBlocks);
-  constexpr bool kDec = std::is_same<Src, k32::SrcSmul>::value;
-  auto kern = k32::encode_kernel<Src, kDec>;
+  auto kern = k32::encode_kernel<Src>;
   constexpr int smem = k32::EncodeSmem<Src>::kBytes;
   allow_smem(kern, smem);
   kern<<<static_cast<unsigned>(nt), k32::kThreads, smem, st>>>(src, out, nb, nt, tail_len_of(n, 32));
@@ -397,9 +396,9 @@ int hsz_dequantize(const int64_t* bins, uint64_t n, double eps, int out_kind, vo
   const unsigned g = static_cast<unsigned>(grid_for(n, 4, 256, 148 * 16));
   const double d = 2.0 * eps;
   if (out_kind == HSZ_OUT_F32)
-    ops::dequant_kernel<<<g, 256, 0, st>>>(bins, n, k32::SinkF32{static_cast<float*>(out), d}, err);
+    ops::dequant_kernel<<<g, 256, 0, st>>>(bins, n, k32::SinkF32{static_cast<float*>(out), d, d * 0x1p33 >= 3.4028234663852886e38}, err);
   else if (out_kind == HSZ_OUT_F64)
-    ops::dequant_kernel<<<g, 256, 0, st>>>(bins, n, k32::SinkF64{static_cast<double*>(out), d}, err);
+    ops::dequant_kernel<<<g, 256, 0, st>>>(bins, n, k32::SinkF64{static_cast<double*>(out), d, d * 0x1p33 >= 1.7976931348623157e308}, err);
   else
     return HSZ_EINVAL;
   return launch_status();
@@ -427,20 +426,29 @@ int hsz_decode(const uint8_t* widths, const int32_t* outliers, const uint8_t* si
   const double d = 2.0 * eps;
   if (k == 32) {
     const k32::StreamIn s{widths, outliers, signs, payload, toff, n, nb, tail_len_of(n, 32)};
-    constexpr int smem = k32::TileIn::kBytes;
+    const unsigned g = static_cast<unsigned>(nt);
     switch (out_kind) {
-      case HSZ_OUT_F32:
-        k32::decode_kernel<k32::SinkF32><<<static_cast<unsigned>(nt), k32::kThreads, smem, st>>>(
-            s, k32::SinkF32{static_cast<float*>(out), d}, err);
+      case HSZ_OUT_F32: {
+        constexpr int smem = k32::DecodeSmem<k32::SinkF32>::kBytes;
+        allow_smem(k32::decode_kernel<k32::SinkF32>, smem);
+        k32::decode_kernel<k32::SinkF32><<<g, k32::kThreads, smem, st>>>(
+            s, k32::SinkF32{static_cast<float*>(out), d, d * 0x1p33 >= 3.4028234663852886e38}, err);
         break;
-      case HSZ_OUT_F64:
-        k32::decode_kernel<k32::SinkF64><<<static_cast<unsigned>(nt), k32::kThreads, smem, st>>>(
-            s, k32::SinkF64{static_cast<double*>(out), d}, err);
+      }
+      case HSZ_OUT_F64: {
+        constexpr int smem = k32::DecodeSmem<k32::SinkF64>::kBytes;
+        allow_smem(k32::decode_kernel<k32::SinkF64>, smem);
+        k32::decode_kernel<k32::SinkF64><<<g, k32::kThreads, smem, st>>>(
+            s, k32::SinkF64{static_cast<double*>(out), d, d * 0x1p33 >= 1.7976931348623157e308}, err);
         break;
-      case HSZ_OUT_BINS:
-        k32::decode_kernel<k32::SinkBins><<<static_cast<unsigned>(nt), k32::kThreads, smem, st>>>(
+      }
+      case HSZ_OUT_BINS: {
+        constexpr int smem = k32::DecodeSmem<k32::SinkBins>::kBytes;
+        allow_smem(k32::decode_kernel<k32::SinkBins>, smem);
+        k32::decode_kernel<k32::SinkBins><<<g, k32::kThreads, smem, st>>>(
             s, k32::SinkBins{static_cast<int64_t*>(out)}, err);
         break;
+      }
       default:
         return HSZ_EINVAL;
     }
@@ -450,11 +458,11 @@ int hsz_decode(const uint8_t* widths, const int32_t* outliers, const uint8_t* si
   switch (out_kind) {
     case HSZ_OUT_F32:
       gen::decode_kernel<k32::SinkF32><<<static_cast<unsigned>(nt), gen::kThreads, 0, st>>>(
-          s, k32::SinkF32{static_cast<float*>(out), d}, err);
+          s, k32::SinkF32{static_cast<float*>(out), d, d * 0x1p33 >= 3.4028234663852886e38}, err);
       break;
     case HSZ_OUT_F64:
       gen::decode_kernel<k32::SinkF64><<<static_cast<unsigned>(nt), gen::kThreads, 0, st>>>(
-          s, k32::SinkF64{static_cast<double*>(out), d}, err);
+          s, k32::SinkF64{static_cast<double*>(out), d, d * 0x1p33 >= 1.7976931348623157e308}, err);
       break;
     case HSZ_OUT_BINS:
       gen::decode_kernel<k32::SinkBins><<<static_cast<unsigned>(nt), gen::kThreads, 0, st>>>(
@@ -529,7 +537,7 @@ int hsz_moments(const uint8_t* widths, const int32_t* outliers, const uint8_t* s
   const uint64_t nt = ceil_div(nb, kTileBlocks);
   if (k == 32) {
     const k32::StreamIn s{widths, outliers, signs, payload, toff, n, nb, tail_len_of(n, 32)};
-    constexpr int smem = k32::TileIn::kBytes;
+    constexpr int smem = k32::kStageFast;
     if (want_sq)
       k32::moments_kernel<true><<<static_cast<unsigned>(nt), k32::kThreads, smem, st>>>(s, out, err, ws);
     else

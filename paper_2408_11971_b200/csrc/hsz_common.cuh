@@ -22,8 +22,8 @@ constexpr unsigned kFull = 0xffffffffu;
 // Tile geometry shared by every kernel and by the tile-offset cache of a
 // device stream: a tile is kTileBlocks consecutive blocks.
 constexpr int kTileBlocks = HSZ_TILE_BLOCKS;   // 128
-constexpr int kCtaWarps = 8;                    // 256-thread CTAs
-constexpr int kBlocksPerWarp = kTileBlocks / kCtaWarps;  // 16
+constexpr int kCtaWarps = 4;                    // 128-thread CTAs (one thread per block of a tile)
+constexpr int kBlocksPerWarp = kTileBlocks / kCtaWarps;  // 32
 
 static_assert(kTileBlocks % kCtaWarps == 0, "tile must split evenly over warps");
 
@@ -146,32 +146,39 @@ __device__ __forceinline__ void draw_ticket(LookbackWs& w, uint64_t ntiles, uint
   *epoch = e;
 }
 
-// Decoupled look-back over (sign bytes, payload bytes), executed by one
-// full warp.  Publishes the tile's aggregate, sums predecessors (32 at a
-// time) until an inclusive prefix is found, then publishes the inclusive
-// prefix.  Returns the exclusive prefix of this tile.
-__device__ __forceinline__ void lookback(LookbackWs& w, uint64_t tile, uint64_t epoch,
-                                         uint64_t agg_s, uint64_t agg_p, uint64_t* excl_s,
-                                         uint64_t* excl_p) {
-  const int lane = threadIdx.x & 31;
+// Decoupled look-back over (sign bytes, payload bytes), in two steps so the
+// CTA can do useful work in between:
+//   publish_aggregate -- lane 0 publishes the tile's aggregate (tile 0: its
+//                        inclusive prefix) as soon as the tile sizes are known;
+//   resolve_prefix    -- one full warp sums predecessors (32 at a time) until
+//                        an inclusive prefix is found, publishes this tile's
+//                        inclusive prefix and returns the exclusive one.
+__device__ __forceinline__ void publish_aggregate(LookbackWs& w, uint64_t tile, uint64_t epoch,
+                                                  uint64_t agg_s, uint64_t agg_p) {
   const uint64_t tag = epoch << 2;
   if (tile == 0) {
-    if (lane == 0) {
-      w.vals[2] = agg_s;   // inclusive slots of tile 0
-      w.vals[3] = agg_p;
-      st_release(&w.flags[0], tag | kStInc);
-    }
-    *excl_s = 0;
-    *excl_p = 0;
-    return;
-  }
-  if (lane == 0) {
+    w.vals[2] = agg_s;   // inclusive slots of tile 0
+    w.vals[3] = agg_p;
+    st_release(&w.flags[0], tag | kStInc);
+  } else {
     w.vals[tile * 4 + 0] = agg_s;
     w.vals[tile * 4 + 1] = agg_p;
     st_release(&w.flags[tile], tag | kStAgg);
   }
+}
+
+__device__ __forceinline__ void resolve_prefix(LookbackWs& w, uint64_t tile, uint64_t epoch,
+                                               uint64_t agg_s, uint64_t agg_p, uint64_t* excl_s,
+                                               uint64_t* excl_p) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    *excl_s = 0;
+    *excl_p = 0;
+    return;
+  }
   uint64_t sum_s = 0, sum_p = 0;
   int64_t base = static_cast<int64_t>(tile) - 1;
+  unsigned backoff = 32;
   while (true) {
     const int64_t idx = base - lane;
     uint64_t st = kStInc;       // virtual inclusive zero before tile 0
@@ -184,7 +191,8 @@ __device__ __forceinline__ void lookback(LookbackWs& w, uint64_t tile, uint64_t 
     const int first = inc ? (__ffs(inc) - 1) : 32;
     const unsigned below = (first >= 32) ? kFull : ((1u << first) - 1u) | (1u << first);
     if (inv & below) {          // a needed predecessor has not published yet
-      __nanosleep(32);
+      __nanosleep(backoff);
+      backoff = backoff < 512 ? backoff * 2 : 512;
       continue;
     }
     uint64_t vs = 0, vp = 0;
@@ -210,10 +218,19 @@ __device__ __forceinline__ void lookback(LookbackWs& w, uint64_t tile, uint64_t 
   if (lane == 0) {
     w.vals[tile * 4 + 2] = sum_s + agg_s;
     w.vals[tile * 4 + 3] = sum_p + agg_p;
-    st_release(&w.flags[tile], tag | kStInc);
+    st_release(&w.flags[tile], (epoch << 2) | kStInc);
   }
   *excl_s = sum_s;
   *excl_p = sum_p;
+}
+
+// both steps back to back (callers with nothing to overlap)
+__device__ __forceinline__ void lookback(LookbackWs& w, uint64_t tile, uint64_t epoch,
+                                         uint64_t agg_s, uint64_t agg_p, uint64_t* excl_s,
+                                         uint64_t* excl_p) {
+  if ((threadIdx.x & 31) == 0) publish_aggregate(w, tile, epoch, agg_s, agg_p);
+  __syncwarp();
+  resolve_prefix(w, tile, epoch, agg_s, agg_p, excl_s, excl_p);
 }
 
 // ---------------------------------------------------------------------------

@@ -68,6 +68,30 @@ __device__ __forceinline__ int64_t quantize1(double x, const QuantConst& c, uint
   return q;
 }
 
+// Fast exact quantization for the fast-path range.  With |y| < 2^30 the
+// reciprocal quotient y = RN(s * RN(1/d)) is within 1.5 * 2^-22 of s/d, so if
+// y - floor(y) is more than 2^-20 away from an integer:
+//   * floor(RN(s/d)) == floor(y), and
+//   * |x - d*m| <= eps - d * 2^-22 even after the reference's two roundings,
+//     so its repair pass (codec.py:140-154) provably does not fire.
+// Returns false (caller must use quantize1) otherwise.  6 FP64 ops; the int
+// conversion uses the 1.5 * 2^52 magic constant instead of F2I.
+__device__ __forceinline__ bool quantize_fast(double x, const QuantConst& c, int32_t* q) {
+  const double s = __dadd_rn(x, c.eps);
+  const double y = __dmul_rn(s, c.rcp_d);
+  const double m = floor(y);
+  const double g = __dsub_rn(__dsub_rn(y, m), 0.5);
+  const double k = __dadd_rn(m, 6755399441055744.0);
+  *q = __double2loint(k);
+  return (fabs(y) < 0x1p30 - 2.0) & (fabs(g) < 0.5 - 0x1p-20) & (c.fast_div != 0);
+}
+
+// exact int32 -> double without a conversion instruction
+__device__ __forceinline__ double i32_to_double(int32_t v) {
+  return __dsub_rn(__hiloint2double(0x43300000, static_cast<int>(static_cast<uint32_t>(v) ^ 0x80000000u)),
+                   4503601774854144.0);   // 2^52 + 2^31
+}
+
 // Reconstruction RN(d * f64(bin)) (codec.py:107-109); int64 -> f64 is RN.
 __device__ __forceinline__ double grid1(int64_t bin, double d) {
   return __dmul_rn(d, __ll2double_rn(bin));

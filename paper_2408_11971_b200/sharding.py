@@ -1,0 +1,150 @@
+"""Multi-GPU partitioning of one field by contiguous block ranges.
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch; gloo for
+the CPU tests).  Blocks are independent and byte-aligned (FORMAT.md:39-40),
+so each rank compresses / transforms its own block range with no data-path
+exchange.  Only three tiny, latency-bound collectives exist:
+
+* C1 ``global_range`` -- allreduce MIN/MAX of the local value range, so every
+  rank resolves the identical relative eps (codec.py:96-99);
+* C2 ``global_offsets`` -- allgather of per-shard (sign bytes, payload bytes)
+  and an exclusive scan: where each shard's sections start in the global
+  stream (widths/outliers start at the shard's first block);
+* C3 ``global_moments`` -- allgather of the exact per-shard (S, Q) limbs and
+  an exact host sum, so mean / variance are bit-identical for any GPU count.
+
+The shard's sections, concatenated in rank order at the C2 offsets, are
+byte-identical to the single-GPU stream of the whole field (tested in
+tests/test_sharding_gloo.py and tests/test_gpu_sharding.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def block_range(nblocks: int, rank: int, world: int):
+    """Contiguous, balanced block range [b0, b1) of `rank`."""
+    base, extra = divmod(nblocks, world)
+    b0 = rank * base + min(rank, extra)
+    b1 = b0 + base + (1 if rank < extra else 0)
+    return b0, b1
+
+
+def element_range(n: int, block_len: int, rank: int, world: int):
+    nb = -(-n // block_len)
+    b0, b1 = block_range(nb, rank, world)
+    return b0 * block_len, min(b1 * block_len, n)
+
+
+def exclusive_scan(values):
+    out, acc = [], 0
+    for v in values:
+        out.append(acc)
+        acc += int(v)
+    return out, acc
+
+
+@dataclass
+class ShardLayout:
+    """Where one shard's sections sit inside the global stream."""
+
+    rank: int
+    block0: int
+    sign_offset: int
+    payload_offset: int
+    sign_total: int
+    payload_total: int
+
+
+class Collectives:
+    """The three collectives over a torch.distributed process group."""
+
+    def __init__(self, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.torch = torch
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        backend = dist.get_backend(group)
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" \
+                else torch.device("cpu")
+        self.device = device
+
+    def global_range(self, lo: float, hi: float):
+        """C1: allreduce MIN over (lo, -hi) in float64 (exact)."""
+        t = self.torch.tensor([lo, -hi], dtype=self.torch.float64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        v = t.cpu().tolist()
+        return float(v[0]), float(-v[1])
+
+    def _allgather_i64(self, vals):
+        t = self.torch.tensor([int(v) for v in vals], dtype=self.torch.int64, device=self.device)
+        out = [self.torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [[int(x) for x in o.cpu().tolist()] for o in out]
+
+    def global_offsets(self, block0: int, sign_bytes: int, payload_bytes: int) -> ShardLayout:
+        """C2: allgather of the shard byte counts, exclusive scan."""
+        rows = self._allgather_i64([block0, sign_bytes, payload_bytes])
+        so, st = exclusive_scan(r[1] for r in rows)
+        po, pt = exclusive_scan(r[2] for r in rows)
+        return ShardLayout(self.rank, block0, so[self.rank], po[self.rank], st, pt)
+
+    def global_moments(self, S: int, Q: int):
+        """C3: allgather of exact (S, Q) as 64-bit limbs, exact host sum."""
+        limbs = _to_limbs(S, Q)
+        rows = self._allgather_i64(limbs)
+        tot_s = tot_q = 0
+        for r in rows:
+            s, q = _from_limbs(r)
+            tot_s += s
+            tot_q += q
+        return tot_s, tot_q
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+    def max_over_ranks(self, value: float) -> float:
+        t = self.torch.tensor([value], dtype=self.torch.float64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+
+def _to_limbs(S: int, Q: int):
+    """S (signed, < 2^127) and Q (unsigned, < 2^192) -> 5 int64 limbs."""
+    m = (1 << 64) - 1
+    s = S & ((1 << 128) - 1)
+    limbs = [s & m, s >> 64, Q & m, (Q >> 64) & m, Q >> 128]
+    return [v - (1 << 64) if v >= (1 << 63) else v for v in limbs]
+
+
+def _from_limbs(limbs):
+    u = [int(v) & ((1 << 64) - 1) for v in limbs]
+    S = u[0] | (u[1] << 64)
+    if S >= 1 << 127:
+        S -= 1 << 128
+    Q = u[2] | (u[3] << 64) | (u[4] << 128)
+    return S, Q
+
+
+def assemble(params, layouts, shards):
+    """Concatenate per-shard host sections (widths, outliers, signs, payload),
+    given in rank order with their layouts, into one global CompressedStream."""
+    from .model import CompressedStream
+
+    order = sorted(range(len(layouts)), key=lambda i: layouts[i].rank)
+    widths = np.concatenate([np.asarray(shards[i][0], dtype=np.uint8) for i in order])
+    outl = np.concatenate([np.asarray(shards[i][1], dtype=np.int64) for i in order])
+    signs = b"".join(bytes(shards[i][2]) for i in order)
+    payload = b"".join(bytes(shards[i][3]) for i in order)
+    for i in order:
+        L = layouts[i]
+        assert L.sign_offset == sum(len(shards[j][2]) for j in order if layouts[j].rank < L.rank)
+    return CompressedStream(params, widths, outl, signs, payload)
