@@ -160,6 +160,9 @@ int hsz_moments(const uint8_t* widths, const int32_t* outliers, const uint8_t* s
 /* library identification (for the loader's sanity check) */
 const char* hsz_version(void);
 
+/* debug builds (-DHSZ_TRACE): copy out per-CTA phase timestamps; -1 otherwise */
+int hsz_trace_read(unsigned long long* host, int cap, int reset);
+
 #ifdef __cplusplus
 }
 #endif

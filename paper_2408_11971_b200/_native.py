@@ -30,6 +30,7 @@ _dbl = C.c_double
 #: symbol -> (restype, argtypes); mirrors include/hsz_b200.h one-to-one
 SIGNATURES = {
     "hsz_version": (C.c_char_p, []),
+    "hsz_trace_read": (_int, [_vp, _int, _int]),
     "hsz_tile_count": (_u64, [_u64, _u32]),
     "hsz_sign_bound": (_u64, [_u64, _u32]),
     "hsz_payload_bound": (_u64, [_u64, _u32]),

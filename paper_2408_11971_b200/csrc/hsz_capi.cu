@@ -31,7 +31,19 @@ __global__ void __launch_bounds__(kThreads) minmax_kernel(const T* x, uint64_t n
     const uint64_t nv = vec ? n / 4 : 0;
     const float4* xv = reinterpret_cast<const float4*>(x);
     float flo = INFINITY, fhi = -INFINITY;
-    for (uint64_t i = tid; i < nv; i += stride) {
+    uint64_t i = tid;
+    for (; i + 3 * stride < nv; i += 4 * stride) {   // 4 independent 16-byte loads in flight
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcs(xv + i + u * stride);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        bad |= !isfinite(v[u].x) | !isfinite(v[u].y) | !isfinite(v[u].z) | !isfinite(v[u].w);
+        flo = fminf(fminf(flo, v[u].x), fminf(fminf(v[u].y, v[u].z), v[u].w));
+        fhi = fmaxf(fmaxf(fhi, v[u].x), fmaxf(fmaxf(v[u].y, v[u].z), v[u].w));
+      }
+    }
+    for (; i < nv; i += stride) {
       const float4 v = __ldcs(xv + i);
       bad |= !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
       flo = fminf(fminf(flo, v.x), fminf(fminf(v.y, v.z), v.w));
@@ -80,11 +92,29 @@ __global__ void __launch_bounds__(kThreads) minmax_kernel(const T* x, uint64_t n
     s_last = atom_add_acq_rel(done, 1) == gridDim.x - 1;
   }
   __syncthreads();
-  if (!s_last || threadIdx.x != 0) return;
+  if (!s_last) return;
   __threadfence();
-  for (unsigned i = 0; i < gridDim.x; ++i) {
+  // the last CTA folds every CTA's partial in parallel
+  lo = INFINITY;
+  hi = -INFINITY;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
     lo = fmin(lo, __longlong_as_double(ld_relaxed(reinterpret_cast<uint64_t*>(part + 2 * i))));
     hi = fmax(hi, __longlong_as_double(ld_relaxed(reinterpret_cast<uint64_t*>(part + 2 * i + 1))));
+  }
+  for (int m = 16; m > 0; m >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(kFull, lo, m));
+    hi = fmax(hi, __shfl_xor_sync(kFull, hi, m));
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    s_lo[warp] = lo;
+    s_hi[warp] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int i = 1; i < kThreads / 32; ++i) {
+    lo = fmin(lo, s_lo[i]);
+    hi = fmax(hi, s_hi[i]);
   }
   out[0] = lo;
   out[1] = hi;
@@ -217,7 +247,19 @@ static int launch_encode32(Src src, const k32::EncodeOut& out, uint64_t n, cudaS
   auto kern = k32::encode_kernel<Src>;
   constexpr int smem = k32::EncodeSmem<Src>::kBytes;
   allow_smem(kern, smem);
-  kern<<<static_cast<unsigned>(nt), k32::kThreads, smem, st>>>(src, out, nb, nt, tail_len_of(n, 32));
+  // persistent: as many CTAs as can be co-resident, each looping over tickets
+  static int resident = 0, resident_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (resident_dev != dev) {
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, k32::kEncThreads, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    resident = per_sm > 0 ? per_sm * sms : sms;
+    resident_dev = dev;
+  }
+  const uint64_t grid = nt < static_cast<uint64_t>(resident) ? nt : static_cast<uint64_t>(resident);
+  kern<<<static_cast<unsigned>(grid), k32::kEncThreads, smem, st>>>(src, out, nb, nt, tail_len_of(n, 32));
   return launch_status();
 }
 
@@ -290,6 +332,26 @@ using namespace hsz;
 extern "C" {
 
 const char* hsz_version(void) { return "hsz_b200 1.0 sm_100a"; }
+
+// debug: copy out phase-trace records (only in -DHSZ_TRACE builds; returns count)
+int hsz_trace_read(unsigned long long* host, int cap, int reset) {
+#ifdef HSZ_TRACE
+  unsigned int n = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&n, g_trace_n, sizeof(n));
+  if (n > static_cast<unsigned>(kTraceCap)) n = kTraceCap;
+  if (static_cast<int>(n) > cap) n = cap;
+  if (host && n) cudaMemcpyFromSymbol(host, g_trace, n * sizeof(unsigned long long));
+  if (reset) {
+    unsigned int z = 0;
+    cudaMemcpyToSymbol(g_trace_n, &z, sizeof(z));
+  }
+  return static_cast<int>(n);
+#else
+  (void)host; (void)cap; (void)reset;
+  return -1;
+#endif
+}
 
 uint64_t hsz_tile_count(uint64_t n, uint32_t k) {
   if (k == 0) return 0;
@@ -514,6 +576,8 @@ int hsz_scalar_mul(const uint8_t* widths, const int32_t* outliers, const uint8_t
     src.in = k32::StreamIn{widths, outliers, signs, payload, toff, n, nb, tail_len_of(n, 32)};
     src.rs = rs;
     src.d = d;
+    src.rsd = static_cast<double>(rs);
+    src.small_rs = rs > -(1ll << 21) && rs < (1ll << 21);
     const k32::EncodeOut out{ow, oo, os, sign_cap, op, payload_cap, otoff, err, ws};
     return launch_encode32(src, out, n, st);
   }

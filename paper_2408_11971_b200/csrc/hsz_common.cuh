@@ -16,6 +16,25 @@
 
 namespace hsz {
 
+// Optional phase tracing (compile with -DHSZ_TRACE): thread 0 of each CTA
+// appends (tag, globaltimer) records; read with hsz_trace_read().
+#ifdef HSZ_TRACE
+constexpr int kTraceCap = 1 << 20;
+__device__ unsigned long long g_trace[kTraceCap];
+__device__ unsigned int g_trace_n;
+__device__ __forceinline__ void trace(uint32_t tag) {
+  if (threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned i = atomicAdd(&g_trace_n, 1u);
+    if (i < kTraceCap) g_trace[i] = (static_cast<unsigned long long>(blockIdx.x) << 48) |
+                                    (static_cast<unsigned long long>(tag) << 40) | (t & ((1ull << 40) - 1));
+  }
+}
+#else
+__device__ __forceinline__ void trace(uint32_t) {}
+#endif
+
 constexpr int kWarp = 32;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -75,6 +94,25 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// named barrier 1 over the 128 compute threads (warps 0-3) of a CTA that may
+// also contain a specialised store warp; equivalent to __syncthreads() in
+// 128-thread CTAs
+__device__ __forceinline__ void grp_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ bool grp_and(bool p) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred q, o;\n\tsetp.ne.u32 q, %1, 0;\n\t"
+      "bar.red.and.pred o, 1, 128, q;\n\tselp.u32 %0, 1, 0, o;\n}"
+      : "=r"(r)
+      : "r"(static_cast<uint32_t>(p))
+      : "memory");
+  return r != 0;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // gpu-scope acquire / release accesses for the look-back protocol
 
@@ -103,7 +141,7 @@ __device__ __forceinline__ uint64_t atom_add_acq_rel(uint64_t* p, uint64_t v) {
 
 // Workspace layout (u64 words; see hsz_workspace_size):
 //   [0]      ticket          [1] epoch       [2] moments done-counter
-//   [3]      minmax done-counter             [4..64) reserved
+//   [3]      minmax done-counter             [8..18) moments carry-save counters
 //   [64 .. 64 + 2*kMinmaxCtasMax)            minmax per-CTA partials
 //   flags[ntiles]   at kWsFlagsOff            (epoch << 2 | state)
 //   vals[ntiles][6] right after the flags     (agg_sign, agg_pay, inc_sign,
@@ -167,6 +205,18 @@ __device__ __forceinline__ void publish_aggregate(LookbackWs& w, uint64_t tile, 
   }
 }
 
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
+// Each lane inspects kLbPerLane consecutive predecessors, so one round trip
+// covers 32 * kLbPerLane tiles: with hundreds of tiles in flight, the nearest
+// published inclusive prefix is usually found in one or two rounds.
+#ifndef HSZ_LB_PER_LANE
+#define HSZ_LB_PER_LANE 1
+#endif
+constexpr int kLbPerLane = HSZ_LB_PER_LANE;
+
 __device__ __forceinline__ void resolve_prefix(LookbackWs& w, uint64_t tile, uint64_t epoch,
                                                uint64_t agg_s, uint64_t agg_p, uint64_t* excl_s,
                                                uint64_t* excl_p) {
@@ -180,29 +230,51 @@ __device__ __forceinline__ void resolve_prefix(LookbackWs& w, uint64_t tile, uin
   int64_t base = static_cast<int64_t>(tile) - 1;
   unsigned backoff = 32;
   while (true) {
-    const int64_t idx = base - lane;
-    uint64_t st = kStInc;       // virtual inclusive zero before tile 0
-    if (idx >= 0) {
-      const uint64_t f = ld_acquire(&w.flags[idx]);
-      st = ((f >> 2) == epoch) ? (f & 3) : 0;
+    // relaxed flag loads (all in flight together), then one acquire fence
+    uint32_t stj[kLbPerLane];
+#pragma unroll
+    for (int j = 0; j < kLbPerLane; ++j) {
+      const int64_t idx = base - (lane * kLbPerLane + j);
+      uint32_t st = kStInc;       // virtual inclusive zero before tile 0
+      if (idx >= 0) {
+        const uint64_t f = ld_relaxed(&w.flags[idx]);
+        st = ((f >> 2) == epoch) ? static_cast<uint32_t>(f & 3) : 0u;
+      }
+      stj[j] = st;
     }
-    const unsigned inv = __ballot_sync(kFull, st == 0);
-    const unsigned inc = __ballot_sync(kFull, st == kStInc);
+    fence_acq_rel_gpu();
+    int fj = kLbPerLane;                 // first inclusive in my run
+    bool inv_all = false, inv_pre = false;
+#pragma unroll
+    for (int j = kLbPerLane - 1; j >= 0; --j) {
+      if (stj[j] == kStInc) fj = j;
+      inv_all |= stj[j] == 0;
+    }
+#pragma unroll
+    for (int j = 0; j < kLbPerLane; ++j) inv_pre |= (j <= fj) && (stj[j] == 0);
+    const unsigned inc = __ballot_sync(kFull, fj < kLbPerLane);
     const int first = inc ? (__ffs(inc) - 1) : 32;
-    const unsigned below = (first >= 32) ? kFull : ((1u << first) - 1u) | (1u << first);
-    if (inv & below) {          // a needed predecessor has not published yet
+    const bool bad = (lane < first && inv_all) || (lane == first && inv_pre);
+    if (__any_sync(kFull, bad)) {        // a needed predecessor has not published yet
       __nanosleep(backoff);
-      backoff = backoff < 512 ? backoff * 2 : 512;
+      backoff = backoff < 256 ? backoff * 2 : 256;
       continue;
     }
     uint64_t vs = 0, vp = 0;
-    if (idx >= 0) {
-      if (lane < first) {
-        vs = ld_relaxed(&w.vals[idx * 4 + 0]);
-        vp = ld_relaxed(&w.vals[idx * 4 + 1]);
-      } else if (lane == first) {
-        vs = ld_relaxed(&w.vals[idx * 4 + 2]);
-        vp = ld_relaxed(&w.vals[idx * 4 + 3]);
+    if (lane <= first) {
+      const int stop = (lane < first) ? kLbPerLane : fj;
+#pragma unroll
+      for (int j = 0; j < kLbPerLane; ++j) {
+        const int64_t idx = base - (lane * kLbPerLane + j);
+        if (idx >= 0 && j <= stop && j < kLbPerLane) {
+          if (j < stop) {
+            vs += ld_relaxed(&w.vals[idx * 4 + 0]);
+            vp += ld_relaxed(&w.vals[idx * 4 + 1]);
+          } else {
+            vs += ld_relaxed(&w.vals[idx * 4 + 2]);
+            vp += ld_relaxed(&w.vals[idx * 4 + 3]);
+          }
+        }
       }
     }
 #pragma unroll
@@ -213,7 +285,7 @@ __device__ __forceinline__ void resolve_prefix(LookbackWs& w, uint64_t tile, uin
     sum_s += vs;
     sum_p += vp;
     if (first < 32) break;
-    base -= 32;
+    base -= 32 * kLbPerLane;
   }
   if (lane == 0) {
     w.vals[tile * 4 + 2] = sum_s + agg_s;

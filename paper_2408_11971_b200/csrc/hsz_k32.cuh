@@ -66,7 +66,7 @@ __device__ __forceinline__ void scan2(uint32_t a, uint32_t b, uint32_t* ea, uint
     s_tmp[warp] = ia;
     s_tmp[4 + warp] = ib;
   }
-  __syncthreads();
+  grp_sync();
   uint32_t pa = 0, pb = 0, sa = 0, sb = 0;
 #pragma unroll
   for (int i = 0; i < kCtaWarps; ++i) {
@@ -294,13 +294,46 @@ __device__ __forceinline__ LaneBlock lane_block(const TileIn& t, int j) {
 }
 
 // ---------------------------------------------------------------------------
-// bin sources of the encoder
+// staging with a reusable mbarrier (persistent CTAs): thread 0 issues TMA bulk
+// copies and arms the barrier; everybody waits on the current phase parity.
+
+struct Stager {
+  uint64_t* bar;
+  uint32_t phase;   // parity of the next completion (flips on every bulk use)
+  bool bulk;        // the current tile was staged with a bulk copy
+  __device__ __forceinline__ void init(uint64_t* b) {
+    bar = b;
+    phase = 0;
+    bulk = false;
+    if (threadIdx.x == 0) {
+      mbar_init(bar, 1);
+      fence_mbar_init();
+    }
+  }
+  // thread 0: make prior generic-proxy accesses of the buffer visible before
+  // the async proxy overwrites it, then arm + issue
+  __device__ __forceinline__ void arm(uint32_t bytes) const {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_expect_tx(bar, bytes);
+  }
+  __device__ __forceinline__ void wait() {
+    if (bulk) {
+      mbar_wait_parity(bar, phase);
+      phase ^= 1u;
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// bin sources of the encoder (all calls are CTA-uniform)
 //
-//   stage(tile, sm, bar, s_tmp, flags)  -- all threads: stage the tile input
-//   rows(rows, flags) -> bool            -- quantize/decode into registers; if
-//        the whole tile fits the fast path, write int32 bin rows in place
-//        (padded, see pad) and return true.  CTA-uniform.
-//   lane_bin(lb, lane, len, flags)       -- fallback: lane's bin of tile block lb
+//   issue(tile, stage, st, s_tmp, flags) -- start staging `tile` (async when
+//                                           possible; the stage buffer is free)
+//   rows(stage, st, rows, flags) -> bool  -- wait for the staged tile, build the
+//        int32 bin rows (padded, see pad) and report whether the whole tile is
+//        on the fast path
+//   lane_bin(lb, lane, len, flags)        -- fallback: lane's exact bin of tile
+//        block lb, read from global memory (the stage may be reused)
 
 template <typename T>
 struct SrcQuant {
@@ -308,19 +341,30 @@ struct SrcQuant {
   uint64_t n;
   QuantConst c;
   uint64_t tile;
-  const T* xs;   // staged tile
   static constexpr uint32_t kStageBytes = kTileElems * sizeof(T);
-  static constexpr int kMinBlocks = 8;   // <= 64 registers
+  static constexpr int kMinBlocks = 4;
 
-  __device__ __forceinline__ void stage(uint64_t t, unsigned char* sm, uint64_t* bar, uint32_t*,
+  __device__ __forceinline__ void issue(uint64_t t, unsigned char* stage, Stager& st, uint32_t*,
                                         uint32_t*) {
     tile = t;
-    xs = reinterpret_cast<const T*>(sm);
-    stage_elems(reinterpret_cast<T*>(sm), x, t * kTileElems, n, bar);
+    const uint64_t e0 = t * kTileElems;
+    const uint64_t cnt = (n - e0 < (uint64_t)kTileElems) ? (n - e0) : (uint64_t)kTileElems;
+    st.bulk = cnt == (uint64_t)kTileElems && (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
+    if (st.bulk) {
+      if (threadIdx.x == 0) {
+        st.arm(kStageBytes);
+        bulk_g2s(stage, x + e0, kStageBytes, st.bar);
+      }
+    } else {
+      T* d = reinterpret_cast<T*>(stage);
+      for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) d[i] = x[e0 + i];
+      grp_sync();
+    }
   }
-  // element-parallel quantize straight into the (separate) bin rows; the
-  // staged input stays intact for the fallback
-  __device__ __forceinline__ bool rows(int32_t* rows, uint32_t* flags) {
+  __device__ __forceinline__ bool rows(const unsigned char* stage, Stager& st, int32_t* rows,
+                                       uint32_t* flags) {
+    st.wait();
+    const T* xs = reinterpret_cast<const T*>(stage);
     const uint64_t e0 = tile * kTileElems;
     const uint32_t cnt = static_cast<uint32_t>((n - e0 < (uint64_t)kTileElems) ? (n - e0) : kTileElems);
     bool ok = true;
@@ -362,11 +406,11 @@ struct SrcQuant {
         rows[base + j * kSweepStride] = v;
       }
     }
-    return __syncthreads_and(ok) != 0;
+    return grp_and(ok);
   }
   __device__ __forceinline__ int64_t lane_bin(int lb, int lane, int len, uint32_t* flags) {
     if (lane >= len) return 0;
-    return quantize1(static_cast<double>(xs[lb * K + lane]), c, flags);
+    return quantize1(static_cast<double>(x[tile * kTileElems + lb * K + lane]), c, flags);
   }
 };
 
@@ -374,17 +418,30 @@ struct SrcBins {
   const int64_t* bins;
   uint64_t n;
   uint64_t tile;
-  const int64_t* bs;
   static constexpr uint32_t kStageBytes = kTileElems * 8;
-  static constexpr int kMinBlocks = 6;
+  static constexpr int kMinBlocks = 4;
 
-  __device__ __forceinline__ void stage(uint64_t t, unsigned char* sm, uint64_t* bar, uint32_t*,
+  __device__ __forceinline__ void issue(uint64_t t, unsigned char* stage, Stager& st, uint32_t*,
                                         uint32_t*) {
     tile = t;
-    bs = reinterpret_cast<const int64_t*>(sm);
-    stage_elems(reinterpret_cast<int64_t*>(sm), bins, t * kTileElems, n, bar);
+    const uint64_t e0 = t * kTileElems;
+    const uint64_t cnt = (n - e0 < (uint64_t)kTileElems) ? (n - e0) : (uint64_t)kTileElems;
+    st.bulk = cnt == (uint64_t)kTileElems && (reinterpret_cast<uintptr_t>(bins) & 15u) == 0;
+    if (st.bulk) {
+      if (threadIdx.x == 0) {
+        st.arm(kStageBytes);
+        bulk_g2s(stage, bins + e0, kStageBytes, st.bar);
+      }
+    } else {
+      int64_t* d = reinterpret_cast<int64_t*>(stage);
+      for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) d[i] = bins[e0 + i];
+      grp_sync();
+    }
   }
-  __device__ __forceinline__ bool rows(int32_t* rows, uint32_t* flags) {
+  __device__ __forceinline__ bool rows(const unsigned char* stage, Stager& st, int32_t* rows,
+                                       uint32_t*) {
+    st.wait();
+    const int64_t* bs = reinterpret_cast<const int64_t*>(stage);
     const uint64_t e0 = tile * kTileElems;
     const uint32_t cnt = static_cast<uint32_t>((n - e0 < (uint64_t)kTileElems) ? (n - e0) : kTileElems);
     bool ok = true;
@@ -400,11 +457,11 @@ struct SrcBins {
       }
       rows[base + j * kSweepStride] = v;
     }
-    return __syncthreads_and(ok) != 0;
+    return grp_and(ok);
   }
   __device__ __forceinline__ int64_t lane_bin(int lb, int lane, int len, uint32_t* flags) {
     if (lane >= len) return 0;
-    const int64_t v = bs[lb * K + lane];
+    const int64_t v = bins[tile * kTileElems + lb * K + lane];
     if (v == INT64_MIN) *flags |= HSZ_ERR_RESCALE_OVERFLOW;   // QuantArray guard model.py:124-128
     return v;
   }
@@ -415,27 +472,80 @@ struct SrcSmul {
   StreamIn in;
   int64_t rs;
   double d;
+  double rsd;      // (double) rs
+  bool small_rs;   // |rs| < 2^21: |bin * rs| < 2^53 for every fast-path bin
   TileIn t;
   static constexpr uint32_t kStageBytes = kStageFast;
   static constexpr int kMinBlocks = 4;
 
-  __device__ __forceinline__ void stage(uint64_t tile, unsigned char* sm, uint64_t* bar,
+  // load block metadata, scan, and (fast tiles) bulk-copy the tile's bytes
+  __device__ __forceinline__ void issue(uint64_t tile, unsigned char* stage, Stager& st,
                                         uint32_t* s_tmp, uint32_t* flags) {
-    stage_tile_in(in, tile, sm, bar, s_tmp, &t, flags);
+    const uint64_t b = tile * TB + threadIdx.x;
+    uint32_t w = 0;
+    int32_t o = 0;
+    int len = 0;
+    if (b < in.nblocks) {
+      w = in.widths[b];
+      o = in.outliers[b];
+      len = (b == in.nblocks - 1) ? static_cast<int>(in.tail_len) : K;
+    }
+    if (w > 64) {
+      *flags |= HSZ_ERR_BAD_WIDTH;
+      w = 0;
+    }
+    const uint32_t sb = w ? (len + 7) / 8 : 0;
+    const uint32_t pb = (len * w + 7) / 8;
+    uint32_t es, ep, ts, tp;
+    scan2(sb, pb, &es, &ep, &ts, &tp, s_tmp);
+    const uint64_t g_s0 = in.toff[2 * tile], g_p0 = in.toff[2 * tile + 1];
+    const bool fast = grp_and(w <= kFastW);
+    t.w = w;
+    t.o = o;
+    t.len = len;
+    t.fast = fast;
+    st.bulk = fast;
+    if (fast) {
+      const uint64_t s_lo = g_s0 & ~15ull, s_hi = (g_s0 + ts + 15) & ~15ull;
+      const uint64_t p_lo = g_p0 & ~15ull, p_hi = (g_p0 + tp + 15) & ~15ull;
+      const uint32_t sbytes = static_cast<uint32_t>(s_hi - s_lo);
+      const uint32_t pbytes = static_cast<uint32_t>(p_hi - p_lo);
+      if (threadIdx.x == 0) {
+        st.arm(sbytes + pbytes);
+        if (sbytes) bulk_g2s(stage, in.signs + s_lo, sbytes, st.bar);
+        if (pbytes) bulk_g2s(stage + kStageSign, in.payload + p_lo, pbytes, st.bar);
+      }
+      t.sgn = stage;
+      t.pay = stage + kStageSign;
+      t.soff = (g_s0 - s_lo) + es;
+      t.poff = (g_p0 - p_lo) + ep;
+    } else {
+      t.sgn = in.signs;
+      t.pay = in.payload;
+      t.soff = g_s0 + es;
+      t.poff = g_p0 + ep;
+    }
   }
-  __device__ __forceinline__ bool rows(int32_t* rows, uint32_t* flags) {
-    if (!t.fast) return false;      // CTA-uniform
+  __device__ __forceinline__ bool rows(const unsigned char*, Stager& st, int32_t* rows,
+                                       uint32_t* flags) {
+    st.wait();
+    if (!t.fast || !small_rs) return false;      // CTA-uniform
     bool ok = true;
-    const int64_t o = t.o;
-    uint32_t f = 0;
     int32_t* row = rows + threadIdx.x * kRow;
+    // |bin| < 2^32 and |rs| < 2^21: bin * rs is exact in float64, so
+    // RN(f64(p)) == f64(bin) * f64(rs); then ops.py:199-208 verbatim.
+    // (Larger scalars take the exact 128-bit fallback.)
+    const double od = static_cast<double>(t.o);
     decode_row_fast(t, [&](int i, int32_t P) {
-      const int64_t v = rescale1(product_rn(o + P, rs), d, &f);
-      ok &= (v > -kWideLimit) & (v < kWideLimit);
-      row[i] = static_cast<int32_t>(v);
+      const double pd = __dmul_rn(__dadd_rn(od, i32_to_double(P)), rsd);
+      const double tt = __dmul_rn(d, pd);
+      const double mag = floor(__dadd_rn(fabs(tt), 0.5));
+      ok &= mag < static_cast<double>(kWideLimit - 1);
+      const int32_t mi = __double2loint(__dadd_rn(mag, 6755399441055744.0));
+      row[i] = tt < 0.0 ? -mi : mi;
     });
-    *flags |= f;
-    return __syncthreads_and(ok) != 0;
+    (void)flags;
+    return grp_and(ok);
   }
   __device__ __forceinline__ int64_t lane_bin(int lb, int lane, int len, uint32_t* flags) {
     const LaneBlock m = lane_block(t, lb & (BPW - 1));
@@ -501,199 +611,56 @@ struct EncodeOut {
   void* ws;
 };
 
+// Fallback encoder (a tile with a bin beyond 2^30, or a stream tile wider than
+// 26 bits): one warp per block, exact 64-bit residuals, widths up to 64.
+// Pass 1 computes sizes (and writes widths / outliers); after the look-back,
+// pass 2 recomputes each block and writes it at its final offset.  Out of
+// line so that the fast path's register budget is not set by it.
 template <class Src>
-struct EncodeSmem {
-  // [staged input | int32 bin rows | packed sign words | fallback scratch];
-  // once the rows are built the fast path packs payload words over the
-  // staged input (<= 31 words per block fits the 16 KB f32 stage)
-  static constexpr uint32_t kStage = ((Src::kStageBytes > TB * 31 * 4 ? Src::kStageBytes : TB * 31 * 4) + 15) & ~15u;
-  static constexpr uint32_t kRows = TB * kRow * 4;
-  static constexpr uint32_t kSign = TB * 4;
-  static constexpr uint32_t kScratch = kCtaWarps * 64 * 4;   // fallback: one block's words per warp
-  static constexpr uint32_t kBytes = kStage + kRows + kSign + kScratch;
-};
-
-template <class Src>
-__global__ void __launch_bounds__(kThreads, Src::kMinBlocks) encode_kernel(Src src, EncodeOut out,
-                                                          uint64_t nblocks, uint64_t ntiles,
-                                                          uint32_t tail_len) {
-  extern __shared__ __align__(16) unsigned char sm[];
-  using L = EncodeSmem<Src>;
-  uint32_t* words = reinterpret_cast<uint32_t*>(sm);          // packed payload (fast path)
-  int32_t* rows = reinterpret_cast<int32_t*>(sm + L::kStage);
-  uint32_t* sm_sign = reinterpret_cast<uint32_t*>(sm + L::kStage + L::kRows);
-  uint32_t* scratch = reinterpret_cast<uint32_t*>(sm + L::kStage + L::kRows + L::kSign);
-  __shared__ uint64_t s_bar;
-  __shared__ uint64_t s_tile, s_epoch, s_excl_s, s_excl_p;
-  __shared__ uint32_t s_tmp[8];
-  __shared__ uint32_t s_wsb[kCtaWarps], s_wpb[kCtaWarps];
-  __shared__ uint32_t s_err;
-
+__device__ __noinline__ uint32_t fallback_sizes(Src src, EncodeOut out, uint64_t tile,
+                                                 uint64_t nblocks, uint32_t tail_len,
+                                                 uint32_t* s_wsb, uint32_t* s_wpb) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  LookbackWs lw = LookbackWs::bind(out.ws, ntiles);
-  if (threadIdx.x == 0) {
-    uint64_t t, e;
-    draw_ticket(lw, ntiles, &t, &e);
-    s_tile = t;
-    s_epoch = e;
-    s_err = 0;
-  }
-  __syncthreads();
-  const uint64_t tile = s_tile;
   uint32_t flags = 0;
-  src.stage(tile, sm, &s_bar, s_tmp, &flags);
-  const bool fast = src.rows(rows, &flags);        // CTA-uniform
+  const uint64_t blk0 = tile * TB + warp * BPW;
+  uint32_t sbytes = 0, pbytes = 0, my_w = 0;
+  int64_t my_o = 0;
+  for (int j = 0; j < BPW; ++j) {
+    const uint64_t b = blk0 + j;
+    if (b >= nblocks) break;
+    const int len = (b == nblocks - 1) ? static_cast<int>(tail_len) : K;
+    const int64_t q = src.lane_bin(warp * BPW + j, lane, len, &flags);
+    const int64_t first = __shfl_sync(kFull, q, 0);
+    const int64_t prev = __shfl_up_sync(kFull, q, 1);
+    bool neg = false;
+    uint64_t mag = 0;
+    if (lane > 0 && lane < len) mag = absdiff64(q, prev, &neg);
+    const int wl = mag ? 64 - __clzll(static_cast<long long>(mag)) : 0;
+    const int w = __reduce_max_sync(kFull, wl);
+    if (lane == j) {
+      my_w = w;
+      my_o = first;
+    }
+    if (w) sbytes += (len + 7) >> 3;
+    pbytes += (len * w + 7) >> 3;
+  }
+  if (blk0 + lane < nblocks) {
+    out.widths[blk0 + lane] = static_cast<uint8_t>(my_w);
+    if (my_o < INT32_MIN || my_o > INT32_MAX) flags |= HSZ_ERR_OUTLIER_OVERFLOW;
+    out.outliers[blk0 + lane] = static_cast<int32_t>(my_o);
+  }
+  if (lane == 0) {
+    s_wsb[warp] = sbytes;
+    s_wpb[warp] = pbytes;
+  }
+  return flags;
+}
 
-  uint32_t tile_s = 0, tile_p = 0;                 // fast path: tile section bytes
-  if (fast) {
-    // ---- thread-per-block: residuals, width, sign word ------------------
-    const int b = threadIdx.x;
-    const uint64_t gb = tile * TB + b;
-    const bool active = gb < nblocks;
-    const int len = active ? ((gb == nblocks - 1) ? static_cast<int>(tail_len) : K) : 0;
-    const int32_t* row = rows + b * kRow;
-    uint32_t mx = 0, sbits = 0;
-    const int32_t first = row[0];
-    {
-      int32_t prev = first;
-#pragma unroll
-      for (int i = 1; i < K; ++i) {
-        const int32_t q = row[i];
-        const int32_t dlt = q - prev;      // |q| < 2^30: no overflow
-        prev = q;
-        const bool live = i < len;
-        mx |= live ? static_cast<uint32_t>(dlt < 0 ? -dlt : dlt) : 0u;   // bit length of OR == of max
-        sbits |= (live && dlt < 0) ? (1u << (31 - i)) : 0u;
-      }
-    }
-    const uint32_t w = mx ? 32 - __clz(mx) : 0;
-    const uint32_t sb = (active && w) ? (len + 7) >> 3 : 0;
-    const uint32_t pb = active ? (len * w + 7) >> 3 : 0;
-    uint32_t es, ep;
-    scan2(sb, pb, &es, &ep, &tile_s, &tile_p, s_tmp);
-    // publish the tile aggregate now; successors can start summing it while
-    // this CTA packs
-    if (threadIdx.x == 0) publish_aggregate(lw, tile, s_epoch, tile_s, tile_p);
-    if (w) {
-      // second walk: MSB-first w-bit fields through a 64-bit shift register,
-      // packed over the (consumed) staged input
-      sm_sign[es >> 2] = bswap32(sbits);
-      uint32_t* dst = words + (ep >> 2);
-      uint64_t acc = 0;
-      int nb = w, wi = 0;                  // slot 0: a zero field
-      int32_t prev = first;
-#pragma unroll
-      for (int i = 1; i < K; ++i) {
-        const int32_t q = row[i];
-        const int32_t dlt = q - prev;
-        prev = q;
-        const uint32_t m = (i < len) ? static_cast<uint32_t>(dlt < 0 ? -dlt : dlt) : 0u;
-        acc = (acc << w) | m;
-        nb += w;
-        if (nb >= 32) {
-          nb -= 32;
-          dst[wi++] = bswap32(static_cast<uint32_t>(acc >> nb));
-        }
-      }
-      if (nb > 0) dst[wi] = bswap32(static_cast<uint32_t>(acc << (32 - nb)));   // tail block only
-    }
-    if (active) {
-      out.widths[gb] = static_cast<uint8_t>(w);
-      out.outliers[gb] = first;
-    }
-  } else {
-    // ---- fallback pass 1: one warp per block, sizes only -----------------
-    const uint64_t blk0 = tile * TB + warp * BPW;
-    uint32_t sbytes = 0, pbytes = 0, my_w = 0;
-    int64_t my_o = 0;
-    for (int j = 0; j < BPW; ++j) {
-      const uint64_t b = blk0 + j;
-      if (b >= nblocks) break;
-      const int len = (b == nblocks - 1) ? static_cast<int>(tail_len) : K;
-      const int64_t q = src.lane_bin(warp * BPW + j, lane, len, &flags);
-      const int64_t first = __shfl_sync(kFull, q, 0);
-      const int64_t prev = __shfl_up_sync(kFull, q, 1);
-      bool neg = false;
-      uint64_t mag = 0;
-      if (lane > 0 && lane < len) mag = absdiff64(q, prev, &neg);
-      const int wl = mag ? 64 - __clzll(static_cast<long long>(mag)) : 0;
-      const int w = __reduce_max_sync(kFull, wl);
-      if (lane == j) {
-        my_w = w;
-        my_o = first;
-      }
-      if (w) sbytes += (len + 7) >> 3;
-      pbytes += (len * w + 7) >> 3;
-    }
-    if (blk0 + lane < nblocks) {
-      out.widths[blk0 + lane] = static_cast<uint8_t>(my_w);
-      if (my_o < INT32_MIN || my_o > INT32_MAX) flags |= HSZ_ERR_OUTLIER_OVERFLOW;
-      out.outliers[blk0 + lane] = static_cast<int32_t>(my_o);
-    }
-    if (lane == 0) {
-      s_wsb[warp] = sbytes;
-      s_wpb[warp] = pbytes;
-    }
-  }
-  flags = __reduce_or_sync(kFull, flags);
-  if (lane == 0 && flags) atomicOr(&s_err, flags);
-  __syncthreads();
-
-  if (warp == 0) {
-    uint64_t agg_s = tile_s, agg_p = tile_p;
-    if (!fast) {
-      agg_s = __reduce_add_sync(kFull, lane < kCtaWarps ? s_wsb[lane] : 0u);
-      agg_p = __reduce_add_sync(kFull, lane < kCtaWarps ? s_wpb[lane] : 0u);
-    }
-    uint64_t es, ep;
-    if (fast) {
-      resolve_prefix(lw, tile, s_epoch, agg_s, agg_p, &es, &ep);
-    } else {
-      lookback(lw, tile, s_epoch, agg_s, agg_p, &es, &ep);
-    }
-    if (lane == 0) {
-      s_excl_s = es;
-      s_excl_p = ep;
-      out.toff[2 * tile] = es;
-      out.toff[2 * tile + 1] = ep;
-      if (tile == ntiles - 1) {
-        out.toff[2 * ntiles] = es + agg_s;
-        out.toff[2 * ntiles + 1] = ep + agg_p;
-      }
-      uint32_t e = s_err;
-      if (es + agg_s > out.sign_cap || ep + agg_p > out.payload_cap) e |= HSZ_ERR_CAPACITY;
-      s_err = e;
-      if (e) atomicOr(out.err, e);
-    }
-  }
-  __syncthreads();
-  if (s_err & HSZ_ERR_CAPACITY) return;
-
-  if (fast) {
-    // ---- stream the packed tile out (coalesced; 16-byte when aligned) ---
-    const uint64_t gs = s_excl_s, gp = s_excl_p;
-    uint32_t* dsg = reinterpret_cast<uint32_t*>(out.signs + gs);
-    const uint32_t nsw = (tile_s + 3) >> 2, npw = (tile_p + 3) >> 2;
-    for (uint32_t i = threadIdx.x; i < nsw; i += kThreads) dsg[i] = sm_sign[i];
-    uint32_t* dpy = reinterpret_cast<uint32_t*>(out.payload + gp);
-    uint32_t head = 0;
-    if ((gp & 15) == 0) {
-      const uint32_t nv = npw >> 2;
-      uint4* dv = reinterpret_cast<uint4*>(dpy);
-      const uint4* sv = reinterpret_cast<const uint4*>(words);
-      for (uint32_t i = threadIdx.x; i < nv; i += kThreads) dv[i] = sv[i];
-      head = nv << 2;
-    }
-    for (uint32_t i = head + threadIdx.x; i < npw; i += kThreads) dpy[i] = words[i];
-    return;
-  }
-  // ---- fallback pass 2: recompute each block, pack, write at its offset --
-  uint64_t gs = s_excl_s, gp = s_excl_p;
-  for (int i = 0; i < warp; ++i) {
-    gs += s_wsb[i];
-    gp += s_wpb[i];
-  }
-  uint32_t* wscr = scratch + warp * 64;
+template <class Src>
+__device__ __noinline__ void fallback_pack(Src src, EncodeOut out, uint64_t tile,
+                                           uint64_t nblocks, uint32_t tail_len, uint64_t gs,
+                                           uint64_t gp, uint32_t* wscr) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t blk0 = tile * TB + warp * BPW;
   for (int j = 0; j < BPW; ++j) {
     const uint64_t b = blk0 + j;
@@ -723,6 +690,284 @@ __global__ void __launch_bounds__(kThreads, Src::kMinBlocks) encode_kernel(Src s
     __syncwarp();
     gp += (len * w + 7) >> 3;
   }
+}
+
+template <class Src>
+struct EncodeSmem {
+  // [staged input | int32 bin rows | 2 x (packed payload | sign words) | fallback scratch]
+  static constexpr uint32_t kStage = (Src::kStageBytes + 15) & ~15u;
+  static constexpr uint32_t kRows = TB * kRow * 4;
+  static constexpr uint32_t kPackedCap = 8192;              // payload bytes per staged tile
+  static constexpr uint32_t kBuf = kPackedCap + TB * 4;     // + sign words
+  static constexpr uint32_t kScratch = kCtaWarps * 64 * 4;  // fallback: one block per warp
+  static constexpr uint32_t kBytes = kStage + kRows + 2 * kBuf + kScratch;
+};
+
+// Persistent, warp-specialised single-pass encoder.  A CTA = 4 compute warps
+// (one thread per block of a 128-block tile) + 1 store warp.  Compute warps
+// loop over tiles drawn from the ticket counter (always one ticket ahead):
+//   rows(t) [TMA-staged input, prefetched during the previous iteration]
+//   -> issue the TMA prefetch of the next tile into the freed stage
+//   -> widths / outliers / sizes of t, CTA scan, publish t's aggregate
+//   -> pack t into one of two staging buffers and hand it to the store warp.
+// The store warp resolves each handed-over tile's look-back prefix and
+// streams its sections out (16-byte stores), then releases the buffer -- the
+// look-back latency overlaps the next tile's compute.  Tiles whose packed
+// payload exceeds a staging buffer, and exact-path (fallback) tiles, are
+// resolved and written by the compute warps themselves.
+constexpr int kEncThreads = kThreads + 32;
+
+template <class Src>
+__global__ void __launch_bounds__(kEncThreads, Src::kMinBlocks) encode_kernel(Src src, EncodeOut out,
+                                                                              uint64_t nblocks,
+                                                                              uint64_t ntiles,
+                                                                              uint32_t tail_len) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  using L = EncodeSmem<Src>;
+  unsigned char* stage = sm;
+  int32_t* rows = reinterpret_cast<int32_t*>(sm + L::kStage);
+  unsigned char* bufs = sm + L::kStage + L::kRows;
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(sm + L::kStage + L::kRows + 2 * L::kBuf);
+  __shared__ uint64_t s_bar, s_full[2], s_empty[2];
+  __shared__ uint64_t s_next, s_epoch, s_excl_s, s_excl_p;
+  __shared__ uint64_t s_hand_tile[2];           // handed-over tile (~0 = stop)
+  __shared__ uint32_t s_hand_s[2], s_hand_p[2];
+  __shared__ uint32_t s_tmp[8];
+  __shared__ uint32_t s_wsb[kCtaWarps], s_wpb[kCtaWarps];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  LookbackWs lw = LookbackWs::bind(out.ws, ntiles);
+  const uint64_t last_draw = ntiles + gridDim.x - 1;   // every CTA draws once past the end
+  Stager st;
+  st.init(&s_bar);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 1);
+    }
+    fence_mbar_init();
+    const uint64_t e = ld_acquire(lw.epoch);
+    const uint64_t t = atom_add_acq_rel(lw.ticket, 1);
+    if (t == last_draw) {
+      st_relaxed(lw.ticket, 0);
+      st_release(lw.epoch, e + 1);
+    }
+    s_next = t;
+    s_epoch = e;
+  }
+  __syncthreads();
+  const uint64_t epoch = s_epoch;
+
+  if (warp == kCtaWarps) {
+    // ===================== store warp =====================
+    uint32_t fp[2] = {0, 0};
+    for (int b = 0;; b ^= 1) {
+      mbar_wait_parity(&s_full[b], fp[b]);
+      fp[b] ^= 1u;
+      const uint64_t t = s_hand_tile[b];
+      if (t == ~0ull) break;
+      const uint32_t ts = s_hand_s[b], tp = s_hand_p[b];
+      const uint32_t* packed = reinterpret_cast<const uint32_t*>(bufs + b * L::kBuf);
+      const uint32_t* sgn = reinterpret_cast<const uint32_t*>(bufs + b * L::kBuf + L::kPackedCap);
+      uint64_t es, ep;
+      resolve_prefix(lw, t, epoch, ts, tp, &es, &ep);
+      const bool fits = es + ts <= out.sign_cap && ep + tp <= out.payload_cap;
+      if (lane == 0) {
+        out.toff[2 * t] = es;
+        out.toff[2 * t + 1] = ep;
+        if (t == ntiles - 1) {
+          out.toff[2 * ntiles] = es + ts;
+          out.toff[2 * ntiles + 1] = ep + tp;
+        }
+        if (!fits) atomicOr(out.err, HSZ_ERR_CAPACITY);
+      }
+      if (fits) {
+        uint32_t* dsg = reinterpret_cast<uint32_t*>(out.signs + es);
+        const uint32_t nsw = (ts + 3) >> 2, npw = (tp + 3) >> 2;
+        for (uint32_t i = lane; i < nsw; i += 32) dsg[i] = sgn[i];
+        uint32_t* dpy = reinterpret_cast<uint32_t*>(out.payload + ep);
+        uint32_t head = static_cast<uint32_t>(((16 - (ep & 15)) & 15) >> 2);
+        head = head < npw ? head : npw;
+        for (uint32_t i = lane; i < head; i += 32) dpy[i] = packed[i];
+        // 16-byte stores from the first 16-byte aligned global word on
+        const uint32_t nv = (npw - head) >> 2;
+        uint4* dv = reinterpret_cast<uint4*>(dpy + head);
+        for (uint32_t i = lane; i < nv; i += 32) {
+          const uint32_t k = head + 4 * i;
+          dv[i] = make_uint4(packed[k], packed[k + 1], packed[k + 2], packed[k + 3]);
+        }
+        for (uint32_t i = head + 4 * nv + lane; i < npw; i += 32) dpy[i] = packed[i];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[b]);
+    }
+    return;
+  }
+
+  // ===================== compute warps =====================
+  uint64_t tile = s_next;
+  uint32_t flags = 0;
+  uint32_t ep_parity[2] = {1, 1};               // both staging buffers start empty
+  int buf = 0;
+  if (tile < ntiles) src.issue(tile, stage, st, s_tmp, &flags);
+  // one ticket ahead: thread 0 fetches the ticket after `tile` now
+  uint64_t ahead = 0;
+  if (threadIdx.x == 0 && tile < ntiles) ahead = atom_add_acq_rel(lw.ticket, 1);
+
+  // resolve a tile in place (compute warps) and return its exclusive offsets
+  auto resolve_here = [&](uint64_t t, uint32_t agg_s, uint32_t agg_p, bool published) -> bool {
+    if (warp == 0) {
+      uint64_t es, ep;
+      if (published) {
+        resolve_prefix(lw, t, epoch, agg_s, agg_p, &es, &ep);
+      } else {
+        lookback(lw, t, epoch, agg_s, agg_p, &es, &ep);
+      }
+      if (lane == 0) {
+        s_excl_s = es;
+        s_excl_p = ep;
+        out.toff[2 * t] = es;
+        out.toff[2 * t + 1] = ep;
+        if (t == ntiles - 1) {
+          out.toff[2 * ntiles] = es + agg_s;
+          out.toff[2 * ntiles + 1] = ep + agg_p;
+        }
+        if (es + agg_s > out.sign_cap || ep + agg_p > out.payload_cap) {
+          atomicOr(out.err, HSZ_ERR_CAPACITY);
+          s_excl_s = ~0ull;
+        }
+      }
+    }
+    grp_sync();
+    return s_excl_s != ~0ull;
+  };
+
+  while (tile < ntiles) {
+    trace(1);
+    const bool fast = src.rows(stage, st, rows, &flags);   // CTA-uniform, ends with a barrier
+    trace(2);
+    // the ticket drawn one iteration ago becomes `next`; draw the one after
+    if (threadIdx.x == 0) {
+      if (ahead == last_draw) {
+        st_relaxed(lw.ticket, 0);
+        st_release(lw.epoch, epoch + 1);
+      }
+      s_next = ahead;
+    }
+    grp_sync();
+    const uint64_t next = s_next;
+    if (threadIdx.x == 0 && next < ntiles) ahead = atom_add_acq_rel(lw.ticket, 1);
+    if (fast) {
+      if (next < ntiles) src.issue(next, stage, st, s_tmp, &flags);   // prefetch
+      // ---- thread-per-block: residuals, width, sign word -----------------
+      const int b = threadIdx.x;
+      const uint64_t gb = tile * TB + b;
+      const bool active = gb < nblocks;
+      const int len = active ? ((gb == nblocks - 1) ? static_cast<int>(tail_len) : K) : 0;
+      const int32_t* row = rows + b * kRow;
+      uint32_t mx = 0, sbits = 0;
+      const int32_t first = row[0];
+      {
+        int32_t prev = first;
+#pragma unroll
+        for (int i = 1; i < K; ++i) {
+          const int32_t q = row[i];
+          const int32_t dlt = q - prev;      // |q| < 2^30: no overflow
+          prev = q;
+          const bool live = i < len;
+          mx |= live ? static_cast<uint32_t>(dlt < 0 ? -dlt : dlt) : 0u;   // bitlen(OR) == bitlen(max)
+          sbits |= (live && dlt < 0) ? (1u << (31 - i)) : 0u;
+        }
+      }
+      const uint32_t w = mx ? 32 - __clz(mx) : 0;
+      const uint32_t sb = (active && w) ? (len + 7) >> 3 : 0;
+      const uint32_t pb = active ? (len * w + 7) >> 3 : 0;
+      uint32_t es, ep, tile_s, tile_p;
+      scan2(sb, pb, &es, &ep, &tile_s, &tile_p, s_tmp);
+      if (threadIdx.x == 0) publish_aggregate(lw, tile, epoch, tile_s, tile_p);
+      if (active) {
+        out.widths[gb] = static_cast<uint8_t>(w);
+        out.outliers[gb] = first;
+      }
+      trace(3);
+      const bool staged = tile_p <= L::kPackedCap;   // CTA-uniform
+      uint32_t* dst;
+      uint32_t* sgn;
+      if (staged) {
+        mbar_wait_parity(&s_empty[buf], ep_parity[buf]);   // buffer streamed out
+        ep_parity[buf] ^= 1u;
+        dst = reinterpret_cast<uint32_t*>(bufs + buf * L::kBuf) + (ep >> 2);
+        sgn = reinterpret_cast<uint32_t*>(bufs + buf * L::kBuf + L::kPackedCap);
+      } else {
+        // rare: a very wide tile -- resolve here, pack straight to global
+        const bool ok = resolve_here(tile, tile_s, tile_p, true);
+        dst = ok ? reinterpret_cast<uint32_t*>(out.payload + s_excl_p + ep) : nullptr;
+        sgn = ok ? reinterpret_cast<uint32_t*>(out.signs + s_excl_s) : nullptr;
+      }
+      trace(4);
+      if (w && dst) {
+        // second walk: MSB-first w-bit fields through a 64-bit shift register
+        sgn[es >> 2] = bswap32(sbits);
+        uint64_t acc = 0;
+        int nb = w, wi = 0;                // slot 0: a zero field
+        int32_t prev = first;
+#pragma unroll
+        for (int i = 1; i < K; ++i) {
+          const int32_t q = row[i];
+          const int32_t dlt = q - prev;
+          prev = q;
+          const uint32_t m = (i < len) ? static_cast<uint32_t>(dlt < 0 ? -dlt : dlt) : 0u;
+          acc = (acc << w) | m;
+          nb += w;
+          if (nb >= 32) {
+            nb -= 32;
+            dst[wi++] = bswap32(static_cast<uint32_t>(acc >> nb));
+          }
+        }
+      }
+      grp_sync();                           // packed tile complete; rows free
+      trace(5);
+      if (staged && threadIdx.x == 0) {
+        s_hand_tile[buf] = tile;
+        s_hand_s[buf] = tile_s;
+        s_hand_p[buf] = tile_p;
+        mbar_arrive(&s_full[buf]);
+      }
+      if (staged) buf ^= 1;
+    } else {
+      // ---- fallback tile: exact path, resolved here ------------------------
+      flags |= fallback_sizes(src, out, tile, nblocks, tail_len, s_wsb, s_wpb);
+      grp_sync();
+      const uint32_t agg_s = s_wsb[0] + s_wsb[1] + s_wsb[2] + s_wsb[3];
+      const uint32_t agg_p = s_wpb[0] + s_wpb[1] + s_wpb[2] + s_wpb[3];
+      if (resolve_here(tile, agg_s, agg_p, false)) {
+        uint64_t gs = s_excl_s, gp = s_excl_p;
+        for (int i = 0; i < warp; ++i) {
+          gs += s_wsb[i];
+          gp += s_wpb[i];
+        }
+        fallback_pack(src, out, tile, nblocks, tail_len, gs, gp, scratch + warp * 64);
+      }
+      grp_sync();
+      if (next < ntiles) src.issue(next, stage, st, s_tmp, &flags);
+    }
+    tile = next;
+  }
+  // stop the store warp after it has drained both buffers
+  for (int i = 0; i < 2; ++i) {
+    mbar_wait_parity(&s_empty[buf], ep_parity[buf]);
+    ep_parity[buf] ^= 1u;
+    if (i == 0) {
+      grp_sync();
+      if (threadIdx.x == 0) {
+        s_hand_tile[buf] = ~0ull;
+        mbar_arrive(&s_full[buf]);
+      }
+    }
+    buf ^= 1;
+  }
+  flags = __reduce_or_sync(kFull, flags);
+  if (lane == 0 && flags) atomicOr(out.err, flags);
 }
 
 // ---------------------------------------------------------------------------
@@ -780,6 +1025,20 @@ struct SinkBins {
   __device__ __forceinline__ T* base() const { return out; }
 };
 
+template <class Sink, typename T>
+__device__ __noinline__ uint32_t fallback_decode(TileIn t, Sink sink, T* ot) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t flags = 0;
+  for (int j = 0; j < BPW; ++j) {
+    const int lb = warp * BPW + j;
+    const LaneBlock m = lane_block(t, j);
+    if (m.len == 0) break;
+    const int64_t q = decode_lane(t.sgn, t.pay, m.w, m.o, m.soff, m.poff, m.len, lane, &flags);
+    ot[pad(lb, lane)] = sink.value(q, &flags);
+  }
+  return flags;
+}
+
 template <class Sink>
 struct DecodeSmem {
   static constexpr uint32_t kOut = TB * kRow * sizeof(typename Sink::T);
@@ -811,13 +1070,7 @@ __global__ void __launch_bounds__(kThreads, Sink::kMinBlocks) decode_kernel(Stre
 #pragma unroll
     for (int i = 0; i < K; ++i) ot[pad(threadIdx.x, i)] = v[i];
   } else {
-    for (int j = 0; j < BPW; ++j) {
-      const int lb = warp * BPW + j;
-      const LaneBlock m = lane_block(t, j);
-      if (m.len == 0) break;
-      const int64_t q = decode_lane(t.sgn, t.pay, m.w, m.o, m.soff, m.poff, m.len, lane, &flags);
-      ot[pad(lb, lane)] = sink.value(q, &flags);
-    }
+    flags |= fallback_decode(t, sink, ot);
   }
   __syncthreads();
   // coalesced store of the tile
@@ -873,10 +1126,23 @@ __device__ __forceinline__ Acc shfl_xor_acc(const Acc& a, int m) {
   return r;
 }
 
-// Partials live in the workspace "vals" area: 6 u64 per CTA.  The last CTA
-// to finish (done counter) reduces them and writes out[5].
-__device__ __forceinline__ void finish_moments(Acc acc, uint64_t ntiles, void* ws,
-                                               uint64_t* out) {
+// Cross-CTA reduction without a serial tail: every CTA adds its S (int128,
+// two's complement) and Q (uint192) as 32-bit chunks into ten u64
+// carry-save counters in the workspace (ws[8..18); a chunk < 2^32, so 2^32
+// CTAs cannot overflow a counter).  The last CTA to finish folds the
+// counters into exact 128/192-bit values, writes out[5] and re-zeroes them.
+__device__ __forceinline__ void add_shifted(uint64_t* L, int nl, uint64_t c, int bit) {
+  // L (nl little-endian u64 limbs) += c << bit
+  const int li = bit >> 6, sh = bit & 63;
+  unsigned __int128 v = static_cast<unsigned __int128>(c) << sh;
+  for (int i = li; i < nl && v; ++i) {
+    const unsigned __int128 sum = static_cast<unsigned __int128>(L[i]) + static_cast<uint64_t>(v);
+    L[i] = static_cast<uint64_t>(sum);
+    v = (v >> 64) + (sum >> 64);
+  }
+}
+
+__device__ __forceinline__ void finish_moments(Acc acc, uint64_t, void* ws, uint64_t* out) {
   __shared__ Acc s_acc[32];
   __shared__ bool s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -886,49 +1152,48 @@ __device__ __forceinline__ void finish_moments(Acc acc, uint64_t ntiles, void* w
   __syncthreads();
   uint64_t* base = static_cast<uint64_t*>(ws);
   uint64_t* done = base + 2;
-  uint64_t* part = base + kWsFlagsOff + ntiles;   // vals area
+  uint64_t* cs = base + 8;
   if (threadIdx.x == 0) {
     Acc t = s_acc[0];
     for (int i = 1; i < nw; ++i) t.merge(s_acc[i]);
-    uint64_t* p = part + 6 * blockIdx.x;
-    p[0] = static_cast<uint64_t>(t.s);
-    p[1] = static_cast<uint64_t>(static_cast<unsigned __int128>(t.s) >> 64);
-    p[2] = static_cast<uint64_t>(t.q);
-    p[3] = static_cast<uint64_t>(t.q >> 64);
-    p[4] = t.q2;
+    const unsigned __int128 su = static_cast<unsigned __int128>(t.s);
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t ch = static_cast<uint64_t>(su >> (32 * k)) & 0xffffffffull;
+      if (ch) atomicAdd(reinterpret_cast<unsigned long long*>(cs + k), ch);
+    }
+    for (int k = 0; k < 6; ++k) {
+      const uint64_t ch = (k < 4) ? static_cast<uint64_t>(t.q >> (32 * k)) & 0xffffffffull
+                                  : (t.q2 >> (32 * (k - 4))) & 0xffffffffull;
+      if (ch) atomicAdd(reinterpret_cast<unsigned long long*>(cs + 4 + k), ch);
+    }
     __threadfence();
-    const uint64_t prev = atom_add_acq_rel(done, 1);
-    s_last = (prev == gridDim.x - 1);
+    s_last = atom_add_acq_rel(done, 1) == gridDim.x - 1;
+    if (s_last) {
+      __threadfence();
+      uint64_t S[2] = {0, 0}, Q[4] = {0, 0, 0, 0};
+      for (int k = 0; k < 4; ++k) add_shifted(S, 2, ld_relaxed(cs + k), 32 * k);
+      for (int k = 0; k < 6; ++k) add_shifted(Q, 4, ld_relaxed(cs + 4 + k), 32 * k);
+      out[0] = S[0];
+      out[1] = S[1];
+      out[2] = Q[0];
+      out[3] = Q[1];
+      out[4] = Q[2];
+      for (int k = 0; k < 10; ++k) st_relaxed(cs + k, 0);
+      st_relaxed(done, 0);   // rearm for the next launch on this workspace
+    }
   }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  Acc tot;
-  tot.s = 0;
-  tot.q = 0;
-  tot.q2 = 0;
-  for (uint64_t i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
-    const uint64_t* p = part + 6 * i;
-    Acc a;
-    a.s = static_cast<__int128>((static_cast<unsigned __int128>(ld_relaxed(p + 1)) << 64) | ld_relaxed(p));
-    a.q = (static_cast<unsigned __int128>(ld_relaxed(p + 3)) << 64) | ld_relaxed(p + 2);
-    a.q2 = ld_relaxed(p + 4);
-    tot.merge(a);
+}
+
+__device__ __noinline__ uint32_t fallback_moments(TileIn t, Acc* acc, bool want_sq) {
+  const int lane = threadIdx.x & 31;
+  uint32_t flags = 0;
+  for (int j = 0; j < BPW; ++j) {
+    const LaneBlock m = lane_block(t, j);
+    if (m.len == 0) break;
+    const int64_t q = decode_lane(t.sgn, t.pay, m.w, m.o, m.soff, m.poff, m.len, lane, &flags);
+    if (lane < m.len) acc->add(q, want_sq);
   }
-  for (int m = 16; m > 0; m >>= 1) tot.merge(shfl_xor_acc(tot, m));
-  __syncthreads();
-  if (lane == 0) s_acc[warp] = tot;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    Acc t = s_acc[0];
-    for (int i = 1; i < nw; ++i) t.merge(s_acc[i]);
-    out[0] = static_cast<uint64_t>(t.s);
-    out[1] = static_cast<uint64_t>(static_cast<unsigned __int128>(t.s) >> 64);
-    out[2] = static_cast<uint64_t>(t.q);
-    out[3] = static_cast<uint64_t>(t.q >> 64);
-    out[4] = t.q2;
-    st_relaxed(done, 0);   // rearm for the next launch on this workspace
-  }
+  return flags;
 }
 
 template <bool kWantSq>
@@ -971,12 +1236,7 @@ __global__ void __launch_bounds__(kThreads) moments_kernel(StreamIn s, uint64_t*
       acc.q = static_cast<unsigned __int128>(tot);
     }
   } else {
-    for (int j = 0; j < BPW; ++j) {
-      const LaneBlock m = lane_block(t, j);
-      if (m.len == 0) break;
-      const int64_t q = decode_lane(t.sgn, t.pay, m.w, m.o, m.soff, m.poff, m.len, lane, &flags);
-      if (lane < m.len) acc.add(q, kWantSq);
-    }
+    flags |= fallback_moments(t, &acc, kWantSq);
   }
   flags = __reduce_or_sync(kFull, flags);
   if (lane == 0 && flags) atomicOr(err, flags);

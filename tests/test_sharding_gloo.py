@@ -1,0 +1,123 @@
+"""Multi-rank path on CPU (gloo, world_size 2 and 3): contiguous block-range
+sharding + the three collectives (C1 global range, C2 global section
+offsets, C3 exact moments).  The per-shard codec here is the CPU oracle (the
+GPU kernels are covered by the -m gpu suite); what is under test is the
+partitioning and collective logic of paper_2408_11971_b200/sharding.py:
+the concatenated shards must equal the single-process stream byte for byte,
+and mean / variance must be bit-identical for any rank count."""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _field(n, seed=3):
+    rng = np.random.default_rng(seed)
+    return (np.cumsum(rng.normal(0, 0.3, n)) + 280).astype(np.float32)
+
+
+def _worker(rank, world, port, n, rel, outdir):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import torch.distributed as dist
+
+    import hoszp_oracle as O
+    from paper_2408_11971_b200.sharding import Collectives, element_range
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        coll = Collectives()
+        x = _field(n)
+        k = 32
+        e0, e1 = element_range(n, k, rank, world)
+        xs = x[e0:e1]
+        lo, hi = coll.global_range(float(xs.min()), float(xs.max()))     # C1
+        eps = float(rel) * (hi - lo)
+        s = O.compress(xs, eps, (xs.size,), k, "f32")
+        lay = coll.global_offsets(e0 // k, len(s["signs"]), len(s["payload"]))   # C2
+        S, Q = O.moments(s)
+        St, Qt = coll.global_moments(S, Q)                                # C3
+        parts = [None] * world
+        dist.all_gather_object(parts, (lay.__dict__, s["widths"].tobytes(),
+                                       np.asarray(s["outliers"], np.int64).tobytes(),
+                                       s["signs"], s["payload"], St, Qt, eps))
+        if rank == 0:
+            np.save(os.path.join(outdir, "parts.npy"), np.array(parts, dtype=object),
+                    allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_equals_single_process(tmp_path, world):
+    import torch.multiprocessing as mp
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import hoszp_oracle as O
+    from paper_2408_11971_b200 import sharding
+
+    n, rel = 32 * 997 + 13, 1e-4
+    mp.spawn(_worker, args=(world, _free_port(), n, rel, str(tmp_path)), nprocs=world, join=True)
+    parts = list(np.load(tmp_path / "parts.npy", allow_pickle=True))
+    x = _field(n)
+    eps = O.resolve_eps(x, rel, "rel")
+    ref = O.compress(x, eps, (n,), 32, "f32")
+    assert all(p[7] == eps for p in parts)                       # C1: identical eps everywhere
+    widths = b"".join(p[1] for p in parts)
+    outl = np.concatenate([np.frombuffer(p[2], np.int64) for p in parts])
+    signs = b"".join(p[3] for p in parts)
+    payload = b"".join(p[4] for p in parts)
+    assert widths == ref["widths"].tobytes()
+    assert np.array_equal(outl, ref["outliers"])
+    assert signs == ref["signs"] and payload == ref["payload"]
+    # C2 offsets are the prefix sums of the shard sections
+    acc_s = acc_p = 0
+    for p in parts:
+        lay = p[0]
+        assert lay["sign_offset"] == acc_s and lay["payload_offset"] == acc_p
+        assert lay["sign_total"] == len(ref["signs"]) and lay["payload_total"] == len(ref["payload"])
+        acc_s += len(p[3])
+        acc_p += len(p[4])
+    # C3: exact global moments -> bit-identical mean / variance
+    S, Q = O.moments(ref)
+    assert all((p[5], p[6]) == (S, Q) for p in parts)
+    assert O.mean_from(parts[0][5], n, eps) == O.mean(ref)
+    assert O.variance_from(parts[0][5], parts[0][6], n, eps) == O.variance(ref)
+
+
+def test_block_ranges_partition_exactly():
+    from paper_2408_11971_b200.sharding import block_range, element_range
+
+    for nb in (1, 7, 128, 1000, 781250):
+        for world in (1, 2, 3, 4, 8):
+            spans = [block_range(nb, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == nb
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            sizes = [b - a for a, b in spans]
+            assert max(sizes) - min(sizes) <= 1
+    # every shard boundary is block aligned; the tail block is the last shard's
+    n = 32 * 10 + 5
+    ranges = [element_range(n, 32, r, 3) for r in range(3)]
+    assert all(a % 32 == 0 for a, _ in ranges) and ranges[-1][1] == n
+
+
+def test_limb_packing_round_trip():
+    from paper_2408_11971_b200.sharding import _from_limbs, _to_limbs
+
+    for S, Q in ((0, 0), (-5, 7), (-(2 ** 120), 2 ** 191 - 1), (2 ** 126, 2 ** 64)):
+        assert _from_limbs(_to_limbs(S, Q)) == (S, Q)
