@@ -26,7 +26,10 @@
  *    their capacity (kernels read/write whole 32-bit words at the end);
  *  - `ws` is a per-stream workspace of hsz_workspace_size() bytes, zeroed
  *    once with hsz_workspace_init(); it is reused across calls on the same
- *    CUDA stream (never concurrently from two streams).
+ *    CUDA stream (never concurrently from two streams).  Encoders tag their
+ *    look-back words with 24 bits of a launch epoch kept in the workspace:
+ *    re-initialise it at least every 2^23 calls (the Python layer does so
+ *    every 2^22).
  */
 #ifndef HSZ_B200_H
 #define HSZ_B200_H
@@ -162,6 +165,8 @@ const char* hsz_version(void);
 
 /* debug builds (-DHSZ_TRACE): copy out per-CTA phase timestamps; -1 otherwise */
 int hsz_trace_read(unsigned long long* host, int cap, int reset);
+/* debug builds: look-back (rounds, sleeps, resolves) since the last call; -1 otherwise */
+int hsz_trace_lookback(unsigned int* out3);
 
 #ifdef __cplusplus
 }

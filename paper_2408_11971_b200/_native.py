@@ -31,6 +31,7 @@ _dbl = C.c_double
 SIGNATURES = {
     "hsz_version": (C.c_char_p, []),
     "hsz_trace_read": (_int, [_vp, _int, _int]),
+    "hsz_trace_lookback": (_int, [_vp]),
     "hsz_tile_count": (_u64, [_u64, _u32]),
     "hsz_sign_bound": (_u64, [_u64, _u32]),
     "hsz_payload_bound": (_u64, [_u64, _u32]),

@@ -32,6 +32,7 @@ from .device import (
     DTYPE_CODE,
     DeviceStream,
     context,
+    download,
     ptr,
     require_cuda,
     run_encoder,
@@ -98,7 +99,7 @@ class RawArray:
 
     def numpy(self) -> np.ndarray:
         if self._host is None:
-            return self._dev.cpu().numpy()
+            return download([self._dev])[0]
         return self._host
 
     def device_values(self, ctx=None):
@@ -200,7 +201,7 @@ def quantize(raw: RawArray, params: QuantParams) -> QuantArray:
     if raw.on_device:
         return QuantArray(bins, params)
     ctx.check("quantize")
-    return QuantArray(bins.cpu().numpy(), params)
+    return QuantArray(download([bins], ctx)[0], params)
 
 
 def dequantize(q: QuantArray) -> RawArray:
@@ -215,7 +216,7 @@ def dequantize(q: QuantArray) -> RawArray:
     if q.on_device:
         return RawArray(out, p.dims, p.dtype, _validated=True)
     ctx.check("dequantize")
-    return RawArray(out.cpu().numpy(), p.dims, p.dtype, _validated=True)
+    return RawArray(download([out], ctx)[0], p.dims, p.dtype, _validated=True)
 
 
 # ---------------------------------------------------------------------------
@@ -271,7 +272,7 @@ def decompress(stream, threads: int = 1, out_dtype=None) -> RawArray:
     if isinstance(stream, DeviceStream):
         return RawArray(out, p.dims, dtype, _validated=True)
     ds.ctx.check("decompress")
-    return RawArray(out.cpu().numpy(), p.dims, dtype, _validated=True)
+    return RawArray(download([out], ds.ctx)[0], p.dims, dtype, _validated=True)
 
 
 def decode_to_quant(stream, threads: int = 1) -> QuantArray:
@@ -281,7 +282,7 @@ def decode_to_quant(stream, threads: int = 1) -> QuantArray:
     if isinstance(stream, DeviceStream):
         return QuantArray(bins, ds.params)
     ds.ctx.check("decode_to_quant")
-    return QuantArray(bins.cpu().numpy(), ds.params)
+    return QuantArray(download([bins], ds.ctx)[0], ds.params)
 
 
 def encode_from_quant(q: QuantArray, threads: int = 1):

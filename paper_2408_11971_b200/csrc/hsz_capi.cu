@@ -6,8 +6,12 @@
 //        -Xcompiler -fPIC -o paper_2408_11971_b200/_lib/libhsz_b200.so hsz_capi.cu
 
 #include <cstdio>
+#include <cstring>
+
+#include <cudaTypedefs.h>
 
 #include "hsz_common.cuh"
+#include "hsz_enc32.cuh"
 #include "hsz_generic.cuh"
 #include "hsz_k32.cuh"
 #include "hsz_quant.cuh"
@@ -263,6 +267,66 @@ static int launch_encode32(Src src, const k32::EncodeOut& out, uint64_t n, cudaS
   return launch_status();
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// compress of a float32 field, block_len 32: register-resident encoder with
+// a swizzled 2-D TMA tile load when the field allows it
+static int launch_compress_f32(const float* x, uint64_t n, const QuantConst& c,
+                               const k32::EncodeOut& out, cudaStream_t st) {
+  const uint64_t nb = ceil_div(n, 32);
+  const uint64_t nt = ceil_div(nb, kTileBlocks);
+  const e32::QuantF32 qf = e32::make_quant_f32(c);
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  bool tma = false;
+  const uint64_t rows = n / 32;
+  if ((reinterpret_cast<uintptr_t>(x) & 15u) == 0 && rows >= static_cast<uint64_t>(kTileBlocks) &&
+      rows < (1ull << 31)) {
+    if (auto enc = tensor_map_encoder()) {
+      cuuint64_t dims[2] = {32, rows};
+      cuuint64_t strides[1] = {128};
+      cuuint32_t box[2] = {32, static_cast<cuuint32_t>(kTileBlocks)};
+      cuuint32_t estr[2] = {1, 1};
+      tma = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(x), dims, strides, box,
+                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+  }
+  constexpr int smem = static_cast<int>(e32::kSmemBytes);
+  auto kern = tma ? e32::compress_f32_kernel<true> : e32::compress_f32_kernel<false>;
+  // persistent grid: every CTA resident (the look-back relies on it)
+  static int resident[2] = {0, 0}, resident_dev[2] = {-1, -1};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (resident_dev[tma] != dev) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, e32::kThreadsWS, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    resident[tma] = (per_sm > 0 ? per_sm : 1) * sms;
+    resident_dev[tma] = dev;
+  }
+  const uint64_t grid = nt < static_cast<uint64_t>(resident[tma]) ? nt : static_cast<uint64_t>(resident[tma]);
+  kern<<<static_cast<unsigned>(grid), e32::kThreadsWS, smem, st>>>(map, x, n, qf, c, out, nb, nt,
+                                                                tail_len_of(n, 32));
+  return launch_status();
+}
+
 template <class G>
 static int launch_encode_generic(G src, uint64_t n, uint32_t k, uint8_t* widths,
                                  int32_t* outliers, uint8_t* signs, uint64_t sign_cap,
@@ -353,6 +417,26 @@ int hsz_trace_read(unsigned long long* host, int cap, int reset) {
 #endif
 }
 
+// debug: look-back statistics since the last call (rounds, sleeps, resolves)
+int hsz_trace_lookback(unsigned int* out3) {
+#ifdef HSZ_TRACE
+  cudaDeviceSynchronize();
+  unsigned int v[3] = {0, 0, 0};
+  cudaMemcpyFromSymbol(&v[0], g_lb_rounds, sizeof(unsigned));
+  cudaMemcpyFromSymbol(&v[1], g_lb_sleeps, sizeof(unsigned));
+  cudaMemcpyFromSymbol(&v[2], g_lb_calls, sizeof(unsigned));
+  const unsigned int z = 0;
+  cudaMemcpyToSymbol(g_lb_rounds, &z, sizeof(z));
+  cudaMemcpyToSymbol(g_lb_sleeps, &z, sizeof(z));
+  cudaMemcpyToSymbol(g_lb_calls, &z, sizeof(z));
+  if (out3) for (int i = 0; i < 3; ++i) out3[i] = v[i];
+  return 3;
+#else
+  (void)out3;
+  return -1;
+#endif
+}
+
 uint64_t hsz_tile_count(uint64_t n, uint32_t k) {
   if (k == 0) return 0;
   return ceil_div(ceil_div(n, k), kTileBlocks);
@@ -369,9 +453,10 @@ uint64_t hsz_payload_bound(uint64_t n, uint32_t k) {
 }
 
 uint64_t hsz_workspace_size(uint64_t n, uint32_t k) {
-  const uint64_t nt = hsz_tile_count(n, k) + 1;
-  // header + minmax partials, then flags[nt] and vals[6*nt]
-  return 8 * (kWsFlagsOff + nt + 6 * nt);
+  const uint64_t nt = hsz_tile_count(n, k);
+  // header + minmax partials, then 8 words per tile: the look-back records
+  // (kLbStride words) or the flag/value protocol (7 words)
+  return 8 * (kWsFlagsOff + 8 * (nt + 1));
 }
 
 int hsz_workspace_init(void* ws, uint64_t ws_bytes, void* stream) {
@@ -410,7 +495,7 @@ int hsz_compress(const void* x, int dtype, uint64_t n, uint32_t k, double eps, u
   const QuantConst c = make_quant_const(eps);
   if (k == 32) {
     const k32::EncodeOut out{widths, outliers, signs, sign_cap, payload, payload_cap, toff, err, ws};
-    if (dtype == HSZ_F32) return launch_encode32(k32::SrcQuant<float>{static_cast<const float*>(x), n, c}, out, n, st);
+    if (dtype == HSZ_F32) return launch_compress_f32(static_cast<const float*>(x), n, c, out, st);
     return launch_encode32(k32::SrcQuant<double>{static_cast<const double*>(x), n, c}, out, n, st);
   }
   if (dtype == HSZ_F32)

@@ -31,8 +31,18 @@ __device__ __forceinline__ void trace(uint32_t tag) {
                                     (static_cast<unsigned long long>(tag) << 40) | (t & ((1ull << 40) - 1));
   }
 }
+// per-tile record: (tile << 40) | (tag << 32) | low 32 bits of globaltimer (ns)
+__device__ __forceinline__ void trace_tile(uint64_t tile, uint32_t tag) {
+  if (threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned i = atomicAdd(&g_trace_n, 1u);
+    if (i < kTraceCap) g_trace[i] = (tile << 40) | (static_cast<unsigned long long>(tag) << 32) | (t & 0xffffffffull);
+  }
+}
 #else
 __device__ __forceinline__ void trace(uint32_t) {}
+__device__ __forceinline__ void trace_tile(uint64_t, uint32_t) {}
 #endif
 
 constexpr int kWarp = 32;
@@ -303,6 +313,138 @@ __device__ __forceinline__ void lookback(LookbackWs& w, uint64_t tile, uint64_t 
   if ((threadIdx.x & 31) == 0) publish_aggregate(w, tile, epoch, agg_s, agg_p);
   __syncwarp();
   resolve_prefix(w, tile, epoch, agg_s, agg_p, excl_s, excl_p);
+}
+
+// ---------------------------------------------------------------------------
+// Fence-free decoupled look-back (register-resident encoders).
+//
+// One 16-byte record per tile in the workspace, {sign, payload}, written with
+// a single 16-byte store; each 8-byte half is self-validating:
+//   bit 63 = 1, bit 62 = inclusive (else aggregate), bits 61..39 = the low 23
+//   bits of the launch epoch, bits 38..0 = the value.
+// A reader accepts a record only if both halves carry the current epoch and
+// the same state, so it needs no acquire fence between a flag and its value.
+// (Words of the flag/value protocol above never have bit 63 set.  The epoch
+// tag repeats after 2^23 launches on one workspace: the host re-initialises
+// the workspace before that, see hsz_workspace_init.)
+constexpr int kLbValBits = 39;
+constexpr uint64_t kLbValMask = (1ull << kLbValBits) - 1;
+constexpr int kLbStride = 2;   // u64 words per tile record
+
+__device__ __forceinline__ uint64_t lb_tag(uint64_t epoch) {   // bits 63..39 of an aggregate
+  return (1ull << 24) | (epoch & 0x7FFFFFull);
+}
+constexpr uint64_t kLbIncBit = 1ull << 23;                      // in the tag: inclusive
+
+__device__ __forceinline__ void st_relaxed_v2(uint64_t* p, uint64_t a, uint64_t b) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_relaxed_v2(const uint64_t* p, uint64_t* a, uint64_t* b) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(*a), "=l"(*b) : "l"(p) : "memory");
+}
+
+__device__ __forceinline__ uint64_t* lb_words(void* ws) {
+  return static_cast<uint64_t*>(ws) + kWsFlagsOff;
+}
+
+// one thread: the tile's aggregate (tile 0: its inclusive prefix)
+__device__ __forceinline__ void lb_publish(uint64_t* words, uint64_t tile, uint64_t epoch,
+                                           uint64_t agg_s, uint64_t agg_p) {
+  const uint64_t t = (lb_tag(epoch) | (tile == 0 ? kLbIncBit : 0)) << kLbValBits;
+  st_relaxed_v2(words + kLbStride * tile, t | agg_s, t | agg_p);
+}
+
+#ifndef HSZ_LB2_PER_LANE
+#define HSZ_LB2_PER_LANE 4
+#endif
+
+#ifdef HSZ_TRACE
+__device__ unsigned int g_lb_rounds, g_lb_sleeps, g_lb_calls;
+#endif
+
+// one full warp: exclusive prefix of `tile` (its aggregate already published);
+// publishes the tile's inclusive prefix.  Each round inspects 32 * L tiles.
+__device__ __forceinline__ void lb_resolve(uint64_t* words, uint64_t tile, uint64_t epoch,
+                                           uint64_t agg_s, uint64_t agg_p, uint64_t* excl_s,
+                                           uint64_t* excl_p) {
+  constexpr int L = HSZ_LB2_PER_LANE;
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    *excl_s = 0;
+    *excl_p = 0;
+    return;
+  }
+  const uint64_t tag = lb_tag(epoch);
+  uint64_t sum_s = 0, sum_p = 0;
+  int64_t base = static_cast<int64_t>(tile) - 1;
+  unsigned backoff = 16;
+#ifdef HSZ_TRACE
+  unsigned rounds = 0, sleeps = 0;
+#endif
+  while (true) {
+#ifdef HSZ_TRACE
+    ++rounds;
+#endif
+    // lane covers tiles base - lane*L - j, j = 0..L-1 (nearest first).  All
+    // loads are issued before any is consumed (one L2 round trip per round).
+    uint64_t ra[L], rb[L];
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      const int64_t idx = base - (lane * L + j);
+      ld_relaxed_v2(words + kLbStride * (idx >= 0 ? idx : 0), &ra[j], &rb[j]);
+    }
+    uint64_t s = 0, p = 0;
+    bool found = false, invalid = false;
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      const bool real = base - (lane * L + j) >= 0;   // else: virtual inclusive 0 before tile 0
+      const uint64_t ta = ra[j] >> kLbValBits, tb = rb[j] >> kLbValBits;
+      const bool ok = !real || ((ta == tb) & ((ta & ~kLbIncBit) == tag));
+      const bool inc = !real || (ta & kLbIncBit) != 0;
+      const bool take = !found;
+      invalid |= take & !ok;
+      s += (take & real) ? (ra[j] & kLbValMask) : 0ull;
+      p += (take & real) ? (rb[j] & kLbValMask) : 0ull;
+      found |= ok & inc;
+    }
+    const unsigned fm = __ballot_sync(kFull, found);
+    const int first = fm ? (__ffs(fm) - 1) : 32;
+    // lanes up to and including the first one holding an inclusive must have
+    // read only valid records before (or at) their inclusive one
+    const bool bad = lane <= first && invalid;
+    if (__any_sync(kFull, bad)) {
+      __nanosleep(backoff);
+      backoff = backoff < 128 ? backoff * 2 : 128;
+#ifdef HSZ_TRACE
+      ++sleeps;
+#endif
+      continue;
+    }
+    if (lane > first) {
+      s = 0;
+      p = 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s += __shfl_xor_sync(kFull, s, o);
+      p += __shfl_xor_sync(kFull, p, o);
+    }
+    sum_s += s;
+    sum_p += p;
+    if (first < 32) break;
+    base -= 32 * L;
+  }
+  if (lane == 0) {
+    const uint64_t t = (tag | kLbIncBit) << kLbValBits;
+    st_relaxed_v2(words + kLbStride * tile, t | (sum_s + agg_s), t | (sum_p + agg_p));
+#ifdef HSZ_TRACE
+    atomicAdd(&g_lb_rounds, rounds);
+    atomicAdd(&g_lb_sleeps, sleeps);
+    atomicAdd(&g_lb_calls, 1u);
+#endif
+  }
+  *excl_s = sum_s;
+  *excl_p = sum_p;
 }
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,535 @@
+// Register-resident block_len-32 encoder (compress of float32 fields).
+//
+// A tile = 128 blocks (4096 elements); a CTA of 128 threads works on one tile
+// at a time and thread b owns block b, keeping its 32 bins in registers from
+// quantization to bit packing:
+//
+//   1. the tile (16 KB) arrives in shared memory by one TMA 2-D tensor load
+//      with the 128-byte swizzle, so thread b's eight 16-byte reads of its
+//      own 128-byte row hit eight different bank groups (conflict free);
+//      as soon as the registers hold it, the next tile's load is issued
+//      into the same buffer;
+//   2. certified float32 quantization (quant_f32 below) -- bit-identical to
+//      the reference's float64 floor((x + eps) / 2eps) + repair pass
+//      (codec.py:118-155) whenever its certificate holds, the exact float64
+//      path (hsz_quant.cuh quantize1) for the ~2^-20 of elements where it
+//      does not;
+//   3. Lorenzo residuals, OR-reduced width and the big-endian sign word
+//      (one funnel shift per element) in registers (codec.py:178-225);
+//   4. one 32-bit CTA scan of the (sign bytes, payload bytes) of the 128
+//      blocks; the tile aggregate is published for the decoupled look-back
+//      at once (fence-free tagged words, hsz_common.cuh lb_*);
+//   5. the PREVIOUS tile of this CTA is placed: warp 0 resolves its global
+//      offsets (its predecessors had a whole iteration to publish theirs, so
+//      the look-back rarely waits) and the CTA streams its staged sign words
+//      and payload out with 16-byte stores;
+//   6. MSB-first element-major packing (codec.py:280-286) of the current
+//      tile -- G = 4 / 2 / 1 fields combined per IMAD step, G chosen per warp
+//      from its widest block -- into the staging buffer (row-XOR swizzle).
+//
+// The grid is persistent (every CTA resident); tiles are handed out in order
+// by an atomic ticket drawn one tile ahead, so every wait of the look-back is
+// on a lower ticket whose owner can always progress.
+//
+// Tiles holding a bin with |bin| >= 2^30 (only possible for eps tiny against
+// the data) fall back to the exact warp-per-block encoder of hsz_k32.cuh.
+#pragma once
+
+#include <cuda.h>
+
+#include "hsz_common.cuh"
+#include "hsz_k32.cuh"
+#include "hsz_quant.cuh"
+
+namespace hsz {
+namespace e32 {
+
+constexpr int K = 32;
+constexpr int TB = kTileBlocks;                  // 128 blocks per tile
+constexpr int kThreads = TB;                     // one thread per block
+constexpr uint32_t kBufBytes = TB * K * 4;       // 16 KB: input tile, then packed payload
+constexpr uint32_t kMagicBits = 0x4B400000u;     // bits of 1.5 * 2^23
+constexpr float kMagicF = 12582912.0f;           // 1.5 * 2^23
+constexpr int64_t kWide = 1ll << 30;             // register path: |bin| < 2^30
+
+static_assert(kThreads == 128, "the CTA scan assumes 4 warps");
+
+// ---------------------------------------------------------------------------
+// certified float32 quantizer
+//
+// t = x/d + 1/2 (d = 2 eps); the reference returns floor(RN(RN(x + eps) / d))
+// (+ a repair pass).  With R = RN64(1/d) split as rh + rl (two floats):
+//   p = RN(x*rh), e = x*rh - p (exact FMA), m = floor(p), f = p - m,
+//   c = RN(x*rl + e), v = RN(RN(f - 1/2) + c)  ~  t - m - 1
+// |v - (t - m - 1)| < 2^-23 for |p| < 2^21 (error analysis in DESIGN.md), so
+// if |v| > delta = 2^-21 then t is at least 2^-22 away from the integer m + 1,
+// floor(t) = m + [v >= 0] equals the reference's floor (whose own error is
+// below 2^-31 here), and |x - d q| <= eps - d 2^-22 proves that the repair
+// pass of codec.py:140-154 does not fire.  Returns the bin offset by the
+// magic constant: bits(m + 1.5*2^23) + [v >= 0] = 0x4B400000 + floor(t).
+struct QuantF32 {
+  float rh, rl;
+  float delta;   // +inf disables the fast path (every element takes quantize1)
+};
+
+__host__ inline QuantF32 make_quant_f32(const QuantConst& c) {
+  QuantF32 q;
+  const double R = 1.0 / c.d;
+  q.rh = static_cast<float>(R);
+  q.rl = static_cast<float>(R - static_cast<double>(q.rh));
+  const bool ok = c.d >= 0x1p-60 && c.d <= 0x1p+60;
+  q.delta = ok ? 0x1p-21f : __builtin_huge_valf();
+  return q;
+}
+
+__device__ __forceinline__ uint32_t quant_f32(float x, const QuantF32& qf, bool& bad) {
+  const float p = __fmul_rn(x, qf.rh);
+  const float e = __fmaf_rn(x, qf.rh, -p);
+  const float m = floorf(p);
+  const float f = __fsub_rn(p, m);
+  const float c = __fmaf_rn(x, qf.rl, e);
+  const float v = __fadd_rn(__fsub_rn(f, 0.5f), c);
+  bad |= !((fabsf(v) > qf.delta) & (fabsf(p) < 2097152.0f));
+  const uint32_t mb = __float_as_uint(__fadd_rn(m, kMagicF));
+  return mb + 1u + static_cast<uint32_t>(__float_as_int(v) >> 31);
+}
+
+struct ExactQ {
+  int64_t q;
+  uint32_t flags;
+};
+
+__device__ __noinline__ ExactQ quant_exact(float x, QuantConst c) {
+  ExactQ r;
+  r.flags = 0;
+  r.q = quantize1(static_cast<double>(x), c, &r.flags);
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// shared memory
+
+struct Smem {
+  unsigned char in[kBufBytes];    // input tile (TMA 128B swizzle; 1024-aligned)
+  unsigned char pk[2][kBufBytes]; // packed payload of the staged tiles (word swizzle; by parity)
+  alignas(16) uint32_t sgn[2][TB];  // their sign words (compacted)
+  uint64_t bar;
+  uint64_t next, epoch;
+  uint64_t excl_s[2], excl_p[2];  // resolved offsets of the staged tile (service warp; by parity)
+  uint32_t agg_ts[2], agg_tp[2];  // aggregate of the current tile (compute warps; by parity)
+  uint32_t scan[4];
+  uint32_t wsb[4], wpb[4];
+};
+constexpr uint32_t kSmemBytes = sizeof(Smem) + 1024;   // + alignment slack
+
+__device__ __forceinline__ Smem& smem_at(unsigned char* raw) {
+  const uint32_t a = smem_u32(raw);
+  return *reinterpret_cast<Smem*>(raw + (((a + 1023u) & ~1023u) - a));
+}
+
+// element i of tile row r in the 128B-swizzled tile image
+__device__ __forceinline__ uint32_t swz_elem(uint32_t r, uint32_t i) {
+  return r * 128u + ((((i >> 2) ^ (r & 7u)) << 4) | ((i & 3u) << 2));
+}
+
+// payload staging: logical word a at a ^ row(a) within its 32-word row
+__device__ __forceinline__ uint32_t swz_word(uint32_t a) { return a ^ ((a >> 5) & 31u); }
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// named barriers: 1 = the 128 compute threads, 2 = "input consumed"
+// (compute arrive, service sync), 3 = "offsets ready" (all 160 threads)
+constexpr int kCompute = 128;
+constexpr int kThreadsWS = kCompute + 32;
+#ifndef HSZ_ENC_CTAS
+#define HSZ_ENC_CTAS 4   // CTAs per SM the register budget is sized for
+#endif
+__device__ __forceinline__ void bar_sync_n(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_n(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ bool bar_or_compute(bool p) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred q, o;\n\tsetp.ne.u32 q, %1, 0;\n\t"
+      "bar.red.or.pred o, 1, 128, q;\n\tselp.u32 %0, 1, 0, o;\n}"
+      : "=r"(r)
+      : "r"(static_cast<uint32_t>(p))
+      : "memory");
+  return r != 0;
+}
+
+// exclusive scan of one u32 over the 128 compute threads; *total = sum
+__device__ __forceinline__ uint32_t cta_scan(uint32_t v, uint32_t* s_scan, uint32_t* total) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t inc = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t o = __shfl_up_sync(kFull, inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (lane == 31) s_scan[warp] = inc;
+  bar_sync_n(1, kCompute);
+  const uint32_t a0 = s_scan[0], a1 = s_scan[1], a2 = s_scan[2], a3 = s_scan[3];
+  const uint32_t pre = (warp > 0 ? a0 : 0u) + (warp > 1 ? a1 : 0u) + (warp > 2 ? a2 : 0u);
+  *total = a0 + a1 + a2 + a3;
+  return pre + inc - v;
+}
+
+// ---------------------------------------------------------------------------
+// per-thread block encoding
+
+struct BlockCode {
+  uint32_t mg[K];   // residual magnitudes (mg[0] = 0: slot 0 holds the outlier)
+  uint32_t sg;      // sign bits, element i at bit 31 - i
+  uint32_t w;       // width
+};
+
+// residuals (codec.py:178-212), width (codec.py:215-225), sign word
+__device__ __forceinline__ void block_code(uint32_t (&qb)[K], int len, BlockCode& bc) {
+  if (len < K) {   // the stream's tail block (or no block): replicate the last live bin
+#pragma unroll
+    for (int i = 1; i < K; ++i) qb[i] = (i < len) ? qb[i] : qb[i - 1];
+  }
+  uint32_t mx = 0, sg = 0;
+  bc.mg[0] = 0;
+#pragma unroll
+  for (int i = 1; i < K; ++i) {
+    const int32_t d = static_cast<int32_t>(qb[i] - qb[i - 1]);
+    sg = __funnelshift_l(static_cast<uint32_t>(d), sg, 1);
+    bc.mg[i] = static_cast<uint32_t>(d < 0 ? -d : d);
+    mx |= bc.mg[i];
+  }
+  bc.sg = sg;
+  bc.w = 32u - __clz(mx);
+}
+
+// MSB-first w-bit fields, G fields combined per step (G * w < 32)
+template <int G>
+__device__ __forceinline__ void pack_fields(const BlockCode& bc, uint32_t a, uint32_t* pbuf) {
+  const uint32_t w = bc.w;
+  const uint32_t pw = 1u << w, pg = 1u << (G * w);
+  uint32_t acc = 0;
+  int nbm = -32;   // pending bits - 32
+#pragma unroll
+  for (int c = 0; c < K / G; ++c) {
+    uint32_t chunk = bc.mg[c * G];
+#pragma unroll
+    for (int g = 1; g < G; ++g) chunk = chunk * pw + bc.mg[c * G + g];
+    const uint64_t t = static_cast<uint64_t>(acc) * pg + chunk;
+    nbm += G * static_cast<int>(w);
+    if (nbm >= 0) {
+      pbuf[swz_word(a)] = bswap32(static_cast<uint32_t>(t >> nbm));
+      ++a;
+      nbm -= 32;
+    }
+    acc = static_cast<uint32_t>(t);
+  }
+  if (nbm > -32) pbuf[swz_word(a)] = bswap32(acc << (-nbm));   // partial tail block
+}
+
+__device__ __forceinline__ void pack_block(const BlockCode& bc, uint32_t a, uint32_t* pbuf) {
+  const uint32_t wmax = __reduce_max_sync(kFull, bc.w);   // warp-uniform grouping
+  if (bc.w == 0) return;
+  if (wmax <= 7) {
+    pack_fields<4>(bc, a, pbuf);
+  } else if (wmax <= 15) {
+    pack_fields<2>(bc, a, pbuf);
+  } else {
+    pack_fields<1>(bc, a, pbuf);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// placement of the staged tile (compute threads; offsets from the service warp)
+
+constexpr uint32_t kSelfPlaced = 0xFFFFFFFFu;   // cur_ts marker: exact-path tile placed itself
+
+__device__ __forceinline__ void copy_staged(Smem& S, const k32::EncodeOut& out, uint32_t ts,
+                                            uint32_t tp, int par) {
+  const int tid = threadIdx.x;
+  const uint64_t es = S.excl_s[par], ep = S.excl_p[par];
+  if (es == ~0ull) return;   // capacity exceeded (flagged)
+  // sign words: offsets are multiples of 4 (the stream's tail block is last)
+  uint32_t* dsg = reinterpret_cast<uint32_t*>(out.signs + es);
+  for (uint32_t i = tid; i < ((ts + 3u) >> 2); i += kCompute) dsg[i] = S.sgn[par][i];
+  // payload: 16-byte stores from the first 16-byte aligned destination word
+  const uint32_t* pbuf = reinterpret_cast<const uint32_t*>(S.pk[par]);
+  uint32_t* dst = reinterpret_cast<uint32_t*>(out.payload + ep);
+  const uint32_t nw = (tp + 3u) >> 2;
+  uint32_t head = static_cast<uint32_t>(((16u - (ep & 15u)) & 15u) >> 2);
+  head = head < nw ? head : nw;
+  if (static_cast<uint32_t>(tid) < head) dst[tid] = pbuf[swz_word(tid)];
+  const uint32_t nv = (nw - head) >> 2;
+  uint4* dv = reinterpret_cast<uint4*>(dst + head);
+  for (uint32_t i = tid; i < nv; i += kCompute) {
+    const uint32_t k = head + 4u * i;
+    dv[i] = make_uint4(pbuf[swz_word(k)], pbuf[swz_word(k + 1)], pbuf[swz_word(k + 2)],
+                       pbuf[swz_word(k + 3)]);
+  }
+  const uint32_t rest = head + 4u * nv + static_cast<uint32_t>(tid);
+  if (rest < nw) dst[rest] = pbuf[swz_word(rest)];
+}
+
+// one warp: resolve `tile` and record its offsets (+ the tile-offset cache)
+__device__ __forceinline__ void resolve_tile(Smem& S, const k32::EncodeOut& out, uint64_t tile,
+                                             uint64_t epoch, uint64_t ntiles, uint32_t ts,
+                                             uint32_t tp, int par) {
+  const int lane = threadIdx.x & 31;
+  uint64_t es, ep;
+  lb_resolve(lb_words(out.ws), tile, epoch, ts, tp, &es, &ep);
+  if (lane == 0) {
+    out.toff[2 * tile] = es;
+    out.toff[2 * tile + 1] = ep;
+    if (tile == ntiles - 1) {
+      out.toff[2 * ntiles] = es + ts;
+      out.toff[2 * ntiles + 1] = ep + tp;
+    }
+    const bool fits = es + ts <= out.sign_cap && ep + tp <= out.payload_cap;
+    if (!fits) atomicOr(out.err, HSZ_ERR_CAPACITY);
+    S.excl_s[par] = fits ? es : ~0ull;
+    S.excl_p[par] = ep;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// compress, float32 input, block_len 32
+//
+// Persistent, warp-specialised: warps 0-3 compute (thread b = block b of the
+// current tile), warp 4 is the service warp -- it draws tickets, issues the
+// TMA load of the next tile as soon as the compute warps have taken the
+// current one into registers, and resolves the look-back of the PREVIOUS
+// tile while the compute warps quantize the current one.  Per iteration:
+//
+//   compute: wait TMA(cur) | quantize | arrive(2) | code + scan + publish
+//            | sync(3) | copy prev out | sync(1) | pack cur into staging
+//   service: sync(2) | TMA(next), draw ticket | resolve prev | sync(3)
+//
+// kTma: tiles arrive by 2-D tensor loads (x 16-byte aligned, >= 128 full
+// rows); otherwise the compute warps load each tile with plain loads.
+template <bool kTma>
+__global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
+    compress_f32_kernel(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ x,
+                        uint64_t n, QuantF32 qf, QuantConst qc, k32::EncodeOut out,
+                        uint64_t nblocks, uint64_t ntiles, uint32_t tail_len) {
+  extern __shared__ unsigned char smraw[];
+  Smem& S = smem_at(smraw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  LookbackWs lw = LookbackWs::bind(out.ws, ntiles);
+  const uint64_t last_draw = ntiles + gridDim.x - 1;   // every CTA draws once past the end
+  const uint64_t full_rows = n / K;
+  uint64_t ahead = ~0ull;                               // service lane 0: ticket after `next`
+  auto draw = [&](uint64_t epoch) -> uint64_t {
+    const uint64_t t = atom_add_acq_rel(lw.ticket, 1);
+    if (t == last_draw) {
+      st_relaxed(lw.ticket, 0);
+      st_release(lw.epoch, epoch + 1);
+    }
+    return t;
+  };
+  auto issue = [&](uint64_t t) {   // service lane 0
+    if (kTma) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx(&S.bar, kBufBytes);
+      tma_load_2d(S.in, &tmap, 0, static_cast<int>(t * TB), &S.bar);
+    }
+  };
+  if (tid == kCompute) {
+    mbar_init(&S.bar, 1);
+    fence_mbar_init();
+    const uint64_t e = ld_acquire(lw.epoch);
+    S.epoch = e;
+    const uint64_t t = draw(e);
+    S.next = t;
+    if (t < ntiles) {
+      issue(t);
+      ahead = draw(e);
+    }
+  }
+  __syncthreads();
+  const uint64_t epoch = S.epoch;
+  uint64_t cur = S.next;
+  bool has_prev = false;
+
+  if (warp == kCompute / 32) {
+    // =========================== service warp ===========================
+    // iteration k: sync(2) | TMA(tile k+1), draw | resolve tile k-1 (its
+    //              aggregate from S.agg, offsets to S.excl, parity (k-1)&1) | sync(3)
+    uint64_t prev = ~0ull;
+    int par = 0;   // parity of the current tile
+    while (cur < ntiles || has_prev) {
+      bar_sync_n(2, kThreadsWS);                 // S.in consumed
+      if (lane == 0) {
+        uint64_t nx = ~0ull;
+        if (cur < ntiles) {
+          nx = ahead;
+          if (nx < ntiles) {
+            issue(nx);
+            ahead = draw(epoch);
+          }
+        }
+        S.next = nx;
+      }
+      if (has_prev) {
+        const uint32_t pts = S.agg_ts[par ^ 1], ptp = S.agg_tp[par ^ 1];
+        if (pts != kSelfPlaced) resolve_tile(S, out, prev, epoch, ntiles, pts, ptp, par ^ 1);
+      }
+      bar_sync_n(3, kThreadsWS);                 // prev's offsets + next tile id out
+      has_prev = cur < ntiles;
+      prev = cur;
+      cur = S.next;
+      par ^= 1;
+      __syncwarp();
+    }
+    return;
+  }
+
+  // =========================== compute warps ===========================
+  // iteration k: wait TMA(tile k) | quantize | arrive(2) | code, scan, publish,
+  //              pack tile k into staging[k&1] | sync(3) | copy tile k-1 out
+  uint32_t phase = 0;
+  uint32_t flags = 0;
+  uint32_t prev_ts = 0, prev_tp = 0;
+  bool prev_self = false;
+  int par = 0;
+  while (cur < ntiles || has_prev) {
+    const bool live = cur < ntiles;
+    bool wide = false;
+    uint32_t ts = 0, tp = 0;
+    {
+      uint32_t qb[K];
+      if (live) {
+        trace_tile(cur, 1);
+        const uint64_t row0 = cur * TB;
+        if (kTma) {
+          mbar_wait_parity(&S.bar, phase);
+          phase ^= 1u;
+          // the partial last block is not covered by the tensor map (zero-filled)
+          if ((n % K) != 0 && full_rows >= row0 && full_rows < row0 + TB) {
+            if (tid < K) {
+              const uint32_t r = static_cast<uint32_t>(n % K);
+              const float v = static_cast<uint32_t>(tid) < r ? x[full_rows * K + tid] : 0.0f;
+              *reinterpret_cast<float*>(S.in + swz_elem(static_cast<uint32_t>(full_rows - row0), tid)) = v;
+            }
+            bar_sync_n(1, kCompute);
+          }
+        } else {
+          const uint64_t e0 = row0 * K;
+          for (uint32_t i = tid; i < TB * K; i += kCompute) {
+            const uint64_t e = e0 + i;
+            const float v = e < n ? x[e] : 0.0f;
+            *reinterpret_cast<float*>(S.in + swz_elem(i >> 5, i & 31u)) = v;
+          }
+          bar_sync_n(1, kCompute);
+        }
+        trace_tile(cur, 2);
+        // ---- quantize this thread's row ------------------------------------
+        const unsigned char* row = S.in + tid * 128;
+        bool bad = false;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 v = *reinterpret_cast<const float4*>(row + ((j ^ (tid & 7)) << 4));
+          qb[4 * j + 0] = quant_f32(v.x, qf, bad);
+          qb[4 * j + 1] = quant_f32(v.y, qf, bad);
+          qb[4 * j + 2] = quant_f32(v.z, qf, bad);
+          qb[4 * j + 3] = quant_f32(v.w, qf, bad);
+        }
+        if (__any_sync(kFull, bad)) {   // rare: an element inside the certificate margin
+#pragma unroll
+          for (int i = 0; i < K; ++i) {
+            const float xi = *reinterpret_cast<const float*>(S.in + swz_elem(tid, i));
+            bool b = false;
+            (void)quant_f32(xi, qf, b);
+            if (b) {
+              const ExactQ r = quant_exact(xi, qc);
+              flags |= r.flags;
+              wide |= !((r.q > -kWide) & (r.q < kWide));
+              qb[i] = static_cast<uint32_t>(static_cast<uint64_t>(r.q) + kMagicBits);
+            }
+          }
+        }
+        wide = bar_or_compute(wide);   // ... and every read of S.in is done
+      }
+      bar_arrive_n(2, kThreadsWS);       // the service warp may refill S.in
+
+      if (live && !wide) {
+        const uint64_t gb = cur * TB + tid;
+        const bool active = gb < nblocks;
+        const int len = !active ? 0 : (gb == nblocks - 1 ? static_cast<int>(tail_len) : K);
+        BlockCode bc;
+        block_code(qb, len, bc);
+        const uint32_t sb = (bc.w && active) ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
+        const uint32_t pb = (static_cast<uint32_t>(len) * bc.w + 7u) >> 3;
+        uint32_t tot;
+        const uint32_t ex = cta_scan(sb | (pb << 10), S.scan, &tot);   // sb <= 512, pb <= 15872
+        const uint32_t es = ex & 1023u, ep = ex >> 10;
+        ts = tot & 1023u;
+        tp = tot >> 10;
+        if (tid == 0) {
+          lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
+          S.agg_ts[par] = ts;
+          S.agg_tp[par] = tp;
+        }
+        trace_tile(cur, 3);
+        if (active) {
+          out.widths[gb] = static_cast<uint8_t>(bc.w);
+          out.outliers[gb] = static_cast<int32_t>(qb[0] - kMagicBits);
+        }
+        if (sb) S.sgn[par][es >> 2] = bswap32(bc.sg);
+        pack_block(bc, ep >> 2, reinterpret_cast<uint32_t*>(S.pk[par]));
+        trace_tile(cur, 4);
+      } else if (live) {
+        // exact path: sizes and publish now, placement after the previous tile
+        k32::SrcQuant<float> src{x, n, qc, cur};
+        flags |= k32::fallback_sizes(src, out, cur, nblocks, tail_len, S.wsb, S.wpb);
+        bar_sync_n(1, kCompute);
+        ts = S.wsb[0] + S.wsb[1] + S.wsb[2] + S.wsb[3];
+        tp = S.wpb[0] + S.wpb[1] + S.wpb[2] + S.wpb[3];
+        if (tid == 0) {
+          lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
+          S.agg_ts[par] = kSelfPlaced;
+        }
+      }
+    }
+    bar_sync_n(3, kThreadsWS);         // tile k-1 resolved, tile k+1 in flight
+    const uint64_t nx = S.next;
+    if (has_prev && !prev_self) copy_staged(S, out, prev_ts, prev_tp, par ^ 1);
+    trace_tile(cur, 5);
+    if (live && wide) {
+      // exact tile: resolve itself (the previous tile's inclusive prefix is out)
+      if (warp == 0) resolve_tile(S, out, cur, epoch, ntiles, ts, tp, par);
+      bar_sync_n(1, kCompute);
+      if (S.excl_s[par] != ~0ull) {
+        uint64_t gs = S.excl_s[par], gp = S.excl_p[par];
+        for (int i = 0; i < warp; ++i) {
+          gs += S.wsb[i];
+          gp += S.wpb[i];
+        }
+        k32::SrcQuant<float> src{x, n, qc, cur};
+        k32::fallback_pack(src, out, cur, nblocks, tail_len, gs, gp,
+                           reinterpret_cast<uint32_t*>(S.pk[par]) + warp * 64);
+      }
+    }
+    bar_sync_n(1, kCompute);           // staging[(k-1)&1] free for tile k+1
+    has_prev = live;
+    prev_self = wide;
+    prev_ts = ts;
+    prev_tp = tp;
+    cur = nx;
+    par ^= 1;
+  }
+  flags = __reduce_or_sync(kFull, flags);
+  if (lane == 0 && flags) atomicOr(out.err, flags);
+}
+
+}  // namespace e32
+}  // namespace hsz

@@ -57,6 +57,7 @@ DTYPE_CODE = {"f32": N.HSZ_F32, "f64": N.HSZ_F64}
 # payload capacity policy: the exact worst case (8 bytes/element) when it is
 # affordable, else 4 bytes/element with an exact-size retry on overflow
 _PAYLOAD_BOUND_LIMIT = 16 << 30
+_WS_REINIT_USES = 1 << 22
 
 
 class Context:
@@ -70,12 +71,20 @@ class Context:
         self.handle = int(stream.cuda_stream)
         self.ws = None
         self.ws_bytes = 0
+        self.ws_uses = 0
         with t.cuda.device(self.device):
             self.err = t.zeros(4, dtype=t.int32, device=self.device)
         self.err_ptr = ptr(self.err)
 
     def workspace(self, n: int, k: int):
         need = int(self.lib.hsz_workspace_size(n, k))
+        self.ws_uses += 1
+        if self.ws_uses >= _WS_REINIT_USES and self.ws is not None:
+            # look-back words carry a 24-bit launch-epoch tag: re-zero the
+            # workspace well before the tag could repeat (hsz_b200.h)
+            N.check(self.lib.hsz_workspace_init(ptr(self.ws), self.ws_bytes, self.handle),
+                    "workspace init")
+            self.ws_uses = 0
         if need > self.ws_bytes:
             t = torch()
             need = max(need, 2 * self.ws_bytes)
@@ -198,11 +207,9 @@ class DeviceStream:
     def to_host(self) -> CompressedStream:
         self.ctx.check()
         s, p = self.totals()
-        w = self.widths.cpu().numpy()
-        o = self.outliers.cpu().numpy()
-        sg = self.signs[:s].cpu().numpy().tobytes()
-        py = self.payload[:p].cpu().numpy().tobytes()
-        return CompressedStream(self.params, w, o, sg, py)
+        w, o, sg, py = download([self.widths, self.outliers.view(torch().uint8), self.signs[:s],
+                                 self.payload[:p]], self.ctx)
+        return CompressedStream(self.params, w, o.view(np.int32), sg, py)
 
     @classmethod
     def from_host(cls, cs: CompressedStream, ctx: Context = None) -> "DeviceStream":
@@ -246,6 +253,39 @@ class DeviceStream:
 
     def __repr__(self):
         return f"DeviceStream({self.params}, device={self.ctx.device})"
+
+
+_PINNED = {}
+
+
+def download(tensors, ctx: Context = None):
+    """Copy device tensors to host numpy arrays through one pinned staging
+    buffer (one async copy each, one synchronize).  The arrays are copies."""
+    t = torch()
+    sizes = [int(x.numel()) * x.element_size() for x in tensors]
+    total = sum(sizes)
+    key = t.cuda.current_device() if ctx is None else ctx.device.index
+    buf = _PINNED.get(key)
+    if buf is None or buf.numel() < total:
+        buf = t.empty(max(total, 1 << 20), dtype=t.uint8, pin_memory=True)
+        _PINNED[key] = buf
+    off = 0
+    views = []
+    for x, nb in zip(tensors, sizes):
+        dst = buf[off:off + nb]
+        if nb:
+            dst.copy_(x.reshape(-1).view(t.uint8), non_blocking=True)
+        views.append((off, nb, x.dtype))
+        off += nb
+    (ctx.stream if ctx is not None else t.cuda.current_stream()).synchronize()
+    host = buf.numpy()
+    out = []
+    for (o, nb, dt), x in zip(views, tensors):
+        a = host[o:o + nb].copy()
+        npdt = {t.uint8: np.uint8, t.int32: np.int32, t.int64: np.int64, t.float32: np.float32,
+                t.float64: np.float64}[dt]
+        out.append(a.view(npdt))
+    return out
 
 
 def new_stream_buffers(ctx: Context, params: QuantParams, payload_cap: int = None):
