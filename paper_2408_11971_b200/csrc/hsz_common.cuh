@@ -33,7 +33,7 @@ __device__ __forceinline__ void trace(uint32_t tag) {
 }
 // per-tile record: (tile << 40) | (tag << 32) | low 32 bits of globaltimer (ns)
 __device__ __forceinline__ void trace_tile(uint64_t tile, uint32_t tag) {
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 || threadIdx.x == 128) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     const unsigned i = atomicAdd(&g_trace_n, 1u);
@@ -141,6 +141,12 @@ __device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
 }
 __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t atom_add_relaxed(uint64_t* p, uint64_t v) {
+  uint64_t old;
+  asm volatile("atom.relaxed.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v)
+               : "memory");
+  return old;
 }
 __device__ __forceinline__ uint64_t atom_add_acq_rel(uint64_t* p, uint64_t v) {
   uint64_t old;

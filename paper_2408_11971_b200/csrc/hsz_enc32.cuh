@@ -113,8 +113,11 @@ struct Smem {
   unsigned char in[kBufBytes];    // input tile (TMA 128B swizzle; 1024-aligned)
   unsigned char pk[2][kBufBytes]; // packed payload of the staged tiles (word swizzle; by parity)
   alignas(16) uint32_t sgn[2][TB];  // their sign words (compacted)
-  uint64_t bar;
-  uint64_t next, epoch;
+  uint64_t bar;                   // input full (TMA or "no more tiles")
+  uint64_t in_empty;              // compute warps consumed S.in        (128 arrivals)
+  uint64_t st_full[2];            // tile staged in pk[b]                (128 arrivals)
+  uint64_t st_empty[2];           // pk[b] copied out by the service warp (1 arrival)
+  uint64_t cur, epoch;
   uint64_t excl_s[2], excl_p[2];  // resolved offsets of the staged tile (service warp; by parity)
   uint32_t agg_ts[2], agg_tp[2];  // aggregate of the current tile (compute warps; by parity)
   uint32_t scan[4];
@@ -254,29 +257,30 @@ __device__ __forceinline__ void pack_block(const BlockCode& bc, uint32_t a, uint
 
 constexpr uint32_t kSelfPlaced = 0xFFFFFFFFu;   // cur_ts marker: exact-path tile placed itself
 
+// copy a staged tile to its resolved offsets; `rank`/`nthr` = this thread's
+// index among the threads sharing the copy
 __device__ __forceinline__ void copy_staged(Smem& S, const k32::EncodeOut& out, uint32_t ts,
-                                            uint32_t tp, int par) {
-  const int tid = threadIdx.x;
+                                            uint32_t tp, int par, uint32_t rank, uint32_t nthr) {
   const uint64_t es = S.excl_s[par], ep = S.excl_p[par];
   if (es == ~0ull) return;   // capacity exceeded (flagged)
   // sign words: offsets are multiples of 4 (the stream's tail block is last)
   uint32_t* dsg = reinterpret_cast<uint32_t*>(out.signs + es);
-  for (uint32_t i = tid; i < ((ts + 3u) >> 2); i += kCompute) dsg[i] = S.sgn[par][i];
+  for (uint32_t i = rank; i < ((ts + 3u) >> 2); i += nthr) dsg[i] = S.sgn[par][i];
   // payload: 16-byte stores from the first 16-byte aligned destination word
   const uint32_t* pbuf = reinterpret_cast<const uint32_t*>(S.pk[par]);
   uint32_t* dst = reinterpret_cast<uint32_t*>(out.payload + ep);
   const uint32_t nw = (tp + 3u) >> 2;
   uint32_t head = static_cast<uint32_t>(((16u - (ep & 15u)) & 15u) >> 2);
   head = head < nw ? head : nw;
-  if (static_cast<uint32_t>(tid) < head) dst[tid] = pbuf[swz_word(tid)];
+  if (rank < head) dst[rank] = pbuf[swz_word(rank)];
   const uint32_t nv = (nw - head) >> 2;
   uint4* dv = reinterpret_cast<uint4*>(dst + head);
-  for (uint32_t i = tid; i < nv; i += kCompute) {
+  for (uint32_t i = rank; i < nv; i += nthr) {
     const uint32_t k = head + 4u * i;
     dv[i] = make_uint4(pbuf[swz_word(k)], pbuf[swz_word(k + 1)], pbuf[swz_word(k + 2)],
                        pbuf[swz_word(k + 3)]);
   }
-  const uint32_t rest = head + 4u * nv + static_cast<uint32_t>(tid);
+  const uint32_t rest = head + 4u * nv + rank;
   if (rest < nw) dst[rest] = pbuf[swz_word(rest)];
 }
 
@@ -329,184 +333,220 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
   const uint64_t full_rows = n / K;
   uint64_t ahead = ~0ull;                               // service lane 0: ticket after `next`
   auto draw = [&](uint64_t epoch) -> uint64_t {
-    const uint64_t t = atom_add_acq_rel(lw.ticket, 1);
+    const uint64_t t = atom_add_relaxed(lw.ticket, 1);
     if (t == last_draw) {
       st_relaxed(lw.ticket, 0);
       st_release(lw.epoch, epoch + 1);
     }
     return t;
   };
-  auto issue = [&](uint64_t t) {   // service lane 0
-    if (kTma) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect_tx(&S.bar, kBufBytes);
-      tma_load_2d(S.in, &tmap, 0, static_cast<int>(t * TB), &S.bar);
+  auto issue = [&](uint64_t t) {   // service lane 0: tile t into S.in (or "no more tiles")
+    S.cur = t;
+    if (t < ntiles) {
+      if (kTma) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(&S.bar, kBufBytes);
+        tma_load_2d(S.in, &tmap, 0, static_cast<int>(t * TB), &S.bar);
+      } else {
+        mbar_arrive(&S.bar);   // the compute warps load the tile themselves
+      }
+    } else {
+      mbar_arrive(&S.bar);
     }
   };
   if (tid == kCompute) {
     mbar_init(&S.bar, 1);
+    mbar_init(&S.in_empty, kCompute);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&S.st_full[b], kCompute);
+      mbar_init(&S.st_empty[b], 1);
+    }
     fence_mbar_init();
     const uint64_t e = ld_acquire(lw.epoch);
     S.epoch = e;
-    const uint64_t t = draw(e);
-    S.next = t;
-    if (t < ntiles) {
-      issue(t);
-      ahead = draw(e);
-    }
   }
   __syncthreads();
   const uint64_t epoch = S.epoch;
-  uint64_t cur = S.next;
-  bool has_prev = false;
 
   if (warp == kCompute / 32) {
     // =========================== service warp ===========================
-    // iteration k: sync(2) | TMA(tile k+1), draw | resolve tile k-1 (its
-    //              aggregate from S.agg, offsets to S.excl, parity (k-1)&1) | sync(3)
-    uint64_t prev = ~0ull;
-    int par = 0;   // parity of the current tile
-    while (cur < ntiles || has_prev) {
-      bar_sync_n(2, kThreadsWS);                 // S.in consumed
-      if (lane == 0) {
-        uint64_t nx = ~0ull;
-        if (cur < ntiles) {
-          nx = ahead;
-          if (nx < ntiles) {
-            issue(nx);
-            ahead = draw(epoch);
-          }
-        }
-        S.next = nx;
-      }
-      if (has_prev) {
-        const uint32_t pts = S.agg_ts[par ^ 1], ptp = S.agg_tp[par ^ 1];
-        if (pts != kSelfPlaced) resolve_tile(S, out, prev, epoch, ntiles, pts, ptp, par ^ 1);
-      }
-      bar_sync_n(3, kThreadsWS);                 // prev's offsets + next tile id out
-      has_prev = cur < ntiles;
-      prev = cur;
-      cur = S.next;
-      par ^= 1;
-      __syncwarp();
+    // per tile k handed to the compute warps (all hand-offs are mbarriers):
+    //   wait in_empty (tile k consumed) | TMA(tile k+1) or "done", draw a
+    //   ticket | wait st_full (tile k-1 staged) | resolve + copy out tile k-1
+    //   | arrive st_empty
+    uint64_t ahead = ~0ull;
+    uint64_t t = ~0ull;
+    if (lane == 0) {
+      t = draw(epoch);
+      issue(t);
+      if (t < ntiles) ahead = draw(epoch);
     }
+    t = __shfl_sync(kFull, t, 0);
+    uint64_t prev = ~0ull;
+    uint32_t k = 0;   // index (in this CTA) of tile t
+    auto place = [&](uint64_t tile, uint32_t kk) {   // tile = the kk-th tile of this CTA
+      const int b = kk & 1;
+      mbar_wait_parity(&S.st_full[b], (kk >> 1) & 1u);
+      const uint32_t pts = S.agg_ts[b], ptp = S.agg_tp[b];
+      if (pts != kSelfPlaced) {
+        trace_tile(tile, 7);
+        resolve_tile(S, out, tile, epoch, ntiles, pts, ptp, b);
+        __syncwarp();
+        copy_staged(S, out, pts, ptp, b, lane, 32);
+        trace_tile(tile, 8);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.st_empty[b]);
+    };
+    while (t < ntiles) {
+      mbar_wait_parity(&S.in_empty, k & 1u);     // S.in holds no unread data
+      uint64_t nx = ~0ull, drawn = ~0ull;
+      if (lane == 0) {
+        nx = ahead;
+        issue(nx);
+        if (nx < ntiles) drawn = atom_add_relaxed(lw.ticket, 1);   // consumed below
+      }
+      nx = __shfl_sync(kFull, nx, 0);
+      if (prev != ~0ull) place(prev, k - 1);
+      if (lane == 0 && drawn != ~0ull) {
+        if (drawn == last_draw) {
+          st_relaxed(lw.ticket, 0);
+          st_release(lw.epoch, epoch + 1);
+        }
+        ahead = drawn;
+      }
+      prev = t;
+      t = nx;
+      ++k;
+    }
+    if (prev != ~0ull) place(prev, k - 1);
     return;
   }
 
   // =========================== compute warps ===========================
-  // iteration k: wait TMA(tile k) | quantize | arrive(2) | code, scan, publish,
-  //              pack tile k into staging[k&1] | sync(3) | copy tile k-1 out
+  // per tile k: wait TMA(tile k) | quantize | arrive in_empty | code, scan,
+  //             publish | wait st_empty (tile k-2 out) | pack into staging[k&1]
+  //             | arrive st_full
   uint32_t phase = 0;
   uint32_t flags = 0;
-  uint32_t prev_ts = 0, prev_tp = 0;
-  bool prev_self = false;
   int par = 0;
-  while (cur < ntiles || has_prev) {
-    const bool live = cur < ntiles;
+  int k = 0;
+  while (true) {
+    mbar_wait_parity(&S.bar, phase);
+    phase ^= 1u;
+    const uint64_t cur = S.cur;
+    if (cur >= ntiles) break;
     bool wide = false;
-    uint32_t ts = 0, tp = 0;
-    {
-      uint32_t qb[K];
-      if (live) {
-        trace_tile(cur, 1);
-        const uint64_t row0 = cur * TB;
-        if (kTma) {
-          mbar_wait_parity(&S.bar, phase);
-          phase ^= 1u;
-          // the partial last block is not covered by the tensor map (zero-filled)
-          if ((n % K) != 0 && full_rows >= row0 && full_rows < row0 + TB) {
-            if (tid < K) {
-              const uint32_t r = static_cast<uint32_t>(n % K);
-              const float v = static_cast<uint32_t>(tid) < r ? x[full_rows * K + tid] : 0.0f;
-              *reinterpret_cast<float*>(S.in + swz_elem(static_cast<uint32_t>(full_rows - row0), tid)) = v;
-            }
-            bar_sync_n(1, kCompute);
-          }
-        } else {
-          const uint64_t e0 = row0 * K;
-          for (uint32_t i = tid; i < TB * K; i += kCompute) {
-            const uint64_t e = e0 + i;
-            const float v = e < n ? x[e] : 0.0f;
-            *reinterpret_cast<float*>(S.in + swz_elem(i >> 5, i & 31u)) = v;
-          }
-          bar_sync_n(1, kCompute);
+    uint32_t qb[K];
+    trace_tile(cur, 1);
+    const uint64_t row0 = cur * TB;
+    if (kTma) {
+      // the partial last block is not covered by the tensor map (zero-filled)
+      if ((n % K) != 0 && full_rows >= row0 && full_rows < row0 + TB) {
+        if (tid < K) {
+          const uint32_t r = static_cast<uint32_t>(n % K);
+          const float v = static_cast<uint32_t>(tid) < r ? x[full_rows * K + tid] : 0.0f;
+          *reinterpret_cast<float*>(S.in + swz_elem(static_cast<uint32_t>(full_rows - row0), tid)) = v;
         }
-        trace_tile(cur, 2);
-        // ---- quantize this thread's row ------------------------------------
-        const unsigned char* row = S.in + tid * 128;
-        bool bad = false;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float4 v = *reinterpret_cast<const float4*>(row + ((j ^ (tid & 7)) << 4));
-          qb[4 * j + 0] = quant_f32(v.x, qf, bad);
-          qb[4 * j + 1] = quant_f32(v.y, qf, bad);
-          qb[4 * j + 2] = quant_f32(v.z, qf, bad);
-          qb[4 * j + 3] = quant_f32(v.w, qf, bad);
-        }
-        if (__any_sync(kFull, bad)) {   // rare: an element inside the certificate margin
-#pragma unroll
-          for (int i = 0; i < K; ++i) {
-            const float xi = *reinterpret_cast<const float*>(S.in + swz_elem(tid, i));
-            bool b = false;
-            (void)quant_f32(xi, qf, b);
-            if (b) {
-              const ExactQ r = quant_exact(xi, qc);
-              flags |= r.flags;
-              wide |= !((r.q > -kWide) & (r.q < kWide));
-              qb[i] = static_cast<uint32_t>(static_cast<uint64_t>(r.q) + kMagicBits);
-            }
-          }
-        }
-        wide = bar_or_compute(wide);   // ... and every read of S.in is done
-      }
-      bar_arrive_n(2, kThreadsWS);       // the service warp may refill S.in
-
-      if (live && !wide) {
-        const uint64_t gb = cur * TB + tid;
-        const bool active = gb < nblocks;
-        const int len = !active ? 0 : (gb == nblocks - 1 ? static_cast<int>(tail_len) : K);
-        BlockCode bc;
-        block_code(qb, len, bc);
-        const uint32_t sb = (bc.w && active) ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
-        const uint32_t pb = (static_cast<uint32_t>(len) * bc.w + 7u) >> 3;
-        uint32_t tot;
-        const uint32_t ex = cta_scan(sb | (pb << 10), S.scan, &tot);   // sb <= 512, pb <= 15872
-        const uint32_t es = ex & 1023u, ep = ex >> 10;
-        ts = tot & 1023u;
-        tp = tot >> 10;
-        if (tid == 0) {
-          lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
-          S.agg_ts[par] = ts;
-          S.agg_tp[par] = tp;
-        }
-        trace_tile(cur, 3);
-        if (active) {
-          out.widths[gb] = static_cast<uint8_t>(bc.w);
-          out.outliers[gb] = static_cast<int32_t>(qb[0] - kMagicBits);
-        }
-        if (sb) S.sgn[par][es >> 2] = bswap32(bc.sg);
-        pack_block(bc, ep >> 2, reinterpret_cast<uint32_t*>(S.pk[par]));
-        trace_tile(cur, 4);
-      } else if (live) {
-        // exact path: sizes and publish now, placement after the previous tile
-        k32::SrcQuant<float> src{x, n, qc, cur};
-        flags |= k32::fallback_sizes(src, out, cur, nblocks, tail_len, S.wsb, S.wpb);
         bar_sync_n(1, kCompute);
-        ts = S.wsb[0] + S.wsb[1] + S.wsb[2] + S.wsb[3];
-        tp = S.wpb[0] + S.wpb[1] + S.wpb[2] + S.wpb[3];
-        if (tid == 0) {
+      }
+    } else {
+      const uint64_t e0 = row0 * K;
+      for (uint32_t i = tid; i < TB * K; i += kCompute) {
+        const uint64_t e = e0 + i;
+        const float v = e < n ? x[e] : 0.0f;
+        *reinterpret_cast<float*>(S.in + swz_elem(i >> 5, i & 31u)) = v;
+      }
+      bar_sync_n(1, kCompute);
+    }
+    trace_tile(cur, 2);
+    // ---- quantize this thread's row ----------------------------------------
+    {
+      const unsigned char* row = S.in + tid * 128;
+      bool bad = false;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 v = *reinterpret_cast<const float4*>(row + ((j ^ (tid & 7)) << 4));
+        qb[4 * j + 0] = quant_f32(v.x, qf, bad);
+        qb[4 * j + 1] = quant_f32(v.y, qf, bad);
+        qb[4 * j + 2] = quant_f32(v.z, qf, bad);
+        qb[4 * j + 3] = quant_f32(v.w, qf, bad);
+      }
+      if (__any_sync(kFull, bad)) {   // rare: an element inside the certificate margin
+        // in place in this thread's own row of S.in (nothing large may be live
+        // across the exact routine's call): fast bins overwrite their inputs,
+        // then the failed elements are redone exactly
+        float* rowf = reinterpret_cast<float*>(S.in + tid * 128);
+        uint32_t mask = 0;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          float* pi = reinterpret_cast<float*>(S.in + swz_elem(tid, i));
+          bool b = false;
+          (void)quant_f32(*pi, qf, b);
+          mask |= (b ? 1u : 0u) << i;
+          if (!b) *reinterpret_cast<uint32_t*>(pi) = qb[i];
+        }
+        (void)rowf;
+#pragma unroll 1
+        for (int i = 0; i < K; ++i) {
+          if ((mask >> i) & 1u) {
+            uint32_t* pi = reinterpret_cast<uint32_t*>(S.in + swz_elem(tid, i));
+            const ExactQ r = quant_exact(__uint_as_float(*pi), qc);
+            flags |= r.flags;
+            wide |= !((r.q > -kWide) & (r.q < kWide));
+            *pi = static_cast<uint32_t>(static_cast<uint64_t>(r.q) + kMagicBits);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < K; ++i) qb[i] = *reinterpret_cast<const uint32_t*>(S.in + swz_elem(tid, i));
+      }
+      wide = bar_or_compute(wide);   // ... and every read of S.in is done
+      mbar_arrive(&S.in_empty);        // the service warp may refill S.in
+      if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);   // tile k-2 copied out
+    }
+    uint32_t ts = 0, tp = 0;
+    if (!wide) {
+      const uint64_t gb = cur * TB + tid;
+      const bool active = gb < nblocks;
+      const int len = !active ? 0 : (gb == nblocks - 1 ? static_cast<int>(tail_len) : K);
+      BlockCode bc;
+      block_code(qb, len, bc);
+      const uint32_t sb = (bc.w && active) ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
+      const uint32_t pb = (static_cast<uint32_t>(len) * bc.w + 7u) >> 3;
+      uint32_t tot;
+      const uint32_t ex = cta_scan(sb | (pb << 10), S.scan, &tot);   // sb <= 512, pb <= 15872
+      const uint32_t es = ex & 1023u, ep = ex >> 10;
+      ts = tot & 1023u;
+      tp = tot >> 10;
+      if (tid == 0) {
+        lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
+        S.agg_ts[par] = ts;
+        S.agg_tp[par] = tp;
+      }
+      trace_tile(cur, 3);
+      if (active) {
+        out.widths[gb] = static_cast<uint8_t>(bc.w);
+        out.outliers[gb] = static_cast<int32_t>(qb[0] - kMagicBits);
+      }
+      if (sb) S.sgn[par][es >> 2] = bswap32(bc.sg);
+      pack_block(bc, ep >> 2, reinterpret_cast<uint32_t*>(S.pk[par]));
+      trace_tile(cur, 4);
+    } else {
+      // exact path: sizes, publish, resolve and place itself (the look-back
+      // waits for the previous tile's inclusive prefix from the service warp)
+      k32::SrcQuant<float> src{x, n, qc, cur};
+      flags |= k32::fallback_sizes(src, out, cur, nblocks, tail_len, S.wsb, S.wpb);
+      bar_sync_n(1, kCompute);
+      ts = S.wsb[0] + S.wsb[1] + S.wsb[2] + S.wsb[3];
+      tp = S.wpb[0] + S.wpb[1] + S.wpb[2] + S.wpb[3];
+      if (warp == 0) {
+        if (lane == 0) {
           lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
           S.agg_ts[par] = kSelfPlaced;
         }
+        __syncwarp();
+        resolve_tile(S, out, cur, epoch, ntiles, ts, tp, par);
       }
-    }
-    bar_sync_n(3, kThreadsWS);         // tile k-1 resolved, tile k+1 in flight
-    const uint64_t nx = S.next;
-    if (has_prev && !prev_self) copy_staged(S, out, prev_ts, prev_tp, par ^ 1);
-    trace_tile(cur, 5);
-    if (live && wide) {
-      // exact tile: resolve itself (the previous tile's inclusive prefix is out)
-      if (warp == 0) resolve_tile(S, out, cur, epoch, ntiles, ts, tp, par);
       bar_sync_n(1, kCompute);
       if (S.excl_s[par] != ~0ull) {
         uint64_t gs = S.excl_s[par], gp = S.excl_p[par];
@@ -514,18 +554,13 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
           gs += S.wsb[i];
           gp += S.wpb[i];
         }
-        k32::SrcQuant<float> src{x, n, qc, cur};
         k32::fallback_pack(src, out, cur, nblocks, tail_len, gs, gp,
                            reinterpret_cast<uint32_t*>(S.pk[par]) + warp * 64);
       }
     }
-    bar_sync_n(1, kCompute);           // staging[(k-1)&1] free for tile k+1
-    has_prev = live;
-    prev_self = wide;
-    prev_ts = ts;
-    prev_tp = tp;
-    cur = nx;
+    mbar_arrive(&S.st_full[par]);      // tile k staged (or placed)
     par ^= 1;
+    ++k;
   }
   flags = __reduce_or_sync(kFull, flags);
   if (lane == 0 && flags) atomicOr(out.err, flags);

@@ -41,14 +41,15 @@ tag = ((a >> 32) & 0xff).astype(np.int64)
 t = (a & 0xffffffff).astype(np.int64)
 t = (t - t.min()) / 1e3
 nt = tile.max() + 1
-T = np.full((nt, 7), np.nan)
+T = np.full((nt, 9), np.nan)
 T[tile, tag] = t
 print("records", n, "tiles", nt, "span us %.1f" % np.nanmax(T))
-names = {(1, 2): "load", (2, 3): "quant+code+scan", (3, 4): "pack", (4, 5): "wait+copy prev"}
+names = {(1, 2): "load wait", (2, 3): "quant+code+scan", (3, 4): "pack", (4, 7): "staged->placing",
+         (7, 8): "svc resolve+copy", (3, 8): "publish->placed"}
 for (a0, a1), nm in names.items():
     d = T[:, a1] - T[:, a0]
     print(f"{nm:11s} mean {np.nanmean(d):6.2f}  p50 {np.nanmedian(d):6.2f}  p90 {np.nanpercentile(d, 90):6.2f}  max {np.nanmax(d):6.2f} us")
-life = T[:, 5] - T[:, 1]
+life = T[:, 4] - T[:, 1]
 print("lifetime    mean %.2f p50 %.2f" % (np.nanmean(life), np.nanmedian(life)))
 for q in (0, 128, 512, 1183, 1184, 2000, 3000, 4000, 5000, nt - 1):
     if q < nt:
@@ -59,3 +60,12 @@ h, e = np.histogram(st, bins=np.arange(0, np.nanmax(T) + 10, 10))
 print("starts per 10us:", h.tolist())
 r = T[:, 5] - T[:, 4]
 print("finalize by tile decile:", [round(float(np.nanmean(r[i * nt // 10:(i + 1) * nt // 10])), 2) for i in range(10)])
+
+# service warps vs compute: when does each tile get placed (tag 8), per 5 us
+pl = T[:, 8]
+h, e = np.histogram(pl[~np.isnan(pl)], bins=np.arange(0, np.nanmax(T) + 5, 5))
+print("resolved per 5us:", h.tolist())
+h, e = np.histogram(T[:, 1][~np.isnan(T[:, 1])], bins=np.arange(0, np.nanmax(T) + 5, 5))
+print("started per 5us:", h.tolist())
+print("first start %.2f  last start %.2f  last pack %.2f  last resolve %.2f" % (
+    np.nanmin(T[:, 1]), np.nanmax(T[:, 1]), np.nanmax(T[:, 4]), np.nanmax(T[:, 8])))
