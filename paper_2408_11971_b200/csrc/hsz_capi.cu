@@ -421,6 +421,18 @@ int hsz_trace_read(unsigned long long* host, int cap, int reset) {
 int hsz_trace_lookback(unsigned int* out3) {
 #ifdef HSZ_TRACE
   cudaDeviceSynchronize();
+  {
+    unsigned long long c[2] = {0, 0};
+    cudaMemcpyFromSymbol(&c[0], g_lb_cycles_round, 8);
+    cudaMemcpyFromSymbol(&c[1], g_lb_cycles_total, 8);
+    unsigned int calls = 0;
+    cudaMemcpyFromSymbol(&calls, g_lb_calls, 4);
+    if (calls) fprintf(stderr, "lookback cycles: round-load %.0f total %.0f per resolve\n",
+                       double(c[0]) / calls, double(c[1]) / calls);
+    const unsigned long long z = 0;
+    cudaMemcpyToSymbol(g_lb_cycles_round, &z, 8);
+    cudaMemcpyToSymbol(g_lb_cycles_total, &z, 8);
+  }
   unsigned int v[3] = {0, 0, 0};
   cudaMemcpyFromSymbol(&v[0], g_lb_rounds, sizeof(unsigned));
   cudaMemcpyFromSymbol(&v[1], g_lb_sleeps, sizeof(unsigned));

@@ -361,11 +361,12 @@ __device__ __forceinline__ void lb_publish(uint64_t* words, uint64_t tile, uint6
 }
 
 #ifndef HSZ_LB2_PER_LANE
-#define HSZ_LB2_PER_LANE 4
+#define HSZ_LB2_PER_LANE 2
 #endif
 
 #ifdef HSZ_TRACE
 __device__ unsigned int g_lb_rounds, g_lb_sleeps, g_lb_calls;
+__device__ unsigned long long g_lb_cycles_round, g_lb_cycles_total;
 #endif
 
 // one full warp: exclusive prefix of `tile` (its aggregate already published);
@@ -387,9 +388,14 @@ __device__ __forceinline__ void lb_resolve(uint64_t* words, uint64_t tile, uint6
 #ifdef HSZ_TRACE
   unsigned rounds = 0, sleeps = 0;
 #endif
+#ifdef HSZ_TRACE
+  const long long c_start = clock64();
+  long long c_round = 0;
+#endif
   while (true) {
 #ifdef HSZ_TRACE
     ++rounds;
+    const long long c0 = clock64();
 #endif
     // lane covers tiles base - lane*L - j, j = 0..L-1 (nearest first).  All
     // loads are issued before any is consumed (one L2 round trip per round).
@@ -414,6 +420,9 @@ __device__ __forceinline__ void lb_resolve(uint64_t* words, uint64_t tile, uint6
       found |= ok & inc;
     }
     const unsigned fm = __ballot_sync(kFull, found);
+#ifdef HSZ_TRACE
+    c_round += clock64() - c0;
+#endif
     const int first = fm ? (__ffs(fm) - 1) : 32;
     // lanes up to and including the first one holding an inclusive must have
     // read only valid records before (or at) their inclusive one
@@ -447,6 +456,8 @@ __device__ __forceinline__ void lb_resolve(uint64_t* words, uint64_t tile, uint6
     atomicAdd(&g_lb_rounds, rounds);
     atomicAdd(&g_lb_sleeps, sleeps);
     atomicAdd(&g_lb_calls, 1u);
+    atomicAdd(&g_lb_cycles_round, static_cast<unsigned long long>(c_round));
+    atomicAdd(&g_lb_cycles_total, static_cast<unsigned long long>(clock64() - c_start));
 #endif
   }
   *excl_s = sum_s;

@@ -116,7 +116,8 @@ struct Smem {
   uint64_t bar;                   // input full (TMA or "no more tiles")
   uint64_t in_empty;              // compute warps consumed S.in        (128 arrivals)
   uint64_t st_full[2];            // tile staged in pk[b]                (128 arrivals)
-  uint64_t st_empty[2];           // pk[b] copied out by the service warp (1 arrival)
+  uint64_t st_empty[2];           // pk[b] copied out by the copy warp      (1 arrival)
+  uint64_t tile_of[2];            // tile id staged in pk[b]
   uint64_t cur, epoch;
   uint64_t excl_s[2], excl_p[2];  // resolved offsets of the staged tile (service warp; by parity)
   uint32_t agg_ts[2], agg_tp[2];  // aggregate of the current tile (compute warps; by parity)
@@ -150,7 +151,7 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 // named barriers: 1 = the 128 compute threads, 2 = "input consumed"
 // (compute arrive, service sync), 3 = "offsets ready" (all 160 threads)
 constexpr int kCompute = 128;
-constexpr int kThreadsWS = kCompute + 32;
+constexpr int kThreadsWS = kCompute + 64;   // + TMA warp (tickets, loads) + placement warp
 #ifndef HSZ_ENC_CTAS
 #define HSZ_ENC_CTAS 4   // CTAs per SM the register budget is sized for
 #endif
@@ -255,7 +256,8 @@ __device__ __forceinline__ void pack_block(const BlockCode& bc, uint32_t a, uint
 // ---------------------------------------------------------------------------
 // placement of the staged tile (compute threads; offsets from the service warp)
 
-constexpr uint32_t kSelfPlaced = 0xFFFFFFFFu;   // cur_ts marker: exact-path tile placed itself
+constexpr uint32_t kSelfPlaced = 0xFFFFFFFFu;   // agg_ts marker: exact-path tile placed itself
+constexpr uint32_t kDone = 0xFFFFFFFEu;         // agg_ts marker: no more tiles (copy warp exits)
 
 // copy a staged tile to its resolved offsets; `rank`/`nthr` = this thread's
 // index among the threads sharing the copy
@@ -369,26 +371,36 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
   const uint64_t epoch = S.epoch;
 
   if (warp == kCompute / 32) {
-    // =========================== service warp ===========================
-    // per tile k handed to the compute warps (all hand-offs are mbarriers):
-    //   wait in_empty (tile k consumed) | TMA(tile k+1) or "done", draw a
-    //   ticket | wait st_full (tile k-1 staged) | resolve + copy out tile k-1
-    //   | arrive st_empty
-    uint64_t ahead = ~0ull;
-    uint64_t t = ~0ull;
+    // ============================ TMA warp ==============================
+    // per tile k handed to the compute warps: wait in_empty (tile k consumed)
+    // | TMA(tile k+1) or "done" | draw the ticket after it
+    uint64_t t = ~0ull, ahead = ~0ull;
     if (lane == 0) {
       t = draw(epoch);
       issue(t);
       if (t < ntiles) ahead = draw(epoch);
+      for (uint32_t k = 0; t < ntiles; ++k) {
+        mbar_wait_parity(&S.in_empty, k & 1u);   // S.in holds no unread data
+        const uint64_t nx = ahead;
+        issue(nx);
+        if (nx < ntiles) ahead = draw(epoch);
+        t = nx;
+      }
     }
-    t = __shfl_sync(kFull, t, 0);
-    uint64_t prev = ~0ull;
-    uint32_t k = 0;   // index (in this CTA) of tile t
-    auto place = [&](uint64_t tile, uint32_t kk) {   // tile = the kk-th tile of this CTA
+    return;
+  }
+
+  if (warp == kCompute / 32 + 1) {
+    // =========================== placement warp ===========================
+    // the kk-th tile of this CTA: wait st_full[b] | resolve its offsets (look-
+    // back) | copy it out of pk[b] | arrive st_empty[b]
+    for (uint32_t kk = 0;; ++kk) {
       const int b = kk & 1;
       mbar_wait_parity(&S.st_full[b], (kk >> 1) & 1u);
       const uint32_t pts = S.agg_ts[b], ptp = S.agg_tp[b];
+      if (pts == kDone) break;
       if (pts != kSelfPlaced) {
+        const uint64_t tile = S.tile_of[b];
         trace_tile(tile, 7);
         resolve_tile(S, out, tile, epoch, ntiles, pts, ptp, b);
         __syncwarp();
@@ -397,29 +409,7 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.st_empty[b]);
-    };
-    while (t < ntiles) {
-      mbar_wait_parity(&S.in_empty, k & 1u);     // S.in holds no unread data
-      uint64_t nx = ~0ull, drawn = ~0ull;
-      if (lane == 0) {
-        nx = ahead;
-        issue(nx);
-        if (nx < ntiles) drawn = atom_add_relaxed(lw.ticket, 1);   // consumed below
-      }
-      nx = __shfl_sync(kFull, nx, 0);
-      if (prev != ~0ull) place(prev, k - 1);
-      if (lane == 0 && drawn != ~0ull) {
-        if (drawn == last_draw) {
-          st_relaxed(lw.ticket, 0);
-          st_release(lw.epoch, epoch + 1);
-        }
-        ahead = drawn;
-      }
-      prev = t;
-      t = nx;
-      ++k;
     }
-    if (prev != ~0ull) place(prev, k - 1);
     return;
   }
 
@@ -435,7 +425,13 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
     mbar_wait_parity(&S.bar, phase);
     phase ^= 1u;
     const uint64_t cur = S.cur;
-    if (cur >= ntiles) break;
+    if (cur >= ntiles) {
+      // stop the placement warp: a "done" marker in the next buffer it waits on
+      if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);
+      if (tid == 0) S.agg_ts[par] = kDone;
+      mbar_arrive(&S.st_full[par]);
+      break;
+    }
     bool wide = false;
     uint32_t qb[K];
     trace_tile(cur, 1);
@@ -502,7 +498,9 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
       }
       wide = bar_or_compute(wide);   // ... and every read of S.in is done
       mbar_arrive(&S.in_empty);        // the service warp may refill S.in
+      trace_tile(cur, 5);
       if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);   // tile k-2 copied out
+      trace_tile(cur, 6);
     }
     uint32_t ts = 0, tp = 0;
     if (!wide) {
@@ -522,6 +520,7 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
         lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
         S.agg_ts[par] = ts;
         S.agg_tp[par] = tp;
+        S.tile_of[par] = cur;
       }
       trace_tile(cur, 3);
       if (active) {

@@ -44,7 +44,7 @@ nt = tile.max() + 1
 T = np.full((nt, 9), np.nan)
 T[tile, tag] = t
 print("records", n, "tiles", nt, "span us %.1f" % np.nanmax(T))
-names = {(1, 2): "load wait", (2, 3): "quant+code+scan", (3, 4): "pack", (4, 7): "staged->placing",
+names = {(1, 2): "load wait", (2, 5): "quant", (5, 6): "st_empty wait", (6, 3): "code+scan", (3, 4): "pack", (4, 7): "staged->placing",
          (7, 8): "svc resolve+copy", (3, 8): "publish->placed"}
 for (a0, a1), nm in names.items():
     d = T[:, a1] - T[:, a0]
