@@ -11,6 +11,7 @@
 #include <cudaTypedefs.h>
 
 #include "hsz_common.cuh"
+#include "hsz_dec32.cuh"
 #include "hsz_enc32.cuh"
 #include "hsz_generic.cuh"
 #include "hsz_k32.cuh"
@@ -669,14 +670,30 @@ int hsz_scalar_mul(const uint8_t* widths, const int32_t* outliers, const uint8_t
   const uint64_t nt = ceil_div(nb, kTileBlocks);
   const double d = 2.0 * eps;
   if (k == 32) {
-    k32::SrcSmul src;
-    src.in = k32::StreamIn{widths, outliers, signs, payload, toff, n, nb, tail_len_of(n, 32)};
-    src.rs = rs;
-    src.d = d;
-    src.rsd = static_cast<double>(rs);
-    src.small_rs = rs > -(1ll << 21) && rs < (1ll << 21);
+    const d32::StreamIn in{widths, outliers, signs, payload, toff, n, nb, nt, tail_len_of(n, 32)};
+    d32::SmulParams sp;
+    sp.rs = rs;
+    sp.d = d;
+    sp.rsd = static_cast<double>(rs);
+    sp.small_rs = (rs > -(1ll << 23) && rs < (1ll << 23)) ? 1 : 0;
     const k32::EncodeOut out{ow, oo, os, sign_cap, op, payload_cap, otoff, err, ws};
-    return launch_encode32(src, out, n, st);
+    constexpr int smem = static_cast<int>(d32::kSmulSmemBytes);
+    static int resident = 0, resident_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (resident_dev != dev) {
+      cudaFuncSetAttribute(d32::smul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(d32::smul_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
+      int per_sm = 0, sms = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d32::smul_kernel, e32::kThreadsWS, smem);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      resident = (per_sm > 0 ? per_sm : 1) * sms;
+      resident_dev = dev;
+    }
+    const uint64_t grid = nt < static_cast<uint64_t>(resident) ? nt : static_cast<uint64_t>(resident);
+    d32::smul_kernel<<<static_cast<unsigned>(grid), e32::kThreadsWS, smem, st>>>(in, sp, out);
+    return launch_status();
   }
   if (!scratch) return HSZ_EINVAL;
   int64_t* bins = static_cast<int64_t*>(scratch);

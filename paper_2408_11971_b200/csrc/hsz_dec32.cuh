@@ -1,0 +1,420 @@
+// Stream-tile front end for block_len 32 (decode side) and the register-
+// resident scalar multiply.
+//
+// A tile = 128 blocks.  The TMA warp stages one input tile per mbarrier phase:
+//   * its widths / outliers with plain loads by the 32 lanes (640 bytes);
+//   * its sign bytes and payload bytes with two cp.async.bulk copies
+//     (UBLKCP), located by the input stream's tile-offset cache
+//     (toff[2t], toff[2t+1] .. toff[2t+2], toff[2t+3]);
+//   * a tile whose payload does not fit the staging buffer is read in place.
+// Compute thread b then decodes block b into 32 registers (prefix sums of
+// the signed residuals seeded with the outlier, codec.py:228-262).
+//
+// scalar_mul (ops.py:199-225) = this front + the exact rescale
+// t = RN(2eps * RN(bin * rs)), bin' = round-half-away(t) + the encoder back
+// half of hsz_enc32.cuh (code, scan, publish, pack, placement warp).
+#pragma once
+
+#include "hsz_enc32.cuh"
+
+namespace hsz {
+namespace d32 {
+
+constexpr int K = 32;
+constexpr int TB = kTileBlocks;
+constexpr int kCompute = e32::kCompute;
+constexpr uint32_t kSignCap = TB * 4 + 32;   // staged sign bytes (+ 16-byte alignment slack)
+constexpr uint32_t kPayCap = 16384;          // staged payload bytes
+constexpr int kFastW = 24;                   // register decode: widths <= 24, |outlier| < 2^29
+
+struct StreamIn {
+  const uint8_t* widths;
+  const int32_t* outliers;
+  const uint8_t* signs;
+  const uint8_t* payload;
+  const uint64_t* toff;
+  uint64_t n;
+  uint64_t nblocks;
+  uint64_t ntiles;
+  uint32_t tail_len;
+};
+
+struct InTile {
+  alignas(16) unsigned char sgn[kSignCap];
+  alignas(16) unsigned char pay[kPayCap];
+  alignas(16) int32_t o[TB];
+  alignas(16) uint8_t w[TB];
+  uint64_t tile;       // >= ntiles: no more tiles
+  uint64_t gs0, gp0;   // global offsets of the tile's first sign / payload byte
+  uint32_t soff;       // offset of that sign byte within sgn[]
+  uint32_t poff;       // offset of that payload byte within pay[] (staged tiles)
+  uint32_t staged;     // payload staged (else read in place from global memory)
+};
+
+__device__ __forceinline__ void bulk_g2s_(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// TMA warp (all 32 lanes): stage tile t (or "no more tiles") into `it`,
+// completing one phase of `bar` (count 1: lane 0's arrive).
+__device__ __forceinline__ void stage_tile(const StreamIn& s, uint64_t t, InTile& it, uint64_t* bar) {
+  const int lane = threadIdx.x & 31;
+  if (t >= s.ntiles) {
+    if (lane == 0) {
+      it.tile = t;
+      mbar_arrive(bar);
+    }
+    __syncwarp();
+    return;
+  }
+  uint64_t v = 0;
+  if (lane < 4) v = s.toff[2 * t + lane];
+  const uint64_t s0 = __shfl_sync(kFull, v, 0), p0 = __shfl_sync(kFull, v, 1);
+  const uint64_t s1 = __shfl_sync(kFull, v, 2), p1 = __shfl_sync(kFull, v, 3);
+  // widths / outliers: 4 blocks per lane
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t lb = 4 * lane + j;
+    const uint64_t b = t * TB + lb;
+    uint8_t w = 0;
+    int32_t o = 0;
+    if (b < s.nblocks) {
+      w = s.widths[b];
+      o = s.outliers[b];
+    }
+    it.w[lb] = w;
+    it.o[lb] = o;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const uint64_t s_lo = s0 & ~15ull, s_hi = (s1 + 15) & ~15ull;
+    const uint64_t p_lo = p0 & ~15ull, p_hi = (p1 + 15) & ~15ull;
+    const uint32_t sbytes = static_cast<uint32_t>(s_hi - s_lo);
+    const uint32_t pbytes = static_cast<uint32_t>(p_hi - p_lo);
+    const bool staged = pbytes <= kPayCap && sbytes <= kSignCap;
+    it.tile = t;
+    it.gs0 = s0;
+    it.gp0 = p0;
+    it.soff = static_cast<uint32_t>(s0 - s_lo);
+    it.poff = static_cast<uint32_t>(p0 - p_lo);
+    it.staged = staged ? 1u : 0u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (staged && (sbytes | pbytes)) {
+      mbar_arrive_expect_tx(bar, sbytes + pbytes);
+      if (sbytes) bulk_g2s_(it.sgn, s.signs + s_lo, sbytes, bar);
+      if (pbytes) bulk_g2s_(it.pay, s.payload + p_lo, pbytes, bar);
+    } else {
+      mbar_arrive(bar);
+    }
+  }
+  __syncwarp();
+}
+
+// Register decode of this thread's block (w <= kFastW, |o| < 2^29): bins as
+// int32 (|bin| < 2^30); elements past `len` replicate the last live bin.
+__device__ __forceinline__ void decode_block(const unsigned char* sgn, const unsigned char* pay,
+                                             uint32_t w, int32_t o, int len, int32_t (&q)[K]) {
+  q[0] = o;
+  if (w == 0) {
+#pragma unroll
+    for (int i = 1; i < K; ++i) q[i] = o;
+    return;
+  }
+  const uint32_t sw = bswap32(*reinterpret_cast<const uint32_t*>(sgn));
+  const uint32_t* pw = reinterpret_cast<const uint32_t*>(pay);
+  const uint32_t mask = (1u << w) - 1u;
+  uint64_t win = bswap32(pw[0]);
+  int nb = 32 - static_cast<int>(w);   // bits left after slot 0's (zero) field
+  int wi = 1;
+  int32_t P = o;
+#pragma unroll
+  for (int i = 1; i < K; ++i) {
+    if (nb < static_cast<int>(w)) {
+      win = (win << 32) | bswap32(pw[wi++]);
+      nb += 32;
+    }
+    nb -= static_cast<int>(w);
+    const int32_t mag = static_cast<int32_t>(static_cast<uint32_t>(win >> nb) & mask);
+    const int32_t neg = -static_cast<int32_t>((sw >> (31 - i)) & 1u);
+    const int32_t d = (i < len) ? ((mag ^ neg) - neg) : 0;
+    P += d;
+    q[i] = P;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// scalar multiply
+
+struct SmulSmem {
+  InTile in;
+  unsigned char pk[2][e32::kBufBytes];
+  alignas(16) uint32_t sgn[2][TB];
+  uint32_t bes[TB], bep[TB];      // per-block offsets within the input tile (exact path)
+  uint64_t bar, in_empty, st_full[2], st_empty[2];
+  uint64_t excl_s[2], excl_p[2];
+  uint32_t agg_ts[2], agg_tp[2];
+  uint64_t tile_of[2];
+  uint64_t epoch;
+  uint32_t scan[4];
+  uint32_t wsb[4], wpb[4];
+};
+
+// exact (64/128-bit) bins of the output for the warp-per-block fallback: the
+// input block is decoded from global memory
+struct SrcSmulExact {
+  StreamIn in;
+  const SmulSmem* S;
+  int64_t rs;
+  double d;
+  __device__ __forceinline__ int64_t lane_bin(int lb, int lane, int len, uint32_t* flags) {
+    uint32_t f = 0;
+    const int64_t q = k32::decode_lane(in.signs, in.payload, S->in.w[lb], S->in.o[lb],
+                                       S->in.gs0 + S->bes[lb], S->in.gp0 + S->bep[lb], len, lane, &f);
+    *flags |= f;
+    if (f || lane >= len) return 0;
+    return rescale1(product_rn(q, rs), d, flags);
+  }
+};
+
+__device__ __forceinline__ void smul_copy_staged(SmulSmem& S, const k32::EncodeOut& out,
+                                                 uint32_t ts, uint32_t tp, int par, uint32_t rank,
+                                                 uint32_t nthr) {
+  const uint64_t es = S.excl_s[par], ep = S.excl_p[par];
+  if (es == ~0ull) return;
+  uint32_t* dsg = reinterpret_cast<uint32_t*>(out.signs + es);
+  for (uint32_t i = rank; i < ((ts + 3u) >> 2); i += nthr) dsg[i] = S.sgn[par][i];
+  const uint32_t* pbuf = reinterpret_cast<const uint32_t*>(S.pk[par]);
+  uint32_t* dst = reinterpret_cast<uint32_t*>(out.payload + ep);
+  const uint32_t nw = (tp + 3u) >> 2;
+  uint32_t head = static_cast<uint32_t>(((16u - (ep & 15u)) & 15u) >> 2);
+  head = head < nw ? head : nw;
+  if (rank < head) dst[rank] = pbuf[e32::swz_word(rank)];
+  const uint32_t nv = (nw - head) >> 2;
+  uint4* dv = reinterpret_cast<uint4*>(dst + head);
+  for (uint32_t i = rank; i < nv; i += nthr) {
+    const uint32_t k = head + 4u * i;
+    dv[i] = make_uint4(pbuf[e32::swz_word(k)], pbuf[e32::swz_word(k + 1)],
+                       pbuf[e32::swz_word(k + 2)], pbuf[e32::swz_word(k + 3)]);
+  }
+  const uint32_t rest = head + 4u * nv + rank;
+  if (rest < nw) dst[rest] = pbuf[e32::swz_word(rest)];
+}
+
+__device__ __forceinline__ void smul_resolve(SmulSmem& S, const k32::EncodeOut& out, uint64_t tile,
+                                             uint64_t epoch, uint64_t ntiles, uint32_t ts,
+                                             uint32_t tp, int par) {
+  const int lane = threadIdx.x & 31;
+  uint64_t es, ep;
+  lb_resolve(lb_words(out.ws), tile, epoch, ts, tp, &es, &ep);
+  if (lane == 0) {
+    out.toff[2 * tile] = es;
+    out.toff[2 * tile + 1] = ep;
+    if (tile == ntiles - 1) {
+      out.toff[2 * ntiles] = es + ts;
+      out.toff[2 * ntiles + 1] = ep + tp;
+    }
+    const bool fits = es + ts <= out.sign_cap && ep + tp <= out.payload_cap;
+    if (!fits) atomicOr(out.err, HSZ_ERR_CAPACITY);
+    S.excl_s[par] = fits ? es : ~0ull;
+    S.excl_p[par] = ep;
+  }
+}
+
+struct SmulParams {
+  int64_t rs;
+  double d;      // 2 eps
+  double rsd;    // (double) rs
+  int small_rs;  // |rs| < 2^23: every register-path product is exact in float64
+};
+
+// Persistent, warp-specialised like the compressor: warps 0-3 decode +
+// rescale + code + pack, warp 4 stages input tiles, warp 5 places output
+// tiles (look-back + copy).
+__global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
+    smul_kernel(StreamIn in, SmulParams sp, k32::EncodeOut out) {
+  extern __shared__ unsigned char smraw[];
+  const uint32_t a0 = smem_u32(smraw);
+  SmulSmem& S = *reinterpret_cast<SmulSmem*>(smraw + (((a0 + 1023u) & ~1023u) - a0));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint64_t ntiles = in.ntiles, nblocks = in.nblocks;
+  LookbackWs lw = LookbackWs::bind(out.ws, ntiles);
+  const uint64_t last_draw = ntiles + gridDim.x - 1;
+  if (tid == kCompute) {
+    mbar_init(&S.bar, 1);
+    mbar_init(&S.in_empty, kCompute);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&S.st_full[b], kCompute);
+      mbar_init(&S.st_empty[b], 1);
+    }
+    fence_mbar_init();
+    S.epoch = ld_acquire(lw.epoch);
+  }
+  __syncthreads();
+  const uint64_t epoch = S.epoch;
+  auto draw = [&]() -> uint64_t {
+    const uint64_t t = atom_add_relaxed(lw.ticket, 1);
+    if (t == last_draw) {
+      st_relaxed(lw.ticket, 0);
+      st_release(lw.epoch, epoch + 1);
+    }
+    return t;
+  };
+
+  if (warp == kCompute / 32) {
+    // ============================ TMA warp ==============================
+    uint64_t t = 0, ahead = 0;
+    if (lane == 0) {
+      t = draw();
+      if (t < ntiles) ahead = draw();
+    }
+    t = __shfl_sync(kFull, t, 0);
+    ahead = __shfl_sync(kFull, ahead, 0);
+    stage_tile(in, t, S.in, &S.bar);
+    for (uint32_t k = 0; t < ntiles; ++k) {
+      mbar_wait_parity(&S.in_empty, k & 1u);
+      const uint64_t nx = ahead;
+      if (lane == 0 && nx < ntiles) ahead = draw();
+      ahead = __shfl_sync(kFull, ahead, 0);
+      stage_tile(in, nx, S.in, &S.bar);
+      t = nx;
+    }
+    return;
+  }
+
+  if (warp == kCompute / 32 + 1) {
+    // =========================== placement warp ===========================
+    for (uint32_t kk = 0;; ++kk) {
+      const int b = kk & 1;
+      mbar_wait_parity(&S.st_full[b], (kk >> 1) & 1u);
+      const uint32_t pts = S.agg_ts[b], ptp = S.agg_tp[b];
+      if (pts == e32::kDone) break;
+      if (pts != e32::kSelfPlaced) {
+        smul_resolve(S, out, S.tile_of[b], epoch, ntiles, pts, ptp, b);
+        __syncwarp();
+        smul_copy_staged(S, out, pts, ptp, b, lane, 32);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.st_empty[b]);
+    }
+    return;
+  }
+
+  // =========================== compute warps ===========================
+  uint32_t phase = 0, flags = 0;
+  int par = 0, k = 0;
+  while (true) {
+    mbar_wait_parity(&S.bar, phase);
+    phase ^= 1u;
+    const uint64_t cur = S.in.tile;
+    if (cur >= ntiles) {
+      if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);
+      if (tid == 0) S.agg_ts[par] = e32::kDone;
+      mbar_arrive(&S.st_full[par]);
+      break;
+    }
+    // ---- locate and decode this thread's block -------------------------------
+    const uint64_t gb = cur * TB + tid;
+    const bool active = gb < nblocks;
+    const int len = !active ? 0 : (gb == nblocks - 1 ? static_cast<int>(in.tail_len) : K);
+    uint32_t w = S.in.w[tid];
+    const int32_t o = S.in.o[tid];
+    bool bad = w > 64;
+    if (bad) {
+      flags |= HSZ_ERR_BAD_WIDTH;
+      w = 0;
+    }
+    const uint32_t isb = w ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
+    const uint32_t ipb = (static_cast<uint32_t>(len) * w + 7u) >> 3;
+    uint32_t itot;
+    const uint32_t iex = e32::cta_scan(isb | (ipb << 10), S.scan, &itot);
+    const uint32_t ies = iex & 1023u, iep = iex >> 10;
+    S.bes[tid] = ies;
+    S.bep[tid] = iep;
+    const bool fast_in = S.in.staged && w <= static_cast<uint32_t>(kFastW) && o > -(1 << 29) && o < (1 << 29);
+    bool exact = !fast_in || !sp.small_rs;
+    uint32_t qb[K];
+    if (!exact) {
+      int32_t q[K];
+      decode_block(S.in.sgn + S.in.soff + ies, S.in.pay + S.in.poff + iep, w, o, len, q);
+      // rescale: |bin| < 2^30, |rs| < 2^23 -> bin * rs exact in float64;
+      // then ops.py:199-208 verbatim
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        const double pd = __dmul_rn(i32_to_double(q[i]), sp.rsd);
+        const double tt = __dmul_rn(sp.d, pd);
+        const double mag = floor(__dadd_rn(fabs(tt), 0.5));
+        exact |= !(mag < 1073741823.0);
+        const int32_t mi = __double2loint(__dadd_rn(mag, 6755399441055744.0));
+        qb[i] = static_cast<uint32_t>(tt < 0.0 ? -mi : mi);
+      }
+    }
+    exact = e32::bar_or_compute(exact);   // ... every read of S.in's staged bytes is done
+    if (!exact) mbar_arrive(&S.in_empty);
+    if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);
+    uint32_t ts = 0, tp = 0;
+    if (!exact) {
+      e32::BlockCode bc;
+      e32::block_code(qb, len, bc);
+      const uint32_t sb = (bc.w && active) ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
+      const uint32_t pb = (static_cast<uint32_t>(len) * bc.w + 7u) >> 3;
+      uint32_t tot;
+      const uint32_t ex = e32::cta_scan(sb | (pb << 10), S.scan, &tot);
+      const uint32_t es = ex & 1023u, ep = ex >> 10;
+      ts = tot & 1023u;
+      tp = tot >> 10;
+      if (tid == 0) {
+        lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
+        S.agg_ts[par] = ts;
+        S.agg_tp[par] = tp;
+        S.tile_of[par] = cur;
+      }
+      if (active) {
+        out.widths[gb] = static_cast<uint8_t>(bc.w);
+        out.outliers[gb] = static_cast<int32_t>(qb[0]);
+      }
+      if (sb) S.sgn[par][es >> 2] = bswap32(bc.sg);
+      e32::pack_block(bc, ep >> 2, reinterpret_cast<uint32_t*>(S.pk[par]));
+    } else {
+      // exact warp-per-block path, decoding from global memory; places itself
+      SrcSmulExact src{in, &S, sp.rs, sp.d};
+      flags |= k32::fallback_sizes(src, out, cur, nblocks, in.tail_len, S.wsb, S.wpb);
+      e32::bar_sync_n(1, kCompute);
+      ts = S.wsb[0] + S.wsb[1] + S.wsb[2] + S.wsb[3];
+      tp = S.wpb[0] + S.wpb[1] + S.wpb[2] + S.wpb[3];
+      if (warp == 0) {
+        if (lane == 0) {
+          lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
+          S.agg_ts[par] = e32::kSelfPlaced;
+        }
+        __syncwarp();
+        smul_resolve(S, out, cur, epoch, ntiles, ts, tp, par);
+      }
+      e32::bar_sync_n(1, kCompute);
+      if (S.excl_s[par] != ~0ull) {
+        uint64_t gs = S.excl_s[par], gp = S.excl_p[par];
+        for (int i = 0; i < warp; ++i) {
+          gs += S.wsb[i];
+          gp += S.wpb[i];
+        }
+        k32::fallback_pack(src, out, cur, nblocks, in.tail_len, gs, gp,
+                           reinterpret_cast<uint32_t*>(S.pk[par]) + warp * 64);
+      }
+      e32::bar_sync_n(1, kCompute);
+      mbar_arrive(&S.in_empty);   // the per-block offsets in S.bes/bep are no longer needed
+    }
+    mbar_arrive(&S.st_full[par]);
+    par ^= 1;
+    ++k;
+  }
+  flags = __reduce_or_sync(kFull, flags);
+  if (lane == 0 && flags) atomicOr(out.err, flags);
+}
+
+constexpr uint32_t kSmulSmemBytes = sizeof(SmulSmem) + 1024;
+
+}  // namespace d32
+}  // namespace hsz
