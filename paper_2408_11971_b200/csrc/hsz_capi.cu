@@ -283,6 +283,54 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+// 2-D tensor map over a float32 field viewed as rows of 32 values (one block
+// per row), 128-row boxes, 128-byte swizzle; false if the field does not allow it
+static bool make_rows_map_f32(const float* x, uint64_t n, CUtensorMap* map) {
+  std::memset(map, 0, sizeof(*map));
+  const uint64_t rows = n / 32;
+  if ((reinterpret_cast<uintptr_t>(x) & 15u) != 0 || rows < static_cast<uint64_t>(kTileBlocks) ||
+      rows >= (1ull << 31))
+    return false;
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {32, rows};
+  cuuint64_t strides[1] = {128};
+  cuuint32_t box[2] = {32, static_cast<cuuint32_t>(kTileBlocks)};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(x), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int kMode>
+static int launch_decode_pipe(const d32::StreamIn& in, float* out, double d, uint64_t* mout,
+                              void* ws, uint32_t* err, cudaStream_t st) {
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  int use_tma = 0;
+  if (kMode == 2) use_tma = make_rows_map_f32(out, in.n, &map) ? 1 : 0;
+  constexpr int smem = static_cast<int>(d32::dec_smem_bytes<kMode>());
+  auto kern = d32::decode_pipe_kernel<kMode>;
+  static int resident = 0, resident_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (resident_dev != dev) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, d32::kDecThreads, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    resident = (per_sm > 0 ? per_sm : 1) * sms;
+    resident_dev = dev;
+  }
+  const uint64_t grid = in.ntiles < static_cast<uint64_t>(resident) ? in.ntiles : static_cast<uint64_t>(resident);
+  const d32::DecF32Sink fs{out, d, d * 0x1p33 >= 3.4028234663852886e38};
+  const d32::MomentsSink ms{mout, ws};
+  kern<<<static_cast<unsigned>(grid), d32::kDecThreads, smem, st>>>(map, in, fs, ms, use_tma, err);
+  return launch_status();
+}
+
 // compress of a float32 field, block_len 32: register-resident encoder with
 // a swizzled 2-D TMA tile load when the field allows it
 static int launch_compress_f32(const float* x, uint64_t n, const QuantConst& c,
@@ -589,11 +637,8 @@ int hsz_decode(const uint8_t* widths, const int32_t* outliers, const uint8_t* si
     const unsigned g = static_cast<unsigned>(nt);
     switch (out_kind) {
       case HSZ_OUT_F32: {
-        constexpr int smem = k32::DecodeSmem<k32::SinkF32>::kBytes;
-        allow_smem(k32::decode_kernel<k32::SinkF32>, smem);
-        k32::decode_kernel<k32::SinkF32><<<g, k32::kThreads, smem, st>>>(
-            s, k32::SinkF32{static_cast<float*>(out), d, d * 0x1p33 >= 3.4028234663852886e38}, err);
-        break;
+        const d32::StreamIn in{widths, outliers, signs, payload, toff, n, nb, nt, tail_len_of(n, 32)};
+        return launch_decode_pipe<2>(in, static_cast<float*>(out), d, nullptr, nullptr, err, st);
       }
       case HSZ_OUT_F64: {
         constexpr int smem = k32::DecodeSmem<k32::SinkF64>::kBytes;
@@ -714,13 +759,9 @@ int hsz_moments(const uint8_t* widths, const int32_t* outliers, const uint8_t* s
   const uint64_t nb = ceil_div(n, k);
   const uint64_t nt = ceil_div(nb, kTileBlocks);
   if (k == 32) {
-    const k32::StreamIn s{widths, outliers, signs, payload, toff, n, nb, tail_len_of(n, 32)};
-    constexpr int smem = k32::kStageFast;
-    if (want_sq)
-      k32::moments_kernel<true><<<static_cast<unsigned>(nt), k32::kThreads, smem, st>>>(s, out, err, ws);
-    else
-      k32::moments_kernel<false><<<static_cast<unsigned>(nt), k32::kThreads, smem, st>>>(s, out, err, ws);
-    return launch_status();
+    const d32::StreamIn in{widths, outliers, signs, payload, toff, n, nb, nt, tail_len_of(n, 32)};
+    if (want_sq) return launch_decode_pipe<1>(in, nullptr, 0.0, out, ws, err, st);
+    return launch_decode_pipe<0>(in, nullptr, 0.0, out, ws, err, st);
   }
   const gen::GStream s{widths, outliers, signs, payload, toff, n, k, nb};
   ops::gen_moments_kernel<<<static_cast<unsigned>(nt), gen::kThreads, 0, st>>>(s, want_sq, out, err, ws);

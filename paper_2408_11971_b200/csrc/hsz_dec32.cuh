@@ -115,9 +115,11 @@ __device__ __forceinline__ void stage_tile(const StreamIn& s, uint64_t t, InTile
 }
 
 // Register decode of this thread's block (w <= kFastW, |o| < 2^29): bins as
-// int32 (|bin| < 2^30); elements past `len` replicate the last live bin.
-__device__ __forceinline__ void decode_block(const unsigned char* sgn, const unsigned char* pay,
-                                             uint32_t w, int32_t o, int len, int32_t (&q)[K]) {
+// int32 (|bin| < 2^30).  kFull: a full block (len == 32, no tail checks);
+// otherwise elements past `len` replicate the last live bin.
+template <bool kFull>
+__device__ __forceinline__ void decode_block_t(const unsigned char* sgn, const unsigned char* pay,
+                                               uint32_t w, int32_t o, int len, int32_t (&q)[K]) {
   q[0] = o;
   if (w == 0) {
 #pragma unroll
@@ -139,10 +141,20 @@ __device__ __forceinline__ void decode_block(const unsigned char* sgn, const uns
     }
     nb -= static_cast<int>(w);
     const int32_t mag = static_cast<int32_t>(static_cast<uint32_t>(win >> nb) & mask);
-    const int32_t neg = -static_cast<int32_t>((sw >> (31 - i)) & 1u);
-    const int32_t d = (i < len) ? ((mag ^ neg) - neg) : 0;
+    const int32_t neg = static_cast<int32_t>(sw << i) >> 31;   // element i's sign bit
+    int32_t d = (mag ^ neg) - neg;
+    if (!kFull) d = (i < len) ? d : 0;
     P += d;
     q[i] = P;
+  }
+}
+
+__device__ __forceinline__ void decode_block(const unsigned char* sgn, const unsigned char* pay,
+                                             uint32_t w, int32_t o, int len, int32_t (&q)[K]) {
+  if (len == K) {
+    decode_block_t<true>(sgn, pay, w, o, len, q);
+  } else {
+    decode_block_t<false>(sgn, pay, w, o, len, q);
   }
 }
 
@@ -415,6 +427,271 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
 }
 
 constexpr uint32_t kSmulSmemBytes = sizeof(SmulSmem) + 1024;
+
+// ---------------------------------------------------------------------------
+// Decode pipeline (moments, decompress to float32): persistent CTAs of 4
+// compute warps + 1 TMA warp; tiles by grid stride (no ordering needed),
+// input double-buffered.
+
+template <int kMode>
+struct DecSmem {
+  InTile in[2];
+  alignas(1024) unsigned char out[kMode == 2 ? e32::kBufBytes : 16];   // decompress: value tile
+  uint64_t full[2], empty[2];
+  uint32_t scan[4];
+};
+template <int kMode>
+constexpr uint32_t dec_smem_bytes() { return sizeof(DecSmem<kMode>) + 1024; }
+constexpr int kDecThreads = kCompute + 32;
+
+// the 32-lane exact decode of one tile's blocks (any width up to 64, any
+// outlier), reading the sections in place; calls f(local block, lane, bin,
+// live) for every element
+template <class F>
+__device__ __forceinline__ uint32_t exact_tile(const StreamIn& in, const InTile& it, uint32_t es,
+                                               uint32_t ep, uint32_t w, int32_t o, int len, F&& f) {
+  k32::TileIn t;
+  t.w = w;
+  t.o = o;
+  t.len = len;
+  t.soff = it.gs0 + es;
+  t.poff = it.gp0 + ep;
+  t.sgn = in.signs;
+  t.pay = in.payload;
+  t.fast = false;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t flags = 0;
+  for (int j = 0; j < 32; ++j) {
+    const k32::LaneBlock m = k32::lane_block(t, j);
+    if (m.len == 0) break;
+    const int64_t q = k32::decode_lane(t.sgn, t.pay, m.w, m.o, m.soff, m.poff, m.len, lane, &flags);
+    f(warp * 32 + j, lane, q, lane < m.len);
+  }
+  return flags;
+}
+
+// exact moments of this CTA's compute threads -> the carry-save counters
+// (same protocol as k32::finish_moments, over the 128 compute threads)
+__device__ __forceinline__ void finish_moments_compute(k32::Acc acc, void* ws, uint64_t* out) {
+  __shared__ k32::Acc s_acc[4];
+  __shared__ bool s_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int m = 16; m > 0; m >>= 1) acc.merge(k32::shfl_xor_acc(acc, m));
+  if (lane == 0) s_acc[warp] = acc;
+  e32::bar_sync_n(1, kCompute);
+  uint64_t* base = static_cast<uint64_t*>(ws);
+  uint64_t* done = base + 2;
+  uint64_t* cs = base + 8;
+  if (threadIdx.x == 0) {
+    k32::Acc t = s_acc[0];
+    for (int i = 1; i < 4; ++i) t.merge(s_acc[i]);
+    const unsigned __int128 su = static_cast<unsigned __int128>(t.s);
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t ch = static_cast<uint64_t>(su >> (32 * k)) & 0xffffffffull;
+      if (ch) atomicAdd(reinterpret_cast<unsigned long long*>(cs + k), ch);
+    }
+    for (int k = 0; k < 6; ++k) {
+      const uint64_t ch = (k < 4) ? static_cast<uint64_t>(t.q >> (32 * k)) & 0xffffffffull
+                                  : (t.q2 >> (32 * (k - 4))) & 0xffffffffull;
+      if (ch) atomicAdd(reinterpret_cast<unsigned long long*>(cs + 4 + k), ch);
+    }
+    __threadfence();
+    s_last = atom_add_acq_rel(done, 1) == gridDim.x - 1;
+    if (s_last) {
+      __threadfence();
+      uint64_t S[2] = {0, 0}, Q[4] = {0, 0, 0, 0};
+      for (int k = 0; k < 4; ++k) k32::add_shifted(S, 2, ld_relaxed(cs + k), 32 * k);
+      for (int k = 0; k < 6; ++k) k32::add_shifted(Q, 4, ld_relaxed(cs + 4 + k), 32 * k);
+      out[0] = S[0];
+      out[1] = S[1];
+      out[2] = Q[0];
+      out[3] = Q[1];
+      out[4] = Q[2];
+      for (int k = 0; k < 10; ++k) st_relaxed(cs + k, 0);
+      st_relaxed(done, 0);
+    }
+  }
+}
+
+struct MomentsSink {
+  uint64_t* out;
+  void* ws;
+};
+struct DecF32Sink {
+  float* out;
+  double d;
+  bool may_overflow;
+};
+
+template <class Sink>
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+
+// kMode 0: mean (S), 1: variance (S, Q), 2: decompress to float32
+template <int kMode>
+__global__ void __launch_bounds__(kDecThreads, 5)
+    decode_pipe_kernel(const __grid_constant__ CUtensorMap omap, StreamIn in, DecF32Sink fs,
+                       MomentsSink ms, int use_tma, uint32_t* err) {
+  extern __shared__ unsigned char smraw[];
+  const uint32_t a0 = smem_u32(smraw);
+  DecSmem<kMode>& S = *reinterpret_cast<DecSmem<kMode>*>(smraw + (((a0 + 1023u) & ~1023u) - a0));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint64_t ntiles = in.ntiles, nblocks = in.nblocks;
+  if (tid == kCompute) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&S.full[b], 1);
+      mbar_init(&S.empty[b], kCompute);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == kCompute / 32) {
+    // ============================ TMA warp ==============================
+    uint32_t i = 0;
+    for (uint64_t t = blockIdx.x;; t += gridDim.x, ++i) {
+      const int b = i & 1;
+      if (i >= 2) mbar_wait_parity(&S.empty[b], ((i >> 1) - 1) & 1u);
+      stage_tile(in, t, S.in[b], &S.full[b]);
+      if (t >= ntiles) break;
+    }
+    return;
+  }
+  // =========================== compute warps ===========================
+  uint32_t flags = 0;
+  k32::Acc acc;
+  acc.s = 0;
+  acc.q = 0;
+  acc.q2 = 0;
+  uint32_t i = 0;
+  for (;; ++i) {
+    const int b = i & 1;
+    mbar_wait_parity(&S.full[b], (i >> 1) & 1u);
+    const InTile& it = S.in[b];
+    const uint64_t cur = it.tile;
+    if (cur >= ntiles) break;
+    const uint64_t gb = cur * TB + tid;
+    const bool active = gb < nblocks;
+    const int len = !active ? 0 : (gb == nblocks - 1 ? static_cast<int>(in.tail_len) : K);
+    uint32_t w = it.w[tid];
+    const int32_t o = it.o[tid];
+    if (w > 64) {
+      flags |= HSZ_ERR_BAD_WIDTH;
+      w = 0;
+    }
+    const uint32_t isb = w ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
+    const uint32_t ipb = (static_cast<uint32_t>(len) * w + 7u) >> 3;
+    uint32_t itot;
+    const uint32_t iex = e32::cta_scan(isb | (ipb << 10), S.scan, &itot);
+    const uint32_t ies = iex & 1023u, iep = iex >> 10;
+    const bool fast = e32::bar_or_compute(!(it.staged && w <= static_cast<uint32_t>(kFastW) &&
+                                            o > -(1 << 29) && o < (1 << 29))) == false;
+    if (kMode == 2 && i > 0 && tid == 0) {
+      // the previous tile's TMA store has finished reading S.out
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    if (kMode == 2) e32::bar_sync_n(1, kCompute);
+    if (fast) {
+      int32_t q[K];
+      decode_block(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, o, len, q);
+      mbar_arrive(&S.empty[b]);          // staged bytes consumed
+      if (kMode == 2) {
+        // f32 values = RN32(RN64(2eps * bin)) (codec.py:107-115), into the
+        // swizzled 128-byte row of this block
+        float v[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          v[k] = __double2float_rn(__dmul_rn(fs.d, i32_to_double(q[k])));
+          if (fs.may_overflow && !isfinite(v[k])) flags |= HSZ_ERR_OUTPUT_NONFINITE;
+        }
+        unsigned char* row = S.out + tid * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(row + ((j ^ (tid & 7)) << 4)) =
+              make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      } else if (len > 0) {
+        // block sums: S_b = sum bin, Q_b = sum bin^2 with bin = o + P_i
+        int64_t sp = 0;
+        uint64_t sp2 = 0;
+        if (len == K) {
+          int32_t sp32 = 0;   // |sum P| < 32 * 2^29
+#pragma unroll
+          for (int k = 1; k < K; ++k) {
+            const int32_t P = q[k] - o;   // |P| < 2^29
+            sp32 += P;
+            if (kMode == 1) sp2 += static_cast<uint64_t>(static_cast<int64_t>(P) * P);
+          }
+          sp = sp32;
+        } else {
+#pragma unroll
+          for (int k = 1; k < K; ++k) {
+            const int32_t P = q[k] - o;
+            if (k < len) {
+              sp += P;
+              if (kMode == 1) sp2 += static_cast<uint64_t>(static_cast<int64_t>(P) * P);
+            }
+          }
+        }
+        const __int128 oo = o;
+        acc.s += oo * len + sp;
+        if (kMode == 1) {
+          const __int128 tot = oo * oo * len + 2 * oo * sp + static_cast<__int128>(sp2);
+          const unsigned __int128 nq = acc.q + static_cast<unsigned __int128>(tot);
+          acc.q2 += nq < acc.q ? 1u : 0u;
+          acc.q = nq;
+        }
+      }
+    } else {
+      // exact lane-per-element path, sections read in place
+      if (kMode == 2) {
+        flags |= exact_tile(in, it, ies, iep, w, o, len, [&](int lb, int ln, int64_t q, bool live) {
+          if (live) {
+            const float v = __double2float_rn(grid1(q, fs.d));
+            if (!isfinite(v)) flags |= HSZ_ERR_OUTPUT_NONFINITE;
+            fs.out[(cur * TB + lb) * K + ln] = v;
+          }
+        });
+      } else {
+        flags |= exact_tile(in, it, ies, iep, w, o, len, [&](int, int, int64_t q, bool live) {
+          if (live) acc.add(q, kMode == 1);
+        });
+      }
+      mbar_arrive(&S.empty[b]);
+    }
+    if (kMode == 2) {
+      // one TMA tensor store of the whole tile (the stream's partial last
+      // block and rows past the end are written by plain stores / clipped)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      e32::bar_sync_n(1, kCompute);
+      if (fast) {
+        const uint64_t full_rows = in.n / K;
+        const uint64_t row0 = cur * TB;
+        if (use_tma) {
+          if (tid == 0) {
+            tma_store_2d<DecF32Sink>(&omap, S.out, 0, static_cast<int>(row0));
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        } else {
+          for (uint32_t e = tid; e < TB * K; e += kCompute) {
+            const uint64_t g = row0 * K + e;
+            if (g < full_rows * K) fs.out[g] = *reinterpret_cast<const float*>(S.out + e32::swz_elem(e >> 5, e & 31u));
+          }
+        }
+        if ((in.n % K) != 0 && full_rows >= row0 && full_rows < row0 + TB && tid < static_cast<int>(in.n % K)) {
+          const uint32_t r = static_cast<uint32_t>(full_rows - row0);
+          fs.out[full_rows * K + tid] = *reinterpret_cast<const float*>(S.out + e32::swz_elem(r, tid));
+        }
+      }
+    }
+  }
+  if (kMode == 2 && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (kMode != 2) finish_moments_compute(acc, ms.ws, ms.out);
+  flags = __reduce_or_sync(kFull, flags);
+  if (lane == 0 && flags) atomicOr(err, flags);
+}
 
 }  // namespace d32
 }  // namespace hsz

@@ -21,12 +21,25 @@ from paper_2408_11971_b200 import ops as O  # noqa: E402
 from paper_2408_11971_b200 import workloads as W  # noqa: E402
 
 
+FLUSH = os.environ.get("HSZ_FLUSH", "read")
+
+
+def do_flush(flush):
+    """Evict L2 between timed launches.  "read" leaves clean lines (a write
+    flush leaves ~126 MB of dirty lines whose write-back the next kernel pays)."""
+    if FLUSH == "write":
+        flush.fill_(1)
+    elif FLUSH == "read":
+        flush.view(torch.int64).max()
+
+
 def device_times(fns, flush, reps):
     out = {}
     for name, fn in fns.items():
         ts = []
         for _ in range(reps + 2):
-            flush.fill_(1)
+            if FLUSH != "none":
+                do_flush(flush)
             torch.cuda._sleep(400_000)          # keep the GPU busy while the host enqueues
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
