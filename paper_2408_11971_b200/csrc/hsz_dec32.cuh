@@ -59,9 +59,20 @@ __device__ __forceinline__ void bulk_g2s_(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+// TMA warp (all 32 lanes): the tile-offset entries of tile t (lanes 0-3 hold
+// toff[2t + lane]); issued a tile ahead so their latency is hidden.
+__device__ __forceinline__ uint64_t prefetch_toff(const StreamIn& s, uint64_t t) {
+  const int lane = threadIdx.x & 31;
+  return (lane < 4 && t < s.ntiles) ? s.toff[2 * t + lane] : 0ull;
+}
+
 // TMA warp (all 32 lanes): stage tile t (or "no more tiles") into `it`,
-// completing one phase of `bar` (count 1: lane 0's arrive).
-__device__ __forceinline__ void stage_tile(const StreamIn& s, uint64_t t, InTile& it, uint64_t* bar) {
+// completing one phase of `bar` (count 1: lane 0's arrive).  `tv` = the
+// prefetched tile-offset entries.  Full tiles arrive by four bulk copies
+// (widths, outliers, sign bytes, payload bytes); the stream's last tile
+// loads its widths / outliers with plain loads.
+__device__ __forceinline__ void stage_tile(const StreamIn& s, uint64_t t, uint64_t tv, InTile& it,
+                                           uint64_t* bar) {
   const int lane = threadIdx.x & 31;
   if (t >= s.ntiles) {
     if (lane == 0) {
@@ -71,23 +82,24 @@ __device__ __forceinline__ void stage_tile(const StreamIn& s, uint64_t t, InTile
     __syncwarp();
     return;
   }
-  uint64_t v = 0;
-  if (lane < 4) v = s.toff[2 * t + lane];
-  const uint64_t s0 = __shfl_sync(kFull, v, 0), p0 = __shfl_sync(kFull, v, 1);
-  const uint64_t s1 = __shfl_sync(kFull, v, 2), p1 = __shfl_sync(kFull, v, 3);
-  // widths / outliers: 4 blocks per lane
+  const uint64_t s0 = __shfl_sync(kFull, tv, 0), p0 = __shfl_sync(kFull, tv, 1);
+  const uint64_t s1 = __shfl_sync(kFull, tv, 2), p1 = __shfl_sync(kFull, tv, 3);
+  const bool full = (t + 1) * TB <= s.nblocks &&
+                    ((reinterpret_cast<uintptr_t>(s.widths) | reinterpret_cast<uintptr_t>(s.outliers)) & 15u) == 0;
+  if (!full) {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint32_t lb = 4 * lane + j;
-    const uint64_t b = t * TB + lb;
-    uint8_t w = 0;
-    int32_t o = 0;
-    if (b < s.nblocks) {
-      w = s.widths[b];
-      o = s.outliers[b];
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t lb = 4 * lane + j;
+      const uint64_t b = t * TB + lb;
+      uint8_t w = 0;
+      int32_t o = 0;
+      if (b < s.nblocks) {
+        w = s.widths[b];
+        o = s.outliers[b];
+      }
+      it.w[lb] = w;
+      it.o[lb] = o;
     }
-    it.w[lb] = w;
-    it.o[lb] = o;
   }
   __syncwarp();
   if (lane == 0) {
@@ -102,11 +114,16 @@ __device__ __forceinline__ void stage_tile(const StreamIn& s, uint64_t t, InTile
     it.soff = static_cast<uint32_t>(s0 - s_lo);
     it.poff = static_cast<uint32_t>(p0 - p_lo);
     it.staged = staged ? 1u : 0u;
+    const uint32_t bytes = (full ? TB * 5u : 0u) + (staged ? sbytes + pbytes : 0u);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (staged && (sbytes | pbytes)) {
-      mbar_arrive_expect_tx(bar, sbytes + pbytes);
-      if (sbytes) bulk_g2s_(it.sgn, s.signs + s_lo, sbytes, bar);
-      if (pbytes) bulk_g2s_(it.pay, s.payload + p_lo, pbytes, bar);
+    if (bytes) {
+      mbar_arrive_expect_tx(bar, bytes);
+      if (full) {
+        bulk_g2s_(it.w, s.widths + t * TB, TB, bar);
+        bulk_g2s_(it.o, s.outliers + t * TB, TB * 4, bar);
+      }
+      if (staged && sbytes) bulk_g2s_(it.sgn, s.signs + s_lo, sbytes, bar);
+      if (staged && pbytes) bulk_g2s_(it.pay, s.payload + p_lo, pbytes, bar);
     } else {
       mbar_arrive(bar);
     }
@@ -285,13 +302,15 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
     }
     t = __shfl_sync(kFull, t, 0);
     ahead = __shfl_sync(kFull, ahead, 0);
-    stage_tile(in, t, S.in, &S.bar);
+    stage_tile(in, t, prefetch_toff(in, t), S.in, &S.bar);
+    uint64_t tv = prefetch_toff(in, ahead);
     for (uint32_t k = 0; t < ntiles; ++k) {
-      mbar_wait_parity(&S.in_empty, k & 1u);
       const uint64_t nx = ahead;
       if (lane == 0 && nx < ntiles) ahead = draw();
       ahead = __shfl_sync(kFull, ahead, 0);
-      stage_tile(in, nx, S.in, &S.bar);
+      mbar_wait_parity(&S.in_empty, k & 1u);
+      stage_tile(in, nx, tv, S.in, &S.bar);
+      tv = prefetch_toff(in, ahead);
       t = nx;
     }
     return;
@@ -552,11 +571,14 @@ __global__ void __launch_bounds__(kDecThreads, 5)
   if (warp == kCompute / 32) {
     // ============================ TMA warp ==============================
     uint32_t i = 0;
+    uint64_t tv = prefetch_toff(in, blockIdx.x);
     for (uint64_t t = blockIdx.x;; t += gridDim.x, ++i) {
       const int b = i & 1;
+      const uint64_t tvn = prefetch_toff(in, t + gridDim.x);   // consumed next iteration
       if (i >= 2) mbar_wait_parity(&S.empty[b], ((i >> 1) - 1) & 1u);
-      stage_tile(in, t, S.in[b], &S.full[b]);
+      stage_tile(in, t, tv, S.in[b], &S.full[b]);
       if (t >= ntiles) break;
+      tv = tvn;
     }
     return;
   }
