@@ -44,6 +44,17 @@ OPS = ("compress", "negate", "scalar_add", "scalar_mul", "mean", "variance", "de
 METRIC = "uncompressed GB/s per op (compress/decompress/homomorphic) & % HBM roofline"
 
 
+def _traffic(op):
+    """DRAM bytes per launch of `op`'s kernel (dram__bytes_read.sum +
+    dram__bytes_write.sum) from the committed ncu capture, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            v = json.load(f)["config2"].get(op)
+        return int(v) if v is not None else None
+    except Exception:
+        return None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -176,8 +187,10 @@ class Chain:
         out = H.decompress(z)                                  # K3
         mark(7)
         if host_out:
+            from paper_2408_11971_b200.device import download
+
             hz = z.to_host()
-            vals = out.values.cpu()
+            vals = download([out.values])[0]
             return hz, vals, mean, var
         return z, out, mean, var
 
@@ -251,6 +264,8 @@ def run_b200(args):
     abytes = _algorithmic_bytes(H, cfg, x)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
+    sampler = ClockSampler(local)
+    sampler.start()                       # samples cover warm-up, timed steps and kernel timing
     for _ in range(max(args.warmup, 3)):
         chain.run(x)
     torch.cuda.synchronize()
@@ -258,14 +273,12 @@ def run_b200(args):
     nev = 8
     per_step = []
     per_op = {op: [] for op in OPS}
-    sampler = ClockSampler(local)
-    sampler.start()
     if coll is not None:
         coll.barrier()
     torch.cuda.synchronize()
     wall0 = time.perf_counter()
     for _ in range(args.steps):
-        flush.fill_(1)                                  # evict L2 (excluded from timing)
+        _flush(flush)                                   # evict L2 (excluded from timing)
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
         chain.run(x, evs)
         torch.cuda.synchronize()
@@ -276,7 +289,6 @@ def run_b200(args):
     if coll is not None:
         coll.barrier()
     wall = time.perf_counter() - wall0
-    clocks = sampler.stop()
 
     step_ms = sum(per_step) / len(per_step)
     if coll is not None:
@@ -285,7 +297,8 @@ def run_b200(args):
     value = len(OPS) * 4.0 * n * world / (step_ms * 1e-3) / 1e9
 
     # ---- per-kernel timing (each op alone, L2 flushed first) for the roofline
-    kern = _kernel_times(H, cfg, x, flush, reps=max(5, min(args.steps, 20)))
+    kern = _kernel_times(H, cfg, x, flush, reps=max(10, min(args.steps, 30)))
+    clocks = sampler.stop()
     peak, peak_kind = _peaks()
     ops_json = {}
     for op in OPS:
@@ -329,7 +342,7 @@ def run_b200(args):
             "compression_ratio": round(abytes["_ratio"], 3),
             "stream_bytes": int(abytes["_C"]),
             "value_definition": "7 ops x 4N bytes (all ranks) / device step time",
-            "l2": "512 MB write between steps (field 100 MB < 126 MB L2), excluded from timing",
+            "l2": "512 MB read between steps (field 100 MB < 126 MB L2), excluded from timing",
             "parallelism": f"{world} rank(s), contiguous block ranges, NCCL C1/C2/C3" if world > 1
             else "1 GPU",
             "wall_s_timed_region": round(wall, 3),
@@ -337,7 +350,9 @@ def run_b200(args):
         "ops": ops_json,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None},
+                     "frac": round(achieved / peak, 4),
+                     "traffic": _traffic(dom) if args.config == 2 else None,
+                     "algorithmic_bytes": int(abytes[dom])},
         "e2e": e2e,
         "gpu_launches": 8 * args.steps,
         "clocks": clocks,
@@ -353,8 +368,18 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def _flush(flush):
+    """Evict L2 with a 512 MB read (clean lines: no write-back charged to the
+    next kernel)."""
+    flush.view(__import__("torch").int64).max()
+
+
 def _kernel_times(H, cfg, x, flush, reps=10):
-    """Median device time of each op launched alone after an L2 flush."""
+    """Mean device time (ms) of each op launched alone after an L2 flush.  A
+    ~0.2 ms spin kernel is queued first so the host enqueues the op while the
+    GPU is busy: the event interval holds device time only, not Python launch
+    latency.  (Events tick in 2.048 us steps on this driver; the mean over
+    `reps` launches resolves below that.)"""
     import torch
     from paper_2408_11971_b200 import ops as O
 
@@ -364,8 +389,14 @@ def _kernel_times(H, cfg, x, flush, reps=10):
     s = H.compress(raw, p)
     z0 = H.scalar_add(H.negate(s), cfg["sadd"])
     z = H.scalar_mul(z0, cfg["smul"])
+    ctx = s.ctx
+    wsp, wsb = ctx.workspace(1, 1)
+    mm = ctx.empty(2, torch.float64)
+    from paper_2408_11971_b200 import _native as N
+    from paper_2408_11971_b200.device import ptr
     fns = {
-        "minmax": lambda: H.RawArray(x, cfg["dims"], "f32", _validated=True)._validate(),
+        "minmax": lambda: N.check(ctx.lib.hsz_minmax(ptr(x), N.HSZ_F32, x.numel(), ptr(mm), ctx.err_ptr,
+                                                     wsp, wsb, ctx.handle), "hsz_minmax"),
         "compress": lambda: H.compress(raw, p),
         "negate": lambda: H.negate(s),
         "scalar_add": lambda: H.scalar_add(s, cfg["sadd"]),
@@ -377,15 +408,16 @@ def _kernel_times(H, cfg, x, flush, reps=10):
     out = {}
     for name, fn in fns.items():
         ts = []
-        for _ in range(reps + 1):
-            flush.fill_(1)
+        for _ in range(reps + 2):
+            _flush(flush)
+            torch.cuda._sleep(400_000)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             fn()
             b.record()
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
-        out[name] = statistics.median(ts[1:])
+        out[name] = sum(ts[2:]) / len(ts[2:])
     z.check()
     return out
 
@@ -399,14 +431,14 @@ def _e2e(H, chain, x, flush, steps, coll):
     ts = []
     bo = 0
     for _ in range(steps + 1):
-        flush.fill_(1)
+        _flush(flush)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         xd = host.to(x.device, non_blocking=True)
         hz, vals, mean, var = chain.run(xd, host_out=True)
         torch.cuda.synchronize()
         ts.append(time.perf_counter() - t0)
-        bo = len(hz.sign_planes) + len(hz.payload) + 5 * hz.params.block_count + vals.numel() * 4 + 16
+        bo = len(hz.sign_planes) + len(hz.payload) + 5 * hz.params.block_count + vals.size * 4 + 16
     t = statistics.median(ts[1:])
     if coll is not None:
         t = coll.max_over_ranks(t)

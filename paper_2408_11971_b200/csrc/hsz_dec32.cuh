@@ -133,45 +133,58 @@ __device__ __forceinline__ void stage_tile(const StreamIn& s, uint64_t t, uint64
 
 // Register decode of this thread's block (w <= kFastW, |o| < 2^29): bins as
 // int32 (|bin| < 2^30).  kFull: a full block (len == 32, no tail checks);
-// otherwise elements past `len` replicate the last live bin.
-template <bool kFull>
+// otherwise elements past `len` replicate the last live bin.  Fields are read
+// G at a time (G * w <= 32): one window refill check per G fields.
+template <bool kFull, int G>
 __device__ __forceinline__ void decode_block_t(const unsigned char* sgn, const unsigned char* pay,
                                                uint32_t w, int32_t o, int len, int32_t (&q)[K]) {
-  q[0] = o;
-  if (w == 0) {
-#pragma unroll
-    for (int i = 1; i < K; ++i) q[i] = o;
-    return;
-  }
   const uint32_t sw = bswap32(*reinterpret_cast<const uint32_t*>(sgn));
   const uint32_t* pw = reinterpret_cast<const uint32_t*>(pay);
   const uint32_t mask = (1u << w) - 1u;
-  uint64_t win = bswap32(pw[0]);
-  int nb = 32 - static_cast<int>(w);   // bits left after slot 0's (zero) field
-  int wi = 1;
+  const int wg = G * static_cast<int>(w);
+  uint64_t win = 0;
+  int nb = 0;   // valid bits at the bottom of win
+  int wi = 0;
   int32_t P = o;
+  q[0] = o;
 #pragma unroll
-  for (int i = 1; i < K; ++i) {
-    if (nb < static_cast<int>(w)) {
+  for (int c = 0; c < K / G; ++c) {
+    if (nb < wg) {
       win = (win << 32) | bswap32(pw[wi++]);
       nb += 32;
     }
-    nb -= static_cast<int>(w);
-    const int32_t mag = static_cast<int32_t>(static_cast<uint32_t>(win >> nb) & mask);
-    const int32_t neg = static_cast<int32_t>(sw << i) >> 31;   // element i's sign bit
-    int32_t d = (mag ^ neg) - neg;
-    if (!kFull) d = (i < len) ? d : 0;
-    P += d;
-    q[i] = P;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int i = c * G + g;
+      nb -= static_cast<int>(w);
+      if (i == 0) continue;   // slot 0: the outlier's zero field
+      const int32_t mag = static_cast<int32_t>(static_cast<uint32_t>(win >> nb) & mask);
+      const int32_t neg = static_cast<int32_t>(sw << i) >> 31;   // element i's sign bit
+      int32_t d = (mag ^ neg) - neg;
+      if (!kFull) d = (i < len) ? d : 0;
+      P += d;
+      q[i] = P;
+    }
   }
 }
 
+// all 32 lanes of the warp call this (the field grouping is warp-uniform)
 __device__ __forceinline__ void decode_block(const unsigned char* sgn, const unsigned char* pay,
                                              uint32_t w, int32_t o, int len, int32_t (&q)[K]) {
-  if (len == K) {
-    decode_block_t<true>(sgn, pay, w, o, len, q);
+  const uint32_t wmax = __reduce_max_sync(kFull, w);
+  if (w == 0) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) q[i] = o;
+    return;
+  }
+  if (len != K) {
+    decode_block_t<false, 1>(sgn, pay, w, o, len, q);
+  } else if (wmax <= 8) {
+    decode_block_t<true, 4>(sgn, pay, w, o, len, q);
+  } else if (wmax <= 16) {
+    decode_block_t<true, 2>(sgn, pay, w, o, len, q);
   } else {
-    decode_block_t<false>(sgn, pay, w, o, len, q);
+    decode_block_t<true, 1>(sgn, pay, w, o, len, q);
   }
 }
 
@@ -366,7 +379,8 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
     S.bes[tid] = ies;
     S.bep[tid] = iep;
     const bool fast_in = S.in.staged && w <= static_cast<uint32_t>(kFastW) && o > -(1 << 29) && o < (1 << 29);
-    bool exact = !fast_in || !sp.small_rs;
+    // CTA-uniform: the register decode is warp-collective (decode_block)
+    bool exact = e32::bar_or_compute(!fast_in || !sp.small_rs);
     uint32_t qb[K];
     if (!exact) {
       int32_t q[K];
