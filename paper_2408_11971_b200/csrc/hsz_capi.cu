@@ -126,6 +126,145 @@ __global__ void __launch_bounds__(kThreads) minmax_kernel(const T* x, uint64_t n
   st_relaxed(done, 0);
 }
 
+// ---- K0 for float32: 8 independent 16-byte loads in flight per thread -------
+constexpr int kMmThreads = 512;
+__global__ void __launch_bounds__(kMmThreads) minmax_f32_kernel(const float* __restrict__ x, uint64_t n,
+                                                                double* out, uint32_t* err, void* ws) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t nv = n / 4;
+  const float4* xv = reinterpret_cast<const float4*>(x);
+  float flo = INFINITY, fhi = -INFINITY;
+  bool bad = false;
+  uint64_t i = tid;
+  for (; i + 7 * stride < nv; i += 8 * stride) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcs(xv + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      bad |= !isfinite(v[u].x) | !isfinite(v[u].y) | !isfinite(v[u].z) | !isfinite(v[u].w);
+      flo = fminf(fminf(flo, v[u].x), fminf(fminf(v[u].y, v[u].z), v[u].w));
+      fhi = fmaxf(fmaxf(fhi, v[u].x), fmaxf(fmaxf(v[u].y, v[u].z), v[u].w));
+    }
+  }
+  for (; i < nv; i += stride) {
+    const float4 v = __ldcs(xv + i);
+    bad |= !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
+    flo = fminf(fminf(flo, v.x), fminf(fminf(v.y, v.z), v.w));
+    fhi = fmaxf(fmaxf(fhi, v.x), fmaxf(fmaxf(v.y, v.z), v.w));
+  }
+  for (uint64_t j = nv * 4 + tid; j < n; j += stride) {
+    const float v = x[j];
+    bad |= !isfinite(v);
+    flo = fminf(flo, v);
+    fhi = fmaxf(fhi, v);
+  }
+  double lo = flo, hi = fhi;
+  for (int m = 16; m > 0; m >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(kFull, lo, m));
+    hi = fmax(hi, __shfl_xor_sync(kFull, hi, m));
+  }
+  if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(err, HSZ_ERR_NONFINITE);
+  __shared__ double s_lo[kMmThreads / 32], s_hi[kMmThreads / 32];
+  __shared__ bool s_last;
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_lo[warp] = lo;
+    s_hi[warp] = hi;
+  }
+  __syncthreads();
+  uint64_t* base = static_cast<uint64_t*>(ws);
+  uint64_t* done = base + 3;
+  double* part = reinterpret_cast<double*>(base + kWsMinmaxOff);
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < kMmThreads / 32; ++k) {
+      lo = fmin(lo, s_lo[k]);
+      hi = fmax(hi, s_hi[k]);
+    }
+    part[2 * blockIdx.x] = lo;
+    part[2 * blockIdx.x + 1] = hi;
+    __threadfence();
+    s_last = atom_add_acq_rel(done, 1) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  lo = INFINITY;
+  hi = -INFINITY;
+  for (unsigned k = threadIdx.x; k < gridDim.x; k += blockDim.x) {
+    lo = fmin(lo, __longlong_as_double(ld_relaxed(reinterpret_cast<uint64_t*>(part + 2 * k))));
+    hi = fmax(hi, __longlong_as_double(ld_relaxed(reinterpret_cast<uint64_t*>(part + 2 * k + 1))));
+  }
+  for (int m = 16; m > 0; m >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(kFull, lo, m));
+    hi = fmax(hi, __shfl_xor_sync(kFull, hi, m));
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    s_lo[warp] = lo;
+    s_hi[warp] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int k = 1; k < kMmThreads / 32; ++k) {
+    lo = fmin(lo, s_lo[k]);
+    hi = fmax(hi, s_hi[k]);
+  }
+  out[0] = lo;
+  out[1] = hi;
+  st_relaxed(done, 0);
+}
+
+// ---- K4 for block_len 32: every stored sign byte flips (full blocks have 4
+// sign bytes, all bits live); only the partial tail block's last byte keeps
+// its zero padding.  Sign chunks and outlier chunks share one index space;
+// each thread issues up to 4 independent 16-byte loads.
+__global__ void __launch_bounds__(kThreads) negate32_kernel(
+    const uint8_t* __restrict__ widths, const int32_t* __restrict__ oin, int32_t* __restrict__ oout,
+    const uint8_t* __restrict__ sin, uint8_t* __restrict__ sout, const uint64_t* __restrict__ toff,
+    uint64_t ntiles, uint64_t n, uint64_t nblocks, uint64_t sign_chunks_max, uint32_t* err) {
+  const uint64_t S = __ldg(toff + 2 * ntiles);
+  const uint64_t nsc = (S + 15) / 16;                  // sign chunks in use
+  const uint64_t noc = nblocks / 4;                    // full outlier chunks
+  const uint32_t r = static_cast<uint32_t>(n % 32);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint32_t flags = 0;
+  // outliers first (independent of S)
+  for (uint64_t c = tid; c < noc; c += stride) {
+    int4 v = reinterpret_cast<const int4*>(oin)[c];
+    flags |= (v.x == INT32_MIN) | (v.y == INT32_MIN) | (v.z == INT32_MIN) | (v.w == INT32_MIN)
+                 ? HSZ_ERR_OUTLIER_OVERFLOW : 0u;
+    v.x = -v.x;
+    v.y = -v.y;
+    v.z = -v.z;
+    v.w = -v.w;
+    reinterpret_cast<int4*>(oout)[c] = v;
+  }
+  for (uint64_t b = noc * 4 + tid; b < nblocks; b += stride) {
+    const int32_t v = oin[b];
+    if (v == INT32_MIN) flags |= HSZ_ERR_OUTLIER_OVERFLOW;
+    oout[b] = -v;
+  }
+  (void)sign_chunks_max;
+  for (uint64_t c = tid; c < nsc; c += stride) {
+    uint4 v = reinterpret_cast<const uint4*>(sin)[c];
+    v.x = ~v.x;
+    v.y = ~v.y;
+    v.z = ~v.z;
+    v.w = ~v.w;
+    if (c == nsc - 1 && (r & 7u) != 0 && widths[nblocks - 1] > 0) {
+      // the tail block's last sign byte: its padding bits stay zero
+      const uint32_t j = static_cast<uint32_t>((S - 1) & 15u);
+      const uint32_t tmask = (0xFFu << (8 - (r & 7u))) & 0xFFu;
+      reinterpret_cast<uint32_t*>(&v)[j >> 2] ^= (0xFFu ^ tmask) << (8 * (j & 3u));
+    }
+    reinterpret_cast<uint4*>(sout)[c] = v;
+  }
+  if (flags) atomicOr(err, flags);
+}
+
 // ---- K4: negate (ops.py:88-109) --------------------------------------------
 // Every stored sign bit flips; padding bits of a block's last sign byte stay
 // 0.  Full non-constant blocks all contribute sk = ceil(k/8) bytes, so the
@@ -180,30 +319,37 @@ __global__ void __launch_bounds__(kThreads) negate_kernel(
 }
 
 // ---- K5: scalar add (ops.py:112-118) -----------------------------------------
+__device__ __forceinline__ int32_t sadd1(int32_t o, int64_t rs, uint32_t& flags) {
+  // numpy int64 addition wraps; any wrapped or true sum outside int32 is
+  // rejected by the int32 guard, so the exact test is equivalent
+  const __int128 v = static_cast<__int128>(o) + rs;
+  if (v < INT32_MIN || v > INT32_MAX) flags |= HSZ_ERR_OUTLIER_OVERFLOW;
+  return static_cast<int32_t>(static_cast<int64_t>(v));
+}
+
 __global__ void __launch_bounds__(kThreads) sadd_kernel(const int32_t* oin, int32_t* oout,
                                                         uint64_t nblocks, int64_t rs,
                                                         uint32_t* err) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   uint32_t flags = 0;
-  auto one = [&](int32_t o) -> int32_t {
-    // numpy int64 addition wraps; any wrapped or true sum outside int32 is
-    // rejected by the int32 guard, so the exact test is equivalent
-    const __int128 v = static_cast<__int128>(o) + rs;
-    if (v < INT32_MIN || v > INT32_MAX) flags |= HSZ_ERR_OUTLIER_OVERFLOW;
-    return static_cast<int32_t>(static_cast<int64_t>(v));
-  };
   const bool vec = ((reinterpret_cast<uintptr_t>(oin) | reinterpret_cast<uintptr_t>(oout)) & 15u) == 0;
   const uint64_t nv = vec ? nblocks / 4 : 0;
-  for (uint64_t i = tid; i < nv; i += stride) {
-    int4 v = reinterpret_cast<const int4*>(oin)[i];
-    v.x = one(v.x);
-    v.y = one(v.y);
-    v.z = one(v.z);
-    v.w = one(v.w);
-    reinterpret_cast<int4*>(oout)[i] = v;
+  uint64_t i = tid;
+  for (; i + stride < nv; i += 2 * stride) {   // two independent 16-byte loads in flight
+    int4 a = reinterpret_cast<const int4*>(oin)[i];
+    int4 b = reinterpret_cast<const int4*>(oin)[i + stride];
+    a = make_int4(sadd1(a.x, rs, flags), sadd1(a.y, rs, flags), sadd1(a.z, rs, flags), sadd1(a.w, rs, flags));
+    b = make_int4(sadd1(b.x, rs, flags), sadd1(b.y, rs, flags), sadd1(b.z, rs, flags), sadd1(b.w, rs, flags));
+    reinterpret_cast<int4*>(oout)[i] = a;
+    reinterpret_cast<int4*>(oout)[i + stride] = b;
   }
-  for (uint64_t i = nv * 4 + tid; i < nblocks; i += stride) oout[i] = one(oin[i]);
+  for (; i < nv; i += stride) {
+    int4 a = reinterpret_cast<const int4*>(oin)[i];
+    a = make_int4(sadd1(a.x, rs, flags), sadd1(a.y, rs, flags), sadd1(a.z, rs, flags), sadd1(a.w, rs, flags));
+    reinterpret_cast<int4*>(oout)[i] = a;
+  }
+  for (uint64_t j = nv * 4 + tid; j < nblocks; j += stride) oout[j] = sadd1(oin[j], rs, flags);
   if (flags) atomicOr(err, flags);
 }
 
@@ -535,7 +681,10 @@ int hsz_minmax(const void* x, int dtype, uint64_t n, double* minmax, uint32_t* e
   if (ws_bytes < 8 * kWsFlagsOff) return HSZ_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const unsigned g = static_cast<unsigned>(grid_for(n, dtype == HSZ_F32 ? 16 : 8, ops::kThreads, ops::kMinmaxCtas));
-  if (dtype == HSZ_F32)
+  if (dtype == HSZ_F32 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0) {
+    const unsigned g2 = static_cast<unsigned>(grid_for(n, 32, ops::kMmThreads, ops::kMinmaxCtas));
+    ops::minmax_f32_kernel<<<g2, ops::kMmThreads, 0, st>>>(static_cast<const float*>(x), n, minmax, err, ws);
+  } else if (dtype == HSZ_F32)
     ops::minmax_kernel<float><<<g, ops::kThreads, 0, st>>>(static_cast<const float*>(x), n, minmax, err, ws);
   else if (dtype == HSZ_F64)
     ops::minmax_kernel<double><<<g, ops::kThreads, 0, st>>>(static_cast<const double*>(x), n, minmax, err, ws);
@@ -686,6 +835,15 @@ int hsz_negate(const uint8_t* widths, const int32_t* oin, int32_t* oout, const u
   const uint64_t nb = ceil_div(n, k);
   const uint64_t nt = ceil_div(nb, kTileBlocks);
   const uint64_t sign_bound = hsz_sign_bound(n, k);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(oin) | reinterpret_cast<uintptr_t>(oout) |
+                         reinterpret_cast<uintptr_t>(sin) | reinterpret_cast<uintptr_t>(sout)) & 15u) == 0;
+  if (k == 32 && aligned) {
+    const uint64_t items = nb / 4 + sign_bound / 16;
+    const unsigned g = static_cast<unsigned>(grid_for(items, 2, ops::kThreads, 148 * 32));
+    ops::negate32_kernel<<<g, ops::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        widths, oin, oout, sin, sout, toff, nt, n, nb, sign_bound / 16, err);
+    return launch_status();
+  }
   const uint64_t items = (sign_bound / 16 > nb) ? sign_bound / 16 : nb;
   const unsigned g = static_cast<unsigned>(grid_for(items, 2, ops::kThreads, 148 * 16));
   ops::negate_kernel<<<g, ops::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
