@@ -94,6 +94,25 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
       : "memory");
 }
 
+// wait for a phase without hogging issue slots (service warps: their waits
+// are long and latency-tolerant, the compute warps of the SM want the slots)
+__device__ __forceinline__ void mbar_wait_parity_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  unsigned ns = 64;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(ns);
+    ns = ns < 512 ? ns * 2 : 512;
+  }
+}
+
 // global -> shared bulk copy; dst/src 16-byte aligned, bytes % 16 == 0
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {

@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
       const uint64_t nx = ahead;
       if (lane == 0 && nx < ntiles) ahead = draw();
       ahead = __shfl_sync(kFull, ahead, 0);
-      mbar_wait_parity(&S.in_empty, k & 1u);
+      mbar_wait_parity_sleep(&S.in_empty, k & 1u);
       stage_tile(in, nx, tv, S.in, &S.bar);
       tv = prefetch_toff(in, ahead);
       t = nx;
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
     // =========================== placement warp ===========================
     for (uint32_t kk = 0;; ++kk) {
       const int b = kk & 1;
-      mbar_wait_parity(&S.st_full[b], (kk >> 1) & 1u);
+      mbar_wait_parity_sleep(&S.st_full[b], (kk >> 1) & 1u);
       const uint32_t pts = S.agg_ts[b], ptp = S.agg_tp[b];
       if (pts == e32::kDone) break;
       if (pts != e32::kSelfPlaced) {
@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(kDecThreads, 5)
     for (uint64_t t = blockIdx.x;; t += gridDim.x, ++i) {
       const int b = i & 1;
       const uint64_t tvn = prefetch_toff(in, t + gridDim.x);   // consumed next iteration
-      if (i >= 2) mbar_wait_parity(&S.empty[b], ((i >> 1) - 1) & 1u);
+      if (i >= 2) mbar_wait_parity_sleep(&S.empty[b], ((i >> 1) - 1) & 1u);
       stage_tile(in, t, tv, S.in[b], &S.full[b]);
       if (t >= ntiles) break;
       tv = tvn;

@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
       issue(t);
       if (t < ntiles) ahead = draw(epoch);
       for (uint32_t k = 0; t < ntiles; ++k) {
-        mbar_wait_parity(&S.in_empty, k & 1u);   // S.in holds no unread data
+        mbar_wait_parity_sleep(&S.in_empty, k & 1u);   // S.in holds no unread data
         const uint64_t nx = ahead;
         issue(nx);
         if (nx < ntiles) ahead = draw(epoch);
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
     // back) | copy it out of pk[b] | arrive st_empty[b]
     for (uint32_t kk = 0;; ++kk) {
       const int b = kk & 1;
-      mbar_wait_parity(&S.st_full[b], (kk >> 1) & 1u);
+      mbar_wait_parity_sleep(&S.st_full[b], (kk >> 1) & 1u);
       const uint32_t pts = S.agg_ts[b], ptp = S.agg_tp[b];
       if (pts == kDone) break;
       if (pts != kSelfPlaced) {
