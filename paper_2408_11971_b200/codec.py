@@ -124,9 +124,8 @@ class RawArray:
         n = x.numel()
         N.check(lib.hsz_minmax(ptr(x), DTYPE_CODE[self.dtype], n, ptr(out), ctx.err_ptr, wsp,
                                wsb, ctx.handle), "hsz_minmax")
-        flags = ctx.read_flags()
-        raise_for_flags(flags, "RawArray")
-        lo, hi = (float(v) for v in out.cpu().numpy())
+        (mm,) = ctx.fetch_checked([out], "RawArray")
+        lo, hi = float(mm[0]), float(mm[1])
         self._range = (lo, hi)
 
     def value_range(self):

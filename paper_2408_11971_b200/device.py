@@ -108,6 +108,17 @@ class Context:
     def check(self, what: str = "") -> None:
         raise_for_flags(self.read_flags(), what)
 
+    def fetch_checked(self, tensors, what: str = ""):
+        """Download `tensors` together with the sticky error word in ONE
+        synchronize; raise the reference's exception for a set error word."""
+        host = download(list(tensors) + [self.err], self)
+        flags = int(host[-1][0])
+        if flags:
+            self.err.zero_()
+            self.stream.synchronize()
+            raise_for_flags(flags, what)
+        return host[:-1]
+
     def empty(self, n, dtype):
         t = torch()
         return t.empty(int(n), dtype=dtype, device=self.device)
@@ -188,9 +199,9 @@ class DeviceStream:
     def totals(self):
         """(sign bytes, payload bytes) -- synchronizes."""
         if self._totals is None:
-            self.ctx.check()
             T = self.ntiles
-            tt = self.toff[2 * T:2 * T + 2].cpu().numpy().view(np.uint64)
+            (tt,) = self.ctx.fetch_checked([self.toff[2 * T:2 * T + 2]])
+            tt = tt.view(np.uint64)
             self._totals = (int(tt[0]), int(tt[1]))
         return self._totals
 
@@ -286,6 +297,24 @@ def download(tensors, ctx: Context = None):
                 t.float64: np.float64}[dt]
         out.append(a.view(npdt))
     return out
+
+
+def download_into(tensors, arena, ctx: Context = None):
+    """Copy device tensors into a caller-owned pinned host arena (uint8 CPU
+    tensor): one async copy each, one synchronize.  Returns numpy views into
+    the arena (valid until the arena is reused)."""
+    t = torch()
+    off = 0
+    views = []
+    for x in tensors:
+        nb = int(x.numel()) * x.element_size()
+        if nb:
+            arena[off:off + nb].copy_(x.reshape(-1).view(t.uint8), non_blocking=True)
+        views.append((off, nb))
+        off += (nb + 15) & ~15
+    (ctx.stream if ctx is not None else t.cuda.current_stream()).synchronize()
+    host = arena.numpy()
+    return [host[o:o + nb] for o, nb in views]
 
 
 def new_stream_buffers(ctx: Context, params: QuantParams, payload_cap: int = None):

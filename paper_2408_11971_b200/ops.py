@@ -187,8 +187,8 @@ def exact_moments(c, want_sq: bool = True):
     """Exact (sum(bins), sum(bins^2)) of a stream (ops.py:313-357)."""
     ds = _as_device_stream(c)
     out = moments_device(ds, want_sq)
-    ds.ctx.check("moments")
-    return unpack_moments(out.cpu().numpy())
+    (limbs,) = ds.ctx.fetch_checked([out], "moments")
+    return unpack_moments(limbs)
 
 
 def mean_from(S: int, n: int, eps: float) -> float:
