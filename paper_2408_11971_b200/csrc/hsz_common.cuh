@@ -88,29 +88,22 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
       "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
 }
 
-// wait for a phase without hogging issue slots (service warps: their waits
-// are long and latency-tolerant, the compute warps of the SM want the slots)
+// wait for a phase without hogging issue slots: try_wait with a suspend-time
+// hint parks the warp until the phase completes (or the hint elapses)
 __device__ __forceinline__ void mbar_wait_parity_sleep(uint64_t* bar, uint32_t parity) {
-  uint32_t done;
-  unsigned ns = 64;
-  while (true) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (done) return;
-    __nanosleep(ns);
-    ns = ns < 512 ? ns * 2 : 512;
-  }
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
+      "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
 
 // global -> shared bulk copy; dst/src 16-byte aligned, bytes % 16 == 0

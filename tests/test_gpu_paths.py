@@ -1,0 +1,161 @@
+"""GPU parity of the less-travelled paths of the block_len-32 kernels, each
+checked byte-exactly against the CPU oracle:
+
+* compress: TMA tensor loads vs plain loads (misaligned input), the stream's
+  partial last block on the TMA path, fields whose bins reach 2^30 (the exact
+  warp-per-block tile path) next to ordinary tiles, elements inside the
+  float32 certificate margin (exact float64 fallback per element);
+* decode pipeline (decompress / mean / variance) and scalar_mul: tiles wider
+  than the register decode (widths > 24), tiles whose payload exceeds the
+  staging buffer (read in place), outliers beyond 2^29, scalars beyond 2^23
+  and products beyond 2^30 (exact fallback), overflow error classes.
+"""
+
+import numpy as np
+import pytest
+
+import hoszp_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def H():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2408_11971_b200 as mod
+
+    return mod
+
+
+def _check_stream(H, s, ref):
+    assert H.serialize(s) == O.serialize(ref)
+
+
+def _full_check(H, x, eps, dims):
+    p = H.QuantParams(eps, dims, 32, "f32")
+    s = H.compress(H.RawArray(x, dims, "f32"), p)
+    ref = O.compress(x, eps, dims, 32, "f32")
+    _check_stream(H, s, ref)
+    assert H.decompress(s).values.tobytes() == O.decompress(ref).tobytes()
+    S, Q = O.moments(ref)
+    assert H.mean(s) == O.mean_from(S, x.size, eps)
+    assert H.variance(s) == O.variance_from(S, Q, x.size, eps)
+    return s, ref
+
+
+@pytest.mark.parametrize("n", [4096 * 3, 4096 * 3 + 7, 4096 * 40 + 31, 128 * 32 + 1, 5000])
+def test_compress_tma_and_tail(H, n):
+    rng = np.random.default_rng(n)
+    x = np.cumsum(rng.normal(0, 0.3, n)).astype(np.float32)
+    _full_check(H, x, 0.01, (n,))
+
+
+def test_compress_misaligned_input_plain_loads(H):
+    import torch
+
+    n = 4096 * 8 + 5
+    rng = np.random.default_rng(7)
+    x = np.cumsum(rng.normal(0, 0.3, n + 1)).astype(np.float32)
+    xd = torch.from_numpy(x).cuda()[1:]          # 4-byte offset: no TMA tensor map
+    assert xd.data_ptr() % 16 != 0
+    p = H.QuantParams(0.01, (n,), 32, "f32")
+    s = H.compress(H.RawArray(xd, (n,), "f32"), p)
+    ref = O.compress(x[1:], 0.01, (n,), 32, "f32")
+    assert H.serialize(s.to_host()) == O.serialize(ref)
+
+
+def test_compress_exact_tiles_mixed(H):
+    """bins beyond 2^30 in some tiles only: exact tiles interleave with
+    register tiles in the look-back chain"""
+    # f32 data can reach |bin| >= 2^30 only on the grid itself (otherwise the
+    # reference raises the resolution error): integer values at eps = 0.5
+    n = 4096 * 12
+    rng = np.random.default_rng(3)
+    x = np.round(rng.normal(0, 50, n)).astype(np.float32)
+    x[4096 * 3:4096 * 4] = (rng.integers(-2 ** 20, 2 ** 20, 4096) * 1536).astype(np.float32)  # |bin| < 2^31
+    x[4096 * 9 + 100] = 1.5 * 2.0 ** 30          # one element in tile 9
+    _full_check(H, x, 0.5, (n,))
+
+
+def test_compress_resolution_error_class(H):
+    n = 4096 * 4
+    x = np.random.default_rng(1).normal(0, 1e4, n).astype(np.float32)
+    with pytest.raises(H.QuantOverflow):
+        H.compress(H.RawArray(x, (n,), "f32"), H.QuantParams(1e-6, (n,), 32, "f32"))
+    with pytest.raises(O.QuantOverflow):
+        O.compress(x, 1e-6, (n,), 32, "f32")
+
+
+def test_compress_certificate_margin(H):
+    """values placed exactly on / next to bin edges (x = (2k+1) eps - eps)"""
+    eps = 0.0123456789
+    k = np.arange(-50000, 50000, dtype=np.float64)
+    edges = (2.0 * k) * eps                       # (x + eps) / 2eps = k + 1/2 ... edges of floor
+    x = np.concatenate([edges, np.nextafter(edges.astype(np.float32), np.inf).astype(np.float64),
+                        np.nextafter(edges.astype(np.float32), -np.inf).astype(np.float64),
+                        (2.0 * k + 1.0) * eps]).astype(np.float32)
+    _full_check(H, x, eps, (x.size,))
+
+
+def _bins_stream(H, bins, n):
+    p = H.QuantParams(0.01, (n,), 32, "f32")
+    s = H.encode_from_quant(H.QuantArray(bins, p))
+    ref = O.encode_bins(bins, 0.01, (n,), 32, "f32")
+    _check_stream(H, s, ref)
+    return s, ref
+
+
+@pytest.mark.parametrize("hi", [2 ** 20, 2 ** 27, 2 ** 31 - 1])
+def test_decode_wide_and_unstaged_tiles(H, hi):
+    """widths > 24 (exact decode), tiles with > 16 KB of payload (in place)"""
+    n = 4096 * 6 + 13
+    rng = np.random.default_rng(hi % 1000)
+    bins = rng.integers(-hi, hi, n)
+    bins[: 4096 * 2] = rng.integers(-50, 50, 4096 * 2)      # ordinary register tiles too
+    s, ref = _bins_stream(H, bins, n)
+    assert np.array_equal(H.decode_to_quant(s).bins, bins)
+    assert H.decompress(s).values.tobytes() == O.decompress(ref).tobytes()
+    S, Q = O.moments(ref)
+    assert H.mean(s) == O.mean_from(S, n, 0.01)
+    assert H.variance(s) == O.variance_from(S, Q, n, 0.01)
+
+
+@pytest.mark.parametrize("scalar", [-1.25, 3.0e5, -7.7e6, 4.3e8])
+def test_scalar_mul_paths(H, scalar):
+    """|rs| < 2^23 register path, larger scalars exact path, overflow classes"""
+    n = 4096 * 5 + 9
+    rng = np.random.default_rng(11)
+    bins = np.cumsum(rng.integers(-40, 40, n))
+    bins[4096:4096 + 64] = rng.integers(-2 ** 29, 2 ** 29, 64)   # big outliers in one tile
+    s, ref = _bins_stream(H, bins, n)
+    try:
+        want = O.serialize(O.scalar_mul(ref, scalar))
+    except O.OracleError as exc:
+        with pytest.raises(H.HoszpError) as ei:
+            H.scalar_mul(s, scalar)
+        assert type(ei.value).__name__ == type(exc).__name__
+    else:
+        assert H.serialize(H.scalar_mul(s, scalar)) == want
+
+
+def test_chain_device_resident_matches_host(H):
+    """the device-resident chain (no host round trips between ops) equals the
+    oracle's chain byte for byte"""
+    import torch
+
+    n = 4096 * 30 + 17
+    rng = np.random.default_rng(5)
+    x = (np.sin(np.arange(n) / 500.0) * 30 + rng.normal(0, 0.05, n)).astype(np.float32)
+    raw = H.RawArray(torch.from_numpy(x).cuda(), (n,), "f32")
+    eps = H.resolve_eps(raw, 1e-4, "rel")
+    p = H.QuantParams(eps, (n,), 32, "f32")
+    z = H.scalar_mul(H.scalar_add(H.negate(H.compress(raw, p)), 3.5), -1.25)
+    zr = O.scalar_mul(O.scalar_add(O.negate(O.compress(x, eps, (n,), 32, "f32")), 3.5), -1.25)
+    assert H.serialize(z.to_host()) == O.serialize(zr)
+    S, Q = O.moments(zr)
+    assert H.mean(z) == O.mean_from(S, n, eps)
+    assert H.variance(z) == O.variance_from(S, Q, n, eps)
+    assert H.decompress(z).values.cpu().numpy().tobytes() == O.decompress(zr).tobytes()
