@@ -160,6 +160,13 @@ int hsz_moments(const uint8_t* widths, const int32_t* outliers, const uint8_t* s
                 uint32_t block_len, int want_sq, uint64_t* out, uint32_t* err, void* ws,
                 uint64_t ws_bytes, void* stream);
 
+/* ---- host plumbing for the Python layer ------------------------------------
+ * hsz_copy_d2h: asynchronous device -> host copy on `stream` (host should be
+ * pinned for a truly asynchronous copy); hsz_stream_sync: wait for `stream`.
+ * Used to fetch a reduction's limbs and the error word in one round trip. */
+int hsz_copy_d2h(void* host, const void* dev, uint64_t bytes, void* stream);
+int hsz_stream_sync(void* stream);
+
 /* library identification (for the loader's sanity check) */
 const char* hsz_version(void);
 

@@ -644,6 +644,18 @@ int hsz_trace_lookback(unsigned int* out3) {
 #endif
 }
 
+int hsz_copy_d2h(void* host, const void* dev, uint64_t bytes, void* stream) {
+  if (!host || !dev) return HSZ_EINVAL;
+  return cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess
+             ? HSZ_OK
+             : HSZ_ECUDA;
+}
+
+int hsz_stream_sync(void* stream) {
+  return cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) == cudaSuccess ? HSZ_OK : HSZ_ECUDA;
+}
+
 uint64_t hsz_tile_count(uint64_t n, uint32_t k) {
   if (k == 0) return 0;
   return ceil_div(ceil_div(n, k), kTileBlocks);

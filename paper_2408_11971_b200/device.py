@@ -20,6 +20,7 @@ reference shares the numpy arrays / bytes objects (ops.py:106-118).
 
 from __future__ import annotations
 
+import functools
 import threading
 
 import numpy as np
@@ -40,12 +41,27 @@ def torch():
     return _torch
 
 
+_CUDA_OK = False
+
+
 def require_cuda():
+    global _CUDA_OK
     t = torch()
-    if not t.cuda.is_available():
-        raise RuntimeError("paper_2408_11971_b200 needs a CUDA device (B200, sm_100a); "
-                           "there is no CPU fallback")
+    if not _CUDA_OK:
+        if not t.cuda.is_available():
+            raise RuntimeError("paper_2408_11971_b200 needs a CUDA device (B200, sm_100a); "
+                               "there is no CPU fallback")
+        _CUDA_OK = True
     return t
+
+
+@functools.lru_cache(maxsize=256)
+def geometry(n: int, k: int):
+    """(tiles, sign bound, payload bound, workspace bytes) for n elements of
+    block length k (C-ABI queries, cached)."""
+    lib = N.load()
+    return (int(lib.hsz_tile_count(n, k)), int(lib.hsz_sign_bound(n, k)),
+            int(lib.hsz_payload_bound(n, k)), int(lib.hsz_workspace_size(n, k)))
 
 
 def ptr(t) -> int:
@@ -75,9 +91,10 @@ class Context:
         with t.cuda.device(self.device):
             self.err = t.zeros(4, dtype=t.int32, device=self.device)
         self.err_ptr = ptr(self.err)
+        self._scratch = t.empty(1 << 12, dtype=t.uint8, pin_memory=True)   # small fetches
 
     def workspace(self, n: int, k: int):
-        need = int(self.lib.hsz_workspace_size(n, k))
+        need = geometry(n, k)[3]
         self.ws_uses += 1
         if self.ws_uses >= _WS_REINIT_USES and self.ws is not None:
             # look-back words carry a 24-bit launch-epoch tag: re-zero the
@@ -109,15 +126,34 @@ class Context:
         raise_for_flags(self.read_flags(), what)
 
     def fetch_checked(self, tensors, what: str = ""):
-        """Download `tensors` together with the sticky error word in ONE
-        synchronize; raise the reference's exception for a set error word."""
-        host = download(list(tensors) + [self.err], self)
-        flags = int(host[-1][0])
+        """Download (small) `tensors` together with the sticky error word in
+        ONE synchronize (C-ABI copies into a pinned scratch); raise the
+        reference's exception for a set error word.  Returns numpy copies."""
+        tensors = list(tensors) + [self.err]
+        sizes = [int(x.numel()) * x.element_size() for x in tensors]
+        total = sum((nb + 15) & ~15 for nb in sizes)
+        if total > self._scratch.numel():
+            self._scratch = torch().empty(max(total, 2 * self._scratch.numel()), dtype=torch().uint8,
+                                          pin_memory=True)
+        base = self._scratch.data_ptr()
+        off = 0
+        offs = []
+        for x, nb in zip(tensors, sizes):
+            if nb:
+                N.check(self.lib.hsz_copy_d2h(base + off, x.data_ptr(), nb, self.handle), "d2h copy")
+            offs.append(off)
+            off += (nb + 15) & ~15
+        N.check(self.lib.hsz_stream_sync(self.handle), "stream sync")
+        host = self._scratch.numpy()
+        out = []
+        for x, nb, o in zip(tensors, sizes, offs):
+            out.append(host[o:o + nb].copy().view(_NP_OF[x.dtype]))
+        flags = int(out[-1][0])
         if flags:
             self.err.zero_()
             self.stream.synchronize()
             raise_for_flags(flags, what)
-        return host[:-1]
+        return out[:-1]
 
     def empty(self, n, dtype):
         t = torch()
@@ -137,14 +173,24 @@ def context(device=None) -> Context:
         idx = t.device(device).index
         if idx is None:
             idx = t.cuda.current_device()
-    stream = t.cuda.current_stream(idx)
-    key = (idx, int(stream.cuda_stream))
-    with _CTX_LOCK:
-        ctx = _CTX.get(key)
-        if ctx is None:
-            ctx = Context(idx, stream)
-            _CTX[key] = ctx
+    raw = _raw_stream(idx)
+    key = (idx, raw)
+    ctx = _CTX.get(key)
+    if ctx is None:
+        with _CTX_LOCK:
+            ctx = _CTX.get(key)
+            if ctx is None:
+                ctx = Context(idx, t.cuda.current_stream(idx))
+                _CTX[key] = ctx
     return ctx
+
+
+def _raw_stream(idx: int) -> int:
+    t = torch()
+    fn = getattr(t._C, "_cuda_getCurrentRawStream", None)
+    if fn is not None:
+        return int(fn(idx))
+    return int(t.cuda.current_stream(idx).cuda_stream)
 
 
 def payload_capacity(lib, n: int, k: int) -> int:
@@ -184,7 +230,7 @@ class DeviceStream:
 
     @property
     def ntiles(self) -> int:
-        return int(self.ctx.lib.hsz_tile_count(self.n, self.k))
+        return geometry(self.n, self.k)[0]
 
     def pointers(self):
         return (ptr(self.widths), ptr(self.outliers), ptr(self.signs), ptr(self.payload),
@@ -267,6 +313,18 @@ class DeviceStream:
 
 
 _PINNED = {}
+_NP_OF_NAMES = {"uint8": np.uint8, "int32": np.int32, "int64": np.int64, "float32": np.float32,
+                "float64": np.float64}
+
+
+class _NpOf(dict):
+    def __missing__(self, dt):
+        v = _NP_OF_NAMES[str(dt).split(".")[-1]]
+        self[dt] = v
+        return v
+
+
+_NP_OF = _NpOf()
 
 
 def download(tensors, ctx: Context = None):
@@ -318,37 +376,46 @@ def download_into(tensors, arena, ctx: Context = None):
 
 
 def new_stream_buffers(ctx: Context, params: QuantParams, payload_cap: int = None):
-    """Allocate output sections for an encoder writing `params`-shaped data."""
+    """Allocate output sections for an encoder writing `params`-shaped data:
+    ONE device allocation carved into 256-byte aligned sections."""
     t = torch()
     n, k = params.element_count, params.block_len
-    lib = ctx.lib
     B = params.block_count
-    T = int(lib.hsz_tile_count(n, k))
-    scap = int(lib.hsz_sign_bound(n, k))
-    pcap = payload_capacity(lib, n, k) if payload_cap is None else int(payload_cap)
-    widths = ctx.empty(B, t.uint8)
-    outliers = ctx.empty(B, t.int32)
-    signs = ctx.empty(scap + N.HSZ_SECTION_SLACK, t.uint8)
-    payload = ctx.empty(pcap + N.HSZ_SECTION_SLACK, t.uint8)
-    toff = ctx.empty(2 * (T + 1), t.int64)
+    T, scap, pbound, _ = geometry(n, k)
+    pcap = (pbound if pbound <= _PAYLOAD_BOUND_LIMIT else max(4 * n, 1 << 20)) \
+        if payload_cap is None else int(payload_cap)
+
+    def up(v):
+        return (v + 255) & ~255
+
+    o_w, o_o = 0, up(B)
+    o_s = o_o + up(4 * B)
+    o_p = o_s + up(scap + N.HSZ_SECTION_SLACK)
+    o_t = o_p + up(pcap + N.HSZ_SECTION_SLACK)
+    total = o_t + 16 * (T + 1)
+    buf = ctx.empty(total, t.uint8)
+    widths = buf[o_w:o_w + B]
+    outliers = buf[o_o:o_o + 4 * B].view(t.int32)
+    signs = buf[o_s:o_s + scap + N.HSZ_SECTION_SLACK]
+    payload = buf[o_p:o_p + pcap + N.HSZ_SECTION_SLACK]
+    toff = buf[o_t:o_t + 16 * (T + 1)].view(t.int64)
     return widths, outliers, signs, payload, toff, scap, pcap
 
 
 def run_encoder(ctx: Context, params: QuantParams, launch) -> DeviceStream:
     """Run an encoder launch(widths, outliers, signs, scap, payload, pcap, toff);
     retry once with the exact payload size if the capacity policy undershot."""
-    lib = ctx.lib
     n, k = params.element_count, params.block_len
     w, o, s, p, toff, scap, pcap = new_stream_buffers(ctx, params)
     launch(w, o, s, scap, p, pcap, toff)
     ds = DeviceStream(params, w, o, s, p, toff, ctx, scap, pcap)
-    if pcap >= int(lib.hsz_payload_bound(n, k)):
+    if pcap >= geometry(n, k)[2]:
         return ds                       # overflow impossible: stay asynchronous
     flags = ctx.read_flags()
     if flags & ~(1 << 6):
         raise_for_flags(flags & ~(1 << 6))
     if flags & (1 << 6):
-        T = int(lib.hsz_tile_count(n, k))
+        T = geometry(n, k)[0]
         need = int(toff[2 * T + 1].item())
         w, o, s, p, toff, scap, pcap = new_stream_buffers(ctx, params, payload_cap=need)
         launch(w, o, s, scap, p, pcap, toff)
