@@ -500,7 +500,7 @@ static int launch_compress_f32(const float* x, uint64_t n, const QuantConst& c,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
   }
-  constexpr int smem = static_cast<int>(e32::kSmemBytes);
+  constexpr int smem = static_cast<int>(e32::kSmem6Bytes);
   auto kern = tma ? e32::compress_f32_kernel<true> : e32::compress_f32_kernel<false>;
   // persistent grid: every CTA resident (the look-back relies on it)
   static int resident[2] = {0, 0}, resident_dev[2] = {-1, -1};

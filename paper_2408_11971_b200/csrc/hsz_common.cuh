@@ -135,6 +135,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// one arrival per warp (barriers initialised with the number of warps): the
+// warp's prior shared-memory writes are ordered before lane 0's arrive
+__device__ __forceinline__ void mbar_arrive_warp(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
+
 // ---------------------------------------------------------------------------
 // gpu-scope acquire / release accesses for the look-back protocol
 

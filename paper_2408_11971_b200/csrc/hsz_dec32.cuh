@@ -287,9 +287,9 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
   const uint64_t last_draw = ntiles + gridDim.x - 1;
   if (tid == kCompute) {
     mbar_init(&S.bar, 1);
-    mbar_init(&S.in_empty, kCompute);
+    mbar_init(&S.in_empty, kCompute / 32);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&S.st_full[b], kCompute);
+      mbar_init(&S.st_full[b], kCompute / 32);
       mbar_init(&S.st_empty[b], 1);
     }
     fence_mbar_init();
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
     if (cur >= ntiles) {
       if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);
       if (tid == 0) S.agg_ts[par] = e32::kDone;
-      mbar_arrive(&S.st_full[par]);
+      mbar_arrive_warp(&S.st_full[par]);
       break;
     }
     // ---- locate and decode this thread's block -------------------------------
@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
       }
     }
     exact = e32::bar_or_compute(exact);   // ... every read of S.in's staged bytes is done
-    if (!exact) mbar_arrive(&S.in_empty);
+    if (!exact) mbar_arrive_warp(&S.in_empty);
     if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);
     uint32_t ts = 0, tp = 0;
     if (!exact) {
@@ -449,9 +449,9 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
                            reinterpret_cast<uint32_t*>(S.pk[par]) + warp * 64);
       }
       e32::bar_sync_n(1, kCompute);
-      mbar_arrive(&S.in_empty);   // the per-block offsets in S.bes/bep are no longer needed
+      mbar_arrive_warp(&S.in_empty);   // the per-block offsets in S.bes/bep are no longer needed
     }
-    mbar_arrive(&S.st_full[par]);
+    mbar_arrive_warp(&S.st_full[par]);
     par ^= 1;
     ++k;
   }
@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(kDecThreads, 5)
   if (tid == kCompute) {
     for (int b = 0; b < 2; ++b) {
       mbar_init(&S.full[b], 1);
-      mbar_init(&S.empty[b], kCompute);
+      mbar_init(&S.empty[b], kCompute / 32);
     }
     fence_mbar_init();
   }
@@ -633,7 +633,7 @@ __global__ void __launch_bounds__(kDecThreads, 5)
     if (fast) {
       int32_t q[K];
       decode_block(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, o, len, q);
-      mbar_arrive(&S.empty[b]);          // staged bytes consumed
+      mbar_arrive_warp(&S.empty[b]);          // staged bytes consumed
       if (kMode == 2) {
         // f32 values = RN32(RN64(2eps * bin)) (codec.py:107-115), into the
         // swizzled 128-byte row of this block
@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(kDecThreads, 5)
           if (live) acc.add(q, kMode == 1);
         });
       }
-      mbar_arrive(&S.empty[b]);
+      mbar_arrive_warp(&S.empty[b]);
     }
     if (kMode == 2) {
       // one TMA tensor store of the whole tile (the stream's partial last

@@ -311,79 +311,151 @@ __device__ __forceinline__ void resolve_tile(Smem& S, const k32::EncodeOut& out,
 // compress, float32 input, block_len 32
 //
 // Persistent, warp-specialised: warps 0-3 compute (thread b = block b of the
-// current tile), warp 4 is the service warp -- it draws tickets, issues the
-// TMA load of the next tile as soon as the compute warps have taken the
-// current one into registers, and resolves the look-back of the PREVIOUS
-// tile while the compute warps quantize the current one.  Per iteration:
+// current tile), warp 4 issues the TMA tile loads (tickets drawn one ahead),
+// warp 5 places staged tiles (look-back + copy-out).  Per tile k:
 //
-//   compute: wait TMA(cur) | quantize | arrive(2) | code + scan + publish
-//            | sync(3) | copy prev out | sync(1) | pack cur into staging
-//   service: sync(2) | TMA(next), draw ticket | resolve prev | sync(3)
+//   compute:   wait full[k&1] | quantize | arrive in_empty[k&1] | code, scan,
+//              publish | claim slot k%4 and ring space | pack into the ring
+//              | arrive st_full[slot]
+//   TMA:       wait in_empty (tile k-1's buffer) | TMA(tile k+1) | draw
+//   placement: wait st_full[slot] | resolve | copy out | free ring space
+//              | arrive st_empty[slot]
 //
-// kTma: tiles arrive by 2-D tensor loads (x 16-byte aligned, >= 128 full
-// rows); otherwise the compute warps load each tile with plain loads.
+// Input tiles are double-buffered (the next load overlaps a whole tile of
+// compute); staged payloads live in a 16 KB byte ring sized by the actual
+// payload (4-5 KB typical, 15.9 KB worst case), so up to 4 tiles can wait
+// for their offsets without stalling the compute warps.
+
+constexpr uint32_t kRingBytes = 16384;
+constexpr int kSlots = 4;
+
+struct RingRec {
+  uint64_t tile;
+  uint64_t end;    // ring bytes allocated up to and including this tile
+  uint32_t ts, tp;
+  uint32_t off;    // byte offset of the tile's payload in the ring (128-aligned)
+  uint32_t pad;
+};
+
+struct Smem6 {
+  unsigned char in[2][kBufBytes];   // input tiles (TMA 128B swizzle; 1024-aligned)
+  unsigned char ring[kRingBytes];   // staged payloads (row-XOR word swizzle per 128 B row)
+  alignas(16) uint32_t sgn[kSlots][TB];
+  uint64_t full[2], in_empty[2];
+  uint64_t st_full[kSlots], st_empty[kSlots];
+  uint64_t cur[2];
+  uint64_t excl_s[kSlots], excl_p[kSlots];
+  RingRec rec[kSlots];
+  volatile uint64_t ring_tail;      // bytes of the ring freed (placement warp)
+  uint64_t epoch;
+  uint32_t alloc_off;
+  uint32_t scan[4];
+  uint32_t wsb[4], wpb[4];
+  uint32_t xscratch[4][64];         // exact path: one block's packed words per warp
+};
+constexpr uint32_t kSmem6Bytes = sizeof(Smem6) + 1024;
+
+__device__ __forceinline__ void copy_ring(const Smem6& S, const k32::EncodeOut& out,
+                                          const RingRec& r, int slot, uint64_t es, uint64_t ep) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t* dsg = reinterpret_cast<uint32_t*>(out.signs + es);
+  for (uint32_t i = lane; i < ((r.ts + 3u) >> 2); i += 32) dsg[i] = S.sgn[slot][i];
+  const uint32_t* pbuf = reinterpret_cast<const uint32_t*>(S.ring + r.off);
+  uint32_t* dst = reinterpret_cast<uint32_t*>(out.payload + ep);
+  const uint32_t nw = (r.tp + 3u) >> 2;
+  uint32_t head = static_cast<uint32_t>(((16u - (ep & 15u)) & 15u) >> 2);
+  head = head < nw ? head : nw;
+  if (lane < head) dst[lane] = pbuf[swz_word(lane)];
+  const uint32_t nv = (nw - head) >> 2;
+  uint4* dv = reinterpret_cast<uint4*>(dst + head);
+  for (uint32_t i = lane; i < nv; i += 32) {
+    const uint32_t k = head + 4u * i;
+    dv[i] = make_uint4(pbuf[swz_word(k)], pbuf[swz_word(k + 1)], pbuf[swz_word(k + 2)],
+                       pbuf[swz_word(k + 3)]);
+  }
+  const uint32_t rest = head + 4u * nv + lane;
+  if (rest < nw) dst[rest] = pbuf[swz_word(rest)];
+}
+
+// one warp: resolve `tile`; returns the offsets (~0 sign offset: over capacity)
+__device__ __forceinline__ void resolve6(const k32::EncodeOut& out, uint64_t tile, uint64_t epoch,
+                                         uint64_t ntiles, uint32_t ts, uint32_t tp, uint64_t* es_out,
+                                         uint64_t* ep_out) {
+  const int lane = threadIdx.x & 31;
+  uint64_t es, ep;
+  lb_resolve(lb_words(out.ws), tile, epoch, ts, tp, &es, &ep);
+  const bool fits = es + ts <= out.sign_cap && ep + tp <= out.payload_cap;
+  if (lane == 0) {
+    out.toff[2 * tile] = es;
+    out.toff[2 * tile + 1] = ep;
+    if (tile == ntiles - 1) {
+      out.toff[2 * ntiles] = es + ts;
+      out.toff[2 * ntiles + 1] = ep + tp;
+    }
+    if (!fits) atomicOr(out.err, HSZ_ERR_CAPACITY);
+  }
+  *es_out = fits ? es : ~0ull;
+  *ep_out = ep;
+}
+
 template <bool kTma>
 __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
     compress_f32_kernel(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ x,
                         uint64_t n, QuantF32 qf, QuantConst qc, k32::EncodeOut out,
                         uint64_t nblocks, uint64_t ntiles, uint32_t tail_len) {
   extern __shared__ unsigned char smraw[];
-  Smem& S = smem_at(smraw);
+  const uint32_t a0 = smem_u32(smraw);
+  Smem6& S = *reinterpret_cast<Smem6*>(smraw + (((a0 + 1023u) & ~1023u) - a0));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   LookbackWs lw = LookbackWs::bind(out.ws, ntiles);
   const uint64_t last_draw = ntiles + gridDim.x - 1;   // every CTA draws once past the end
   const uint64_t full_rows = n / K;
-  uint64_t ahead = ~0ull;                               // service lane 0: ticket after `next`
-  auto draw = [&](uint64_t epoch) -> uint64_t {
-    const uint64_t t = atom_add_relaxed(lw.ticket, 1);
-    if (t == last_draw) {
-      st_relaxed(lw.ticket, 0);
-      st_release(lw.epoch, epoch + 1);
-    }
-    return t;
-  };
-  auto issue = [&](uint64_t t) {   // service lane 0: tile t into S.in (or "no more tiles")
-    S.cur = t;
-    if (t < ntiles) {
-      if (kTma) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive_expect_tx(&S.bar, kBufBytes);
-        tma_load_2d(S.in, &tmap, 0, static_cast<int>(t * TB), &S.bar);
-      } else {
-        mbar_arrive(&S.bar);   // the compute warps load the tile themselves
-      }
-    } else {
-      mbar_arrive(&S.bar);
-    }
-  };
   if (tid == kCompute) {
-    mbar_init(&S.bar, 1);
-    mbar_init(&S.in_empty, kCompute);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&S.st_full[b], kCompute);
-      mbar_init(&S.st_empty[b], 1);
+      mbar_init(&S.full[b], 1);
+      mbar_init(&S.in_empty[b], kCompute / 32);
     }
+    for (int i = 0; i < kSlots; ++i) {
+      mbar_init(&S.st_full[i], kCompute / 32);
+      mbar_init(&S.st_empty[i], 1);
+    }
+    S.ring_tail = 0;
     fence_mbar_init();
-    const uint64_t e = ld_acquire(lw.epoch);
-    S.epoch = e;
+    S.epoch = ld_acquire(lw.epoch);
   }
   __syncthreads();
   const uint64_t epoch = S.epoch;
 
   if (warp == kCompute / 32) {
     // ============================ TMA warp ==============================
-    // per tile k handed to the compute warps: wait in_empty (tile k consumed)
-    // | TMA(tile k+1) or "done" | draw the ticket after it
-    uint64_t t = ~0ull, ahead = ~0ull;
     if (lane == 0) {
-      t = draw(epoch);
-      issue(t);
-      if (t < ntiles) ahead = draw(epoch);
-      for (uint32_t k = 0; t < ntiles; ++k) {
-        mbar_wait_parity_sleep(&S.in_empty, k & 1u);   // S.in holds no unread data
+      auto draw = [&]() -> uint64_t {
+        const uint64_t t = atom_add_relaxed(lw.ticket, 1);
+        if (t == last_draw) {
+          st_relaxed(lw.ticket, 0);
+          st_release(lw.epoch, epoch + 1);
+        }
+        return t;
+      };
+      auto issue = [&](uint64_t t, int b) {   // tile t into in[b] (or "no more tiles")
+        S.cur[b] = t;
+        if (t < ntiles && kTma) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive_expect_tx(&S.full[b], kBufBytes);
+          tma_load_2d(S.in[b], &tmap, 0, static_cast<int>(t * TB), &S.full[b]);
+        } else {
+          mbar_arrive(&S.full[b]);   // no more tiles / the compute warps load it
+        }
+      };
+      uint64_t t = draw();
+      issue(t, 0);
+      uint64_t ahead = t < ntiles ? draw() : ~0ull;
+      for (uint32_t k = 1; t < ntiles; ++k) {   // issue the k-th tile
+        const int b = k & 1;
+        if (k >= 2) mbar_wait_parity_sleep(&S.in_empty[b], ((k >> 1) - 1) & 1u);
         const uint64_t nx = ahead;
-        issue(nx);
-        if (nx < ntiles) ahead = draw(epoch);
+        issue(nx, b);
+        if (nx < ntiles) ahead = draw();
         t = nx;
       }
     }
@@ -392,46 +464,47 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
 
   if (warp == kCompute / 32 + 1) {
     // =========================== placement warp ===========================
-    // the kk-th tile of this CTA: wait st_full[b] | resolve its offsets (look-
-    // back) | copy it out of pk[b] | arrive st_empty[b]
     for (uint32_t kk = 0;; ++kk) {
-      const int b = kk & 1;
-      mbar_wait_parity_sleep(&S.st_full[b], (kk >> 1) & 1u);
-      const uint32_t pts = S.agg_ts[b], ptp = S.agg_tp[b];
-      if (pts == kDone) break;
-      if (pts != kSelfPlaced) {
-        const uint64_t tile = S.tile_of[b];
-        trace_tile(tile, 7);
-        resolve_tile(S, out, tile, epoch, ntiles, pts, ptp, b);
-        __syncwarp();
-        copy_staged(S, out, pts, ptp, b, lane, 32);
-        trace_tile(tile, 8);
+      const int slot = kk % kSlots;
+      mbar_wait_parity_sleep(&S.st_full[slot], (kk / kSlots) & 1u);
+      const RingRec r = S.rec[slot];
+      if (r.ts == kDone) break;
+      if (r.ts != kSelfPlaced) {
+        trace_tile(r.tile, 7);
+        uint64_t es, ep;
+        resolve6(out, r.tile, epoch, ntiles, r.ts, r.tp, &es, &ep);
+        if (es != ~0ull) copy_ring(S, out, r, slot, es, ep);
+        trace_tile(r.tile, 8);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.st_empty[b]);
+      if (lane == 0) {
+        __threadfence_block();   // the ring reads complete before the space is reused
+        S.ring_tail = r.end;
+        mbar_arrive(&S.st_empty[slot]);
+      }
     }
     return;
   }
 
   // =========================== compute warps ===========================
-  // per tile k: wait TMA(tile k) | quantize | arrive in_empty | code, scan,
-  //             publish | wait st_empty (tile k-2 out) | pack into staging[k&1]
-  //             | arrive st_full
-  uint32_t phase = 0;
   uint32_t flags = 0;
-  int par = 0;
-  int k = 0;
-  while (true) {
-    mbar_wait_parity(&S.bar, phase);
-    phase ^= 1u;
-    const uint64_t cur = S.cur;
+  uint64_t head = 0;   // thread 0: ring bytes allocated
+  for (uint32_t k = 0;; ++k) {
+    const int b = k & 1;
+    const int slot = k % kSlots;
+    mbar_wait_parity(&S.full[b], (k >> 1) & 1u);
+    const uint64_t cur = S.cur[b];
     if (cur >= ntiles) {
-      // stop the placement warp: a "done" marker in the next buffer it waits on
-      if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);
-      if (tid == 0) S.agg_ts[par] = kDone;
-      mbar_arrive(&S.st_full[par]);
+      // stop the placement warp
+      if (k >= kSlots) mbar_wait_parity(&S.st_empty[slot], ((k / kSlots) - 1) & 1u);
+      if (tid == 0) {
+        S.rec[slot].ts = kDone;
+        S.rec[slot].end = head;
+      }
+      mbar_arrive_warp(&S.st_full[slot]);
       break;
     }
+    unsigned char* in = S.in[b];
     bool wide = false;
     uint32_t qb[K];
     trace_tile(cur, 1);
@@ -442,7 +515,7 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
         if (tid < K) {
           const uint32_t r = static_cast<uint32_t>(n % K);
           const float v = static_cast<uint32_t>(tid) < r ? x[full_rows * K + tid] : 0.0f;
-          *reinterpret_cast<float*>(S.in + swz_elem(static_cast<uint32_t>(full_rows - row0), tid)) = v;
+          *reinterpret_cast<float*>(in + swz_elem(static_cast<uint32_t>(full_rows - row0), tid)) = v;
         }
         bar_sync_n(1, kCompute);
       }
@@ -451,14 +524,14 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
       for (uint32_t i = tid; i < TB * K; i += kCompute) {
         const uint64_t e = e0 + i;
         const float v = e < n ? x[e] : 0.0f;
-        *reinterpret_cast<float*>(S.in + swz_elem(i >> 5, i & 31u)) = v;
+        *reinterpret_cast<float*>(in + swz_elem(i >> 5, i & 31u)) = v;
       }
       bar_sync_n(1, kCompute);
     }
     trace_tile(cur, 2);
     // ---- quantize this thread's row ----------------------------------------
     {
-      const unsigned char* row = S.in + tid * 128;
+      const unsigned char* row = in + tid * 128;
       bool bad = false;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -469,24 +542,21 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
         qb[4 * j + 3] = quant_f32(v.w, qf, bad);
       }
       if (__any_sync(kFull, bad)) {   // rare: an element inside the certificate margin
-        // in place in this thread's own row of S.in (nothing large may be live
-        // across the exact routine's call): fast bins overwrite their inputs,
-        // then the failed elements are redone exactly
-        float* rowf = reinterpret_cast<float*>(S.in + tid * 128);
+        // in place in this thread's own row of the input buffer (nothing large
+        // may be live across the exact routine's call)
         uint32_t mask = 0;
 #pragma unroll
         for (int i = 0; i < K; ++i) {
-          float* pi = reinterpret_cast<float*>(S.in + swz_elem(tid, i));
-          bool b = false;
-          (void)quant_f32(*pi, qf, b);
-          mask |= (b ? 1u : 0u) << i;
-          if (!b) *reinterpret_cast<uint32_t*>(pi) = qb[i];
+          float* pi = reinterpret_cast<float*>(in + swz_elem(tid, i));
+          bool bb = false;
+          (void)quant_f32(*pi, qf, bb);
+          mask |= (bb ? 1u : 0u) << i;
+          if (!bb) *reinterpret_cast<uint32_t*>(pi) = qb[i];
         }
-        (void)rowf;
 #pragma unroll 1
         for (int i = 0; i < K; ++i) {
           if ((mask >> i) & 1u) {
-            uint32_t* pi = reinterpret_cast<uint32_t*>(S.in + swz_elem(tid, i));
+            uint32_t* pi = reinterpret_cast<uint32_t*>(in + swz_elem(tid, i));
             const ExactQ r = quant_exact(__uint_as_float(*pi), qc);
             flags |= r.flags;
             wide |= !((r.q > -kWide) & (r.q < kWide));
@@ -494,15 +564,11 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
           }
         }
 #pragma unroll
-        for (int i = 0; i < K; ++i) qb[i] = *reinterpret_cast<const uint32_t*>(S.in + swz_elem(tid, i));
+        for (int i = 0; i < K; ++i) qb[i] = *reinterpret_cast<const uint32_t*>(in + swz_elem(tid, i));
       }
-      wide = bar_or_compute(wide);   // ... and every read of S.in is done
-      mbar_arrive(&S.in_empty);        // the service warp may refill S.in
-      trace_tile(cur, 5);
-      if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);   // tile k-2 copied out
-      trace_tile(cur, 6);
+      wide = bar_or_compute(wide);    // ... and every read of this input buffer is done
+      mbar_arrive_warp(&S.in_empty[b]);
     }
-    uint32_t ts = 0, tp = 0;
     if (!wide) {
       const uint64_t gb = cur * TB + tid;
       const bool active = gb < nblocks;
@@ -514,52 +580,76 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
       uint32_t tot;
       const uint32_t ex = cta_scan(sb | (pb << 10), S.scan, &tot);   // sb <= 512, pb <= 15872
       const uint32_t es = ex & 1023u, ep = ex >> 10;
-      ts = tot & 1023u;
-      tp = tot >> 10;
-      if (tid == 0) {
-        lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
-        S.agg_ts[par] = ts;
-        S.agg_tp[par] = tp;
-        S.tile_of[par] = cur;
-      }
+      const uint32_t ts = tot & 1023u, tp = tot >> 10;
+      if (tid == 0) lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
       trace_tile(cur, 3);
       if (active) {
         out.widths[gb] = static_cast<uint8_t>(bc.w);
         out.outliers[gb] = static_cast<int32_t>(qb[0] - kMagicBits);
       }
-      if (sb) S.sgn[par][es >> 2] = bswap32(bc.sg);
-      pack_block(bc, ep >> 2, reinterpret_cast<uint32_t*>(S.pk[par]));
+      // claim metadata slot k%4 and ring space for the packed payload
+      if (k >= kSlots) mbar_wait_parity(&S.st_empty[slot], ((k / kSlots) - 1) & 1u);
+      if (tid == 0) {
+        const uint32_t need = (tp + 127u) & ~127u;
+        uint32_t pos = static_cast<uint32_t>(head % kRingBytes);
+        if (pos + need > kRingBytes) {   // no wrap inside a tile: skip to the ring start
+          head += kRingBytes - pos;
+          pos = 0;
+        }
+        unsigned ns = 32;
+        while (head + need - S.ring_tail > kRingBytes) {
+          __nanosleep(ns);
+          ns = ns < 256 ? ns * 2 : 256;
+        }
+        head += need;
+        S.rec[slot].tile = cur;
+        S.rec[slot].end = head;
+        S.rec[slot].ts = ts;
+        S.rec[slot].tp = tp;
+        S.rec[slot].off = pos;
+        S.alloc_off = pos;
+      }
+      bar_sync_n(1, kCompute);
       trace_tile(cur, 4);
+      if (sb) S.sgn[slot][es >> 2] = bswap32(bc.sg);
+      pack_block(bc, ep >> 2, reinterpret_cast<uint32_t*>(S.ring + S.alloc_off));
+      trace_tile(cur, 5);
+      mbar_arrive_warp(&S.st_full[slot]);
     } else {
-      // exact path: sizes, publish, resolve and place itself (the look-back
-      // waits for the previous tile's inclusive prefix from the service warp)
+      // exact path: sizes and publish first; the tile then resolves and
+      // places itself (the placement warp resolves the previous tiles)
       k32::SrcQuant<float> src{x, n, qc, cur};
       flags |= k32::fallback_sizes(src, out, cur, nblocks, tail_len, S.wsb, S.wpb);
       bar_sync_n(1, kCompute);
-      ts = S.wsb[0] + S.wsb[1] + S.wsb[2] + S.wsb[3];
-      tp = S.wpb[0] + S.wpb[1] + S.wpb[2] + S.wpb[3];
+      const uint32_t ts = S.wsb[0] + S.wsb[1] + S.wsb[2] + S.wsb[3];
+      const uint32_t tp = S.wpb[0] + S.wpb[1] + S.wpb[2] + S.wpb[3];
+      if (tid == 0) lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
+      if (k >= kSlots) mbar_wait_parity(&S.st_empty[slot], ((k / kSlots) - 1) & 1u);
+      if (tid == 0) {
+        S.rec[slot].tile = cur;
+        S.rec[slot].end = head;
+        S.rec[slot].ts = kSelfPlaced;
+      }
+      mbar_arrive_warp(&S.st_full[slot]);
       if (warp == 0) {
+        uint64_t es, ep;
+        resolve6(out, cur, epoch, ntiles, ts, tp, &es, &ep);
         if (lane == 0) {
-          lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
-          S.agg_ts[par] = kSelfPlaced;
+          S.excl_s[slot] = es;
+          S.excl_p[slot] = ep;
         }
-        __syncwarp();
-        resolve_tile(S, out, cur, epoch, ntiles, ts, tp, par);
       }
       bar_sync_n(1, kCompute);
-      if (S.excl_s[par] != ~0ull) {
-        uint64_t gs = S.excl_s[par], gp = S.excl_p[par];
+      if (S.excl_s[slot] != ~0ull) {
+        uint64_t gs = S.excl_s[slot], gp = S.excl_p[slot];
         for (int i = 0; i < warp; ++i) {
           gs += S.wsb[i];
           gp += S.wpb[i];
         }
-        k32::fallback_pack(src, out, cur, nblocks, tail_len, gs, gp,
-                           reinterpret_cast<uint32_t*>(S.pk[par]) + warp * 64);
+        k32::fallback_pack(src, out, cur, nblocks, tail_len, gs, gp, S.xscratch[warp]);
       }
+      bar_sync_n(1, kCompute);
     }
-    mbar_arrive(&S.st_full[par]);      // tile k staged (or placed)
-    par ^= 1;
-    ++k;
   }
   flags = __reduce_or_sync(kFull, flags);
   if (lane == 0 && flags) atomicOr(out.err, flags);

@@ -44,8 +44,8 @@ nt = tile.max() + 1
 T = np.full((nt, 9), np.nan)
 T[tile, tag] = t
 print("records", n, "tiles", nt, "span us %.1f" % np.nanmax(T))
-names = {(1, 2): "load wait", (2, 5): "quant", (5, 6): "st_empty wait", (6, 3): "code+scan", (3, 4): "pack", (4, 7): "staged->placing",
-         (7, 8): "svc resolve+copy", (3, 8): "publish->placed"}
+names = {(1, 2): "load wait", (2, 3): "quant+code+scan", (3, 4): "slot/ring wait", (4, 5): "pack",
+         (5, 7): "staged->placing", (7, 8): "svc resolve+copy", (3, 8): "publish->placed"}
 for (a0, a1), nm in names.items():
     d = T[:, a1] - T[:, a0]
     print(f"{nm:11s} mean {np.nanmean(d):6.2f}  p50 {np.nanmedian(d):6.2f}  p90 {np.nanpercentile(d, 90):6.2f}  max {np.nanmax(d):6.2f} us")
