@@ -404,6 +404,7 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
     if (!exact) {
       e32::BlockCode bc;
       e32::block_code(qb, len, bc);
+      const uint32_t wmax = __reduce_max_sync(kFull, bc.w);
       const uint32_t sb = (bc.w && active) ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
       const uint32_t pb = (static_cast<uint32_t>(len) * bc.w + 7u) >> 3;
       uint32_t tot;
@@ -422,7 +423,7 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
         out.outliers[gb] = static_cast<int32_t>(qb[0]);
       }
       if (sb) S.sgn[par][es >> 2] = bswap32(bc.sg);
-      e32::pack_block(bc, ep >> 2, reinterpret_cast<uint32_t*>(S.pk[par]));
+      e32::pack_block(bc, wmax, ep >> 2, reinterpret_cast<uint32_t*>(S.pk[par]));
     } else {
       // exact warp-per-block path, decoding from global memory; places itself
       SrcSmulExact src{in, &S, sp.rs, sp.d};

@@ -62,14 +62,17 @@ static_assert(kThreads == 128, "the CTA scan assumes 4 warps");
 //   p = RN(x*rh), e = x*rh - p (exact FMA), m = floor(p), f = p - m,
 //   c = RN(x*rl + e), v = RN(RN(f - 1/2) + c)  ~  t - m - 1
 // |v - (t - m - 1)| < 2^-23 for |p| < 2^21 (error analysis in DESIGN.md), so
-// if |v| > delta = 2^-21 then t is at least 2^-22 away from the integer m + 1,
+// if |v| > 2^-21 then t is at least 2^-22 away from the integer m + 1,
 // floor(t) = m + [v >= 0] equals the reference's floor (whose own error is
 // below 2^-31 here), and |x - d q| <= eps - d 2^-22 proves that the repair
 // pass of codec.py:140-154 does not fire.  Returns the bin offset by the
 // magic constant: bits(m + 1.5*2^23) + [v >= 0] = 0x4B400000 + floor(t).
+// (A round-to-nearest variant without FRND was tried: products that are
+// exact half-integers, 2^-10 of them at |p| ~ 2^13, land on its certificate
+// boundary and push whole warps into the slow path -- 40% slower.)
 struct QuantF32 {
   float rh, rl;
-  float delta;   // +inf disables the fast path (every element takes quantize1)
+  float delta;   // > 0 enables the fast path (else every element takes quantize1)
 };
 
 __host__ inline QuantF32 make_quant_f32(const QuantConst& c) {
@@ -78,7 +81,7 @@ __host__ inline QuantF32 make_quant_f32(const QuantConst& c) {
   q.rh = static_cast<float>(R);
   q.rl = static_cast<float>(R - static_cast<double>(q.rh));
   const bool ok = c.d >= 0x1p-60 && c.d <= 0x1p+60;
-  q.delta = ok ? 0x1p-21f : __builtin_huge_valf();
+  q.delta = ok ? 0x1p-21f : -1.0f;
   return q;
 }
 
@@ -89,7 +92,7 @@ __device__ __forceinline__ uint32_t quant_f32(float x, const QuantF32& qf, bool&
   const float f = __fsub_rn(p, m);
   const float c = __fmaf_rn(x, qf.rl, e);
   const float v = __fadd_rn(__fsub_rn(f, 0.5f), c);
-  bad |= !((fabsf(v) > qf.delta) & (fabsf(p) < 2097152.0f));
+  bad |= !((fabsf(v) > qf.delta) & (fabsf(p) < 2097152.0f) & (qf.delta > 0.0f));
   const uint32_t mb = __float_as_uint(__fadd_rn(m, kMagicF));
   return mb + 1u + static_cast<uint32_t>(__float_as_int(v) >> 31);
 }
@@ -241,8 +244,10 @@ __device__ __forceinline__ void pack_fields(const BlockCode& bc, uint32_t a, uin
   if (nbm > -32) pbuf[swz_word(a)] = bswap32(acc << (-nbm));   // partial tail block
 }
 
-__device__ __forceinline__ void pack_block(const BlockCode& bc, uint32_t a, uint32_t* pbuf) {
-  const uint32_t wmax = __reduce_max_sync(kFull, bc.w);   // warp-uniform grouping
+// wmax = __reduce_max_sync over the warp (warp-uniform grouping; computed by
+// the caller early so its latency overlaps other work)
+__device__ __forceinline__ void pack_block(const BlockCode& bc, uint32_t wmax, uint32_t a,
+                                           uint32_t* pbuf) {
   if (bc.w == 0) return;
   if (wmax <= 7) {
     pack_fields<4>(bc, a, pbuf);
@@ -575,6 +580,7 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
       const int len = !active ? 0 : (gb == nblocks - 1 ? static_cast<int>(tail_len) : K);
       BlockCode bc;
       block_code(qb, len, bc);
+      const uint32_t wmax = __reduce_max_sync(kFull, bc.w);
       const uint32_t sb = (bc.w && active) ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
       const uint32_t pb = (static_cast<uint32_t>(len) * bc.w + 7u) >> 3;
       uint32_t tot;
@@ -612,7 +618,7 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
       bar_sync_n(1, kCompute);
       trace_tile(cur, 4);
       if (sb) S.sgn[slot][es >> 2] = bswap32(bc.sg);
-      pack_block(bc, ep >> 2, reinterpret_cast<uint32_t*>(S.ring + S.alloc_off));
+      pack_block(bc, wmax, ep >> 2, reinterpret_cast<uint32_t*>(S.ring + S.alloc_off));
       trace_tile(cur, 5);
       mbar_arrive_warp(&S.st_full[slot]);
     } else {
