@@ -127,7 +127,13 @@ __global__ void __launch_bounds__(kThreads) minmax_kernel(const T* x, uint64_t n
 }
 
 // ---- K0 for float32: 8 independent 16-byte loads in flight per thread -------
-constexpr int kMmThreads = 512;
+#ifndef HSZ_MM_LOAD
+#define HSZ_MM_LOAD __ldcs
+#endif
+#ifndef HSZ_MM_THREADS
+#define HSZ_MM_THREADS 256
+#endif
+constexpr int kMmThreads = HSZ_MM_THREADS;
 __global__ void __launch_bounds__(kMmThreads) minmax_f32_kernel(const float* __restrict__ x, uint64_t n,
                                                                 double* out, uint32_t* err, void* ws) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -140,7 +146,7 @@ __global__ void __launch_bounds__(kMmThreads) minmax_f32_kernel(const float* __r
   for (; i + 7 * stride < nv; i += 8 * stride) {
     float4 v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldcs(xv + i + u * stride);
+    for (int u = 0; u < 8; ++u) v[u] = HSZ_MM_LOAD(xv + i + u * stride);
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       bad |= !isfinite(v[u].x) | !isfinite(v[u].y) | !isfinite(v[u].z) | !isfinite(v[u].w);
@@ -500,7 +506,7 @@ static int launch_compress_f32(const float* x, uint64_t n, const QuantConst& c,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
   }
-  constexpr int smem = static_cast<int>(e32::kSmem6Bytes);
+  constexpr int smem = static_cast<int>(e32::kSmem7Bytes);
   auto kern = tma ? e32::compress_f32_kernel<true> : e32::compress_f32_kernel<false>;
   // persistent grid: every CTA resident (the look-back relies on it)
   static int resident[2] = {0, 0}, resident_dev[2] = {-1, -1};
@@ -511,13 +517,13 @@ static int launch_compress_f32(const float* x, uint64_t n, const QuantConst& c,
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
     int per_sm = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, e32::kThreadsWS, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, e32::kThreadsC, smem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     resident[tma] = (per_sm > 0 ? per_sm : 1) * sms;
     resident_dev[tma] = dev;
   }
   const uint64_t grid = nt < static_cast<uint64_t>(resident[tma]) ? nt : static_cast<uint64_t>(resident[tma]);
-  kern<<<static_cast<unsigned>(grid), e32::kThreadsWS, smem, st>>>(map, x, n, qf, c, out, nb, nt,
+  kern<<<static_cast<unsigned>(grid), e32::kThreadsC, smem, st>>>(map, x, n, qf, c, out, nb, nt,
                                                                 tail_len_of(n, 32));
   return launch_status();
 }

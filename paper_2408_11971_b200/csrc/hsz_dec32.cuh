@@ -337,9 +337,11 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
       const uint32_t pts = S.agg_ts[b], ptp = S.agg_tp[b];
       if (pts == e32::kDone) break;
       if (pts != e32::kSelfPlaced) {
+        trace_tile(S.tile_of[b], 7);
         smul_resolve(S, out, S.tile_of[b], epoch, ntiles, pts, ptp, b);
         __syncwarp();
         smul_copy_staged(S, out, pts, ptp, b, lane, 32);
+        trace_tile(S.tile_of[b], 8);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.st_empty[b]);
@@ -354,6 +356,7 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
     mbar_wait_parity(&S.bar, phase);
     phase ^= 1u;
     const uint64_t cur = S.in.tile;
+    if (cur < ntiles) trace_tile(cur, 1);
     if (cur >= ntiles) {
       if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);
       if (tid == 0) S.agg_ts[par] = e32::kDone;
@@ -381,6 +384,7 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
     const bool fast_in = S.in.staged && w <= static_cast<uint32_t>(kFastW) && o > -(1 << 29) && o < (1 << 29);
     // CTA-uniform: the register decode is warp-collective (decode_block)
     bool exact = e32::bar_or_compute(!fast_in || !sp.small_rs);
+    trace_tile(cur, 2);
     uint32_t qb[K];
     if (!exact) {
       int32_t q[K];
@@ -398,6 +402,7 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
       }
     }
     exact = e32::bar_or_compute(exact);   // ... every read of S.in's staged bytes is done
+    trace_tile(cur, 3);
     if (!exact) mbar_arrive_warp(&S.in_empty);
     if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);
     uint32_t ts = 0, tp = 0;
@@ -423,7 +428,9 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
         out.outliers[gb] = static_cast<int32_t>(qb[0]);
       }
       if (sb) S.sgn[par][es >> 2] = bswap32(bc.sg);
+      trace_tile(cur, 4);
       e32::pack_block(bc, wmax, ep >> 2, reinterpret_cast<uint32_t*>(S.pk[par]));
+      trace_tile(cur, 5);
     } else {
       // exact warp-per-block path, decoding from global memory; places itself
       SrcSmulExact src{in, &S, sp.rs, sp.d};
@@ -567,7 +574,10 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 
 // kMode 0: mean (S), 1: variance (S, Q), 2: decompress to float32
 template <int kMode>
-__global__ void __launch_bounds__(kDecThreads, 5)
+#ifndef HSZ_DEC_CTAS
+#define HSZ_DEC_CTAS 5
+#endif
+__global__ void __launch_bounds__(kDecThreads, HSZ_DEC_CTAS)
     decode_pipe_kernel(const __grid_constant__ CUtensorMap omap, StreamIn in, DecF32Sink fs,
                        MomentsSink ms, int use_tma, uint32_t* err) {
   extern __shared__ unsigned char smraw[];

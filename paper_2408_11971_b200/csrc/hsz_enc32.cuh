@@ -360,12 +360,13 @@ struct Smem6 {
 };
 constexpr uint32_t kSmem6Bytes = sizeof(Smem6) + 1024;
 
-__device__ __forceinline__ void copy_ring(const Smem6& S, const k32::EncodeOut& out,
-                                          const RingRec& r, int slot, uint64_t es, uint64_t ep) {
+__device__ __forceinline__ void copy_ring(const uint32_t* sgn, const unsigned char* ring,
+                                          const k32::EncodeOut& out, const RingRec& r, uint64_t es,
+                                          uint64_t ep) {
   const uint32_t lane = threadIdx.x & 31;
   uint32_t* dsg = reinterpret_cast<uint32_t*>(out.signs + es);
-  for (uint32_t i = lane; i < ((r.ts + 3u) >> 2); i += 32) dsg[i] = S.sgn[slot][i];
-  const uint32_t* pbuf = reinterpret_cast<const uint32_t*>(S.ring + r.off);
+  for (uint32_t i = lane; i < ((r.ts + 3u) >> 2); i += 32) dsg[i] = sgn[i];
+  const uint32_t* pbuf = reinterpret_cast<const uint32_t*>(ring + r.off);
   uint32_t* dst = reinterpret_cast<uint32_t*>(out.payload + ep);
   const uint32_t nw = (r.tp + 3u) >> 2;
   uint32_t head = static_cast<uint32_t>(((16u - (ep & 15u)) & 15u) >> 2);
@@ -403,23 +404,47 @@ __device__ __forceinline__ void resolve6(const k32::EncodeOut& out, uint64_t til
   *ep_out = ep;
 }
 
+// v7: 4 compute warps + 1 placement warp (160 threads, 5 CTAs per SM).  The
+// compute warps' thread 0 issues the next tile's TMA load as soon as the CTA
+// has read the current tile (single input buffer) and draws tickets one tile
+// ahead; placement and the staging ring are as described above.
+constexpr int kThreadsC = kCompute + 32;
+#ifndef HSZ_CMP_CTAS
+#define HSZ_CMP_CTAS 5
+#endif
+
+struct Smem7 {
+  unsigned char in[kBufBytes];      // input tile (TMA 128B swizzle; 1024-aligned)
+  unsigned char ring[kRingBytes];   // staged payloads (row-XOR word swizzle per 128 B row)
+  alignas(16) uint32_t sgn[kSlots][TB];
+  uint64_t full;
+  uint64_t st_full[kSlots], st_empty[kSlots];
+  uint64_t cur;
+  uint64_t excl_s[kSlots], excl_p[kSlots];
+  RingRec rec[kSlots];
+  volatile uint64_t ring_tail;      // bytes of the ring freed (placement warp)
+  uint64_t epoch;
+  uint32_t alloc_off;
+  uint32_t scan[4];
+  uint32_t wsb[4], wpb[4];
+  uint32_t xscratch[4][64];         // exact path: one block's packed words per warp
+};
+constexpr uint32_t kSmem7Bytes = sizeof(Smem7) + 1024;
+
 template <bool kTma>
-__global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
+__global__ void __launch_bounds__(kThreadsC, HSZ_CMP_CTAS)
     compress_f32_kernel(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ x,
                         uint64_t n, QuantF32 qf, QuantConst qc, k32::EncodeOut out,
                         uint64_t nblocks, uint64_t ntiles, uint32_t tail_len) {
   extern __shared__ unsigned char smraw[];
   const uint32_t a0 = smem_u32(smraw);
-  Smem6& S = *reinterpret_cast<Smem6*>(smraw + (((a0 + 1023u) & ~1023u) - a0));
+  Smem7& S = *reinterpret_cast<Smem7*>(smraw + (((a0 + 1023u) & ~1023u) - a0));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   LookbackWs lw = LookbackWs::bind(out.ws, ntiles);
   const uint64_t last_draw = ntiles + gridDim.x - 1;   // every CTA draws once past the end
   const uint64_t full_rows = n / K;
-  if (tid == kCompute) {
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&S.full[b], 1);
-      mbar_init(&S.in_empty[b], kCompute / 32);
-    }
+  if (tid == 0) {
+    mbar_init(&S.full, 1);
     for (int i = 0; i < kSlots; ++i) {
       mbar_init(&S.st_full[i], kCompute / 32);
       mbar_init(&S.st_empty[i], 1);
@@ -432,42 +457,6 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
   const uint64_t epoch = S.epoch;
 
   if (warp == kCompute / 32) {
-    // ============================ TMA warp ==============================
-    if (lane == 0) {
-      auto draw = [&]() -> uint64_t {
-        const uint64_t t = atom_add_relaxed(lw.ticket, 1);
-        if (t == last_draw) {
-          st_relaxed(lw.ticket, 0);
-          st_release(lw.epoch, epoch + 1);
-        }
-        return t;
-      };
-      auto issue = [&](uint64_t t, int b) {   // tile t into in[b] (or "no more tiles")
-        S.cur[b] = t;
-        if (t < ntiles && kTma) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_arrive_expect_tx(&S.full[b], kBufBytes);
-          tma_load_2d(S.in[b], &tmap, 0, static_cast<int>(t * TB), &S.full[b]);
-        } else {
-          mbar_arrive(&S.full[b]);   // no more tiles / the compute warps load it
-        }
-      };
-      uint64_t t = draw();
-      issue(t, 0);
-      uint64_t ahead = t < ntiles ? draw() : ~0ull;
-      for (uint32_t k = 1; t < ntiles; ++k) {   // issue the k-th tile
-        const int b = k & 1;
-        if (k >= 2) mbar_wait_parity_sleep(&S.in_empty[b], ((k >> 1) - 1) & 1u);
-        const uint64_t nx = ahead;
-        issue(nx, b);
-        if (nx < ntiles) ahead = draw();
-        t = nx;
-      }
-    }
-    return;
-  }
-
-  if (warp == kCompute / 32 + 1) {
     // =========================== placement warp ===========================
     for (uint32_t kk = 0;; ++kk) {
       const int slot = kk % kSlots;
@@ -475,11 +464,9 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
       const RingRec r = S.rec[slot];
       if (r.ts == kDone) break;
       if (r.ts != kSelfPlaced) {
-        trace_tile(r.tile, 7);
         uint64_t es, ep;
         resolve6(out, r.tile, epoch, ntiles, r.ts, r.tp, &es, &ep);
-        if (es != ~0ull) copy_ring(S, out, r, slot, es, ep);
-        trace_tile(r.tile, 8);
+        if (es != ~0ull) copy_ring(S.sgn[slot], S.ring, out, r, es, ep);
       }
       __syncwarp();
       if (lane == 0) {
@@ -492,13 +479,37 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
   }
 
   // =========================== compute warps ===========================
+  // thread 0: tickets and TMA issue
+  auto draw_raw = [&]() -> uint64_t { return atom_add_relaxed(lw.ticket, 1); };
+  auto consume = [&](uint64_t t) {   // a drawn ticket: the CTA drawing the last one re-arms
+    if (t == last_draw) {
+      st_relaxed(lw.ticket, 0);
+      st_release(lw.epoch, epoch + 1);
+    }
+  };
+  auto issue = [&](uint64_t t) {     // tile t into S.in (or "no more tiles")
+    S.cur = t;
+    if (t < ntiles && kTma) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx(&S.full, kBufBytes);
+      tma_load_2d(S.in, &tmap, 0, static_cast<int>(t * TB), &S.full);
+    } else {
+      mbar_arrive(&S.full);
+    }
+  };
+  uint64_t ahead = ~0ull;   // thread 0: ticket in flight
+  if (tid == 0) {
+    const uint64_t t = draw_raw();
+    consume(t);
+    issue(t);
+    if (t < ntiles) ahead = draw_raw();
+  }
   uint32_t flags = 0;
   uint64_t head = 0;   // thread 0: ring bytes allocated
   for (uint32_t k = 0;; ++k) {
-    const int b = k & 1;
     const int slot = k % kSlots;
-    mbar_wait_parity(&S.full[b], (k >> 1) & 1u);
-    const uint64_t cur = S.cur[b];
+    mbar_wait_parity(&S.full, k & 1u);
+    const uint64_t cur = S.cur;
     if (cur >= ntiles) {
       // stop the placement warp
       if (k >= kSlots) mbar_wait_parity(&S.st_empty[slot], ((k / kSlots) - 1) & 1u);
@@ -509,10 +520,9 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
       mbar_arrive_warp(&S.st_full[slot]);
       break;
     }
-    unsigned char* in = S.in[b];
+    unsigned char* in = S.in;
     bool wide = false;
     uint32_t qb[K];
-    trace_tile(cur, 1);
     const uint64_t row0 = cur * TB;
     if (kTma) {
       // the partial last block is not covered by the tensor map (zero-filled)
@@ -533,7 +543,6 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
       }
       bar_sync_n(1, kCompute);
     }
-    trace_tile(cur, 2);
     // ---- quantize this thread's row ----------------------------------------
     {
       const unsigned char* row = in + tid * 128;
@@ -547,8 +556,6 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
         qb[4 * j + 3] = quant_f32(v.w, qf, bad);
       }
       if (__any_sync(kFull, bad)) {   // rare: an element inside the certificate margin
-        // in place in this thread's own row of the input buffer (nothing large
-        // may be live across the exact routine's call)
         uint32_t mask = 0;
 #pragma unroll
         for (int i = 0; i < K; ++i) {
@@ -571,8 +578,13 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
 #pragma unroll
         for (int i = 0; i < K; ++i) qb[i] = *reinterpret_cast<const uint32_t*>(in + swz_elem(tid, i));
       }
-      wide = bar_or_compute(wide);    // ... and every read of this input buffer is done
-      mbar_arrive_warp(&S.in_empty[b]);
+      wide = bar_or_compute(wide);    // ... and every read of the input buffer is done
+      if (tid == 0) {                 // refill it: the next tile's load overlaps this tile
+        const uint64_t nx = ahead;
+        consume(nx);
+        issue(nx);
+        if (nx < ntiles) ahead = draw_raw();
+      }
     }
     if (!wide) {
       const uint64_t gb = cur * TB + tid;
@@ -588,7 +600,6 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
       const uint32_t es = ex & 1023u, ep = ex >> 10;
       const uint32_t ts = tot & 1023u, tp = tot >> 10;
       if (tid == 0) lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
-      trace_tile(cur, 3);
       if (active) {
         out.widths[gb] = static_cast<uint8_t>(bc.w);
         out.outliers[gb] = static_cast<int32_t>(qb[0] - kMagicBits);
@@ -616,10 +627,8 @@ __global__ void __launch_bounds__(kThreadsWS, HSZ_ENC_CTAS)
         S.alloc_off = pos;
       }
       bar_sync_n(1, kCompute);
-      trace_tile(cur, 4);
       if (sb) S.sgn[slot][es >> 2] = bswap32(bc.sg);
       pack_block(bc, wmax, ep >> 2, reinterpret_cast<uint32_t*>(S.ring + S.alloc_off));
-      trace_tile(cur, 5);
       mbar_arrive_warp(&S.st_full[slot]);
     } else {
       // exact path: sizes and publish first; the tile then resolves and
