@@ -497,15 +497,18 @@ __global__ void __launch_bounds__(kThreadsC, HSZ_CMP_CTAS)
       mbar_arrive(&S.full);
     }
   };
-  uint64_t ahead = ~0ull;   // thread 0: ticket in flight
-  if (tid == 0) {
+  // warp 1 lane 0 (thread kTmaThread) owns tickets and TMA issue, thread 0 the
+  // aggregate publication and ring claims: the serial work of a tile is spread
+  constexpr int kTmaThread = 32;
+  uint64_t ahead = ~0ull;   // ticket in flight
+  if (tid == kTmaThread) {
     const uint64_t t = draw_raw();
     consume(t);
     issue(t);
     if (t < ntiles) ahead = draw_raw();
   }
   uint32_t flags = 0;
-  uint64_t head = 0;   // thread 0: ring bytes allocated
+  uint64_t head = 0;   // ring bytes allocated (identical in every compute thread)
   for (uint32_t k = 0;; ++k) {
     const int slot = k % kSlots;
     mbar_wait_parity(&S.full, k & 1u);
@@ -579,7 +582,7 @@ __global__ void __launch_bounds__(kThreadsC, HSZ_CMP_CTAS)
         for (int i = 0; i < K; ++i) qb[i] = *reinterpret_cast<const uint32_t*>(in + swz_elem(tid, i));
       }
       wide = bar_or_compute(wide);    // ... and every read of the input buffer is done
-      if (tid == 0) {                 // refill it: the next tile's load overlaps this tile
+      if (tid == kTmaThread) {        // refill it: the next tile's load overlaps this tile
         const uint64_t nx = ahead;
         consume(nx);
         issue(nx);
@@ -604,31 +607,33 @@ __global__ void __launch_bounds__(kThreadsC, HSZ_CMP_CTAS)
         out.widths[gb] = static_cast<uint8_t>(bc.w);
         out.outliers[gb] = static_cast<int32_t>(qb[0] - kMagicBits);
       }
-      // claim metadata slot k%4 and ring space for the packed payload
+      // claim metadata slot k%4 and ring space for the packed payload; every
+      // thread tracks the ring head itself (same tp on all threads), so no
+      // broadcast barrier is needed
       if (k >= kSlots) mbar_wait_parity(&S.st_empty[slot], ((k / kSlots) - 1) & 1u);
-      if (tid == 0) {
-        const uint32_t need = (tp + 127u) & ~127u;
-        uint32_t pos = static_cast<uint32_t>(head % kRingBytes);
-        if (pos + need > kRingBytes) {   // no wrap inside a tile: skip to the ring start
-          head += kRingBytes - pos;
-          pos = 0;
-        }
+      const uint32_t need = (tp + 127u) & ~127u;
+      uint32_t pos = static_cast<uint32_t>(head % kRingBytes);
+      if (pos + need > kRingBytes) {   // no wrap inside a tile: skip to the ring start
+        head += kRingBytes - pos;
+        pos = 0;
+      }
+      if (head + need - S.ring_tail > kRingBytes) {
         unsigned ns = 32;
         while (head + need - S.ring_tail > kRingBytes) {
           __nanosleep(ns);
           ns = ns < 256 ? ns * 2 : 256;
         }
-        head += need;
+      }
+      head += need;
+      if (tid == 0) {
         S.rec[slot].tile = cur;
         S.rec[slot].end = head;
         S.rec[slot].ts = ts;
         S.rec[slot].tp = tp;
         S.rec[slot].off = pos;
-        S.alloc_off = pos;
       }
-      bar_sync_n(1, kCompute);
       if (sb) S.sgn[slot][es >> 2] = bswap32(bc.sg);
-      pack_block(bc, wmax, ep >> 2, reinterpret_cast<uint32_t*>(S.ring + S.alloc_off));
+      pack_block(bc, wmax, ep >> 2, reinterpret_cast<uint32_t*>(S.ring + pos));
       mbar_arrive_warp(&S.st_full[slot]);
     } else {
       // exact path: sizes and publish first; the tile then resolves and
