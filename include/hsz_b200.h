@@ -151,6 +151,22 @@ int hsz_scalar_mul(const uint8_t* widths, const int32_t* outliers, const uint8_t
                    uint8_t* out_payload, uint64_t payload_cap, uint64_t* out_tile_offsets,
                    void* scratch, uint32_t* err, void* ws, uint64_t ws_bytes, void* stream);
 
+/* ---- K8: element-wise add / sub of two streams (ops.py:163-192) ----------
+ * out = a + b (sub = 0) or a - b (sub = 1); a and b share n / block_len /
+ * eps (the caller checks the params, ops.py:77-81).  Outliers combine in
+ * int64 under the int32 guard (HSZ_ERR_OUTLIER_OVERFLOW), signed residuals
+ * combine element by element, the result is re-encoded and placed by
+ * look-back.  `scratch` as sized by hsz_elementwise_scratch_size. */
+uint64_t hsz_elementwise_scratch_size(uint64_t n, uint32_t block_len);
+int hsz_elementwise(const uint8_t* a_widths, const int32_t* a_outliers, const uint8_t* a_signs,
+                    const uint8_t* a_payload, const uint64_t* a_tile_offsets,
+                    const uint8_t* b_widths, const int32_t* b_outliers, const uint8_t* b_signs,
+                    const uint8_t* b_payload, const uint64_t* b_tile_offsets, uint64_t n,
+                    uint32_t block_len, int sub, uint8_t* out_widths, int32_t* out_outliers,
+                    uint8_t* out_signs, uint64_t sign_cap, uint8_t* out_payload,
+                    uint64_t payload_cap, uint64_t* out_tile_offsets, void* scratch, uint32_t* err,
+                    void* ws, uint64_t ws_bytes, void* stream);
+
 /* ---- K7: exact moments (ops.py:249-357) -------------------------------------
  * out (device u64[5]) = S as signed 128-bit (lo, hi) and, if want_sq,
  * Q = sum(bins^2) as unsigned 192-bit (limb0, limb1, limb2).  The host

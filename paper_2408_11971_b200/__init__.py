@@ -39,6 +39,8 @@ from .ops import (
     ScalarBin,
     apply_reduction,
     apply_stream_op,
+    elementwise_add,
+    elementwise_sub,
     mean,
     negate,
     scalar_add,

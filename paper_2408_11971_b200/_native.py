@@ -51,6 +51,9 @@ SIGNATURES = {
     "hsz_scalar_add": (_int, [_vp, _vp, _u64, _i64, _vp, _vp]),
     "hsz_scalar_mul": (_int, [_vp, _vp, _vp, _vp, _vp, _u64, _u32, _dbl, _i64, _vp, _vp, _vp,
                               _u64, _vp, _u64, _vp, _vp, _vp, _vp, _u64, _vp]),
+    "hsz_elementwise_scratch_size": (_u64, [_u64, _u32]),
+    "hsz_elementwise": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _u64, _u32, _int,
+                               _vp, _vp, _vp, _u64, _vp, _u64, _vp, _vp, _vp, _vp, _u64, _vp]),
     "hsz_moments": (_int, [_vp, _vp, _vp, _vp, _vp, _u64, _u32, _int, _vp, _vp, _vp, _u64, _vp]),
     "hsz_copy_d2h": (_int, [_vp, _vp, _u64, _vp]),
     "hsz_stream_sync": (_int, [_vp]),

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "_lib")
-LIB = os.path.join(LIB_DIR, "libhsz_b200.so")
+LIB = os.environ.get("HSZ_B200_LIB") or os.path.join(LIB_DIR, "libhsz_b200.so")
 SOURCES = ["hsz_capi.cu"]
 HEADERS = ["hsz_common.cuh", "hsz_quant.cuh", "hsz_k32.cuh", "hsz_generic.cuh", "hsz_enc32.cuh", "hsz_dec32.cuh"]
 
@@ -47,7 +47,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]
+    extra = os.environ.get("HSZ_NVCC_EXTRA", "").split()   # experiments: -D knobs
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", LIB + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)

@@ -556,6 +556,20 @@ __global__ void quantize_kernel(const T* x, uint64_t n, QuantConst c, int64_t* b
 }  // namespace ops
 
 namespace ops {
+// element-wise combination sink: acc[e] = acc[e] (+|-) bin, modulo 2^64 --
+// the re-encoder's residuals bin[i] - bin[i-1] are then exactly the sums of
+// the operands' residuals (ops.py:171-176) whenever those fit 63 bits
+struct SinkCombineBins {
+  int64_t* acc;
+  int sub;
+  __device__ __forceinline__ void put(uint64_t e, int64_t bin, uint32_t*) const {
+    const uint64_t a = static_cast<uint64_t>(acc[e]);
+    acc[e] = static_cast<int64_t>(sub ? a - static_cast<uint64_t>(bin) : a + static_cast<uint64_t>(bin));
+  }
+};
+}  // namespace ops
+
+namespace ops {
 struct SinkAcc {
   k32::Acc acc;
   bool want_sq;
@@ -921,6 +935,38 @@ int hsz_scalar_mul(const uint8_t* widths, const int32_t* outliers, const uint8_t
   const gen::GStream s{widths, outliers, signs, payload, toff, n, k, nb};
   gen::decode_kernel<gen::SinkSmul><<<static_cast<unsigned>(nt), gen::kThreads, 0, st>>>(
       s, gen::SinkSmul{bins, rs, d}, err);
+  return launch_encode_generic(gen::GBins{bins}, n, k, ow, oo, os, sign_cap, op, payload_cap, otoff,
+                               err, ws, st);
+}
+
+uint64_t hsz_elementwise_scratch_size(uint64_t n, uint32_t k) { return k ? 8 * n : 0; }
+
+int hsz_elementwise(const uint8_t* wa, const int32_t* oa, const uint8_t* sa, const uint8_t* pa,
+                    const uint64_t* ta, const uint8_t* wb, const int32_t* ob, const uint8_t* sb,
+                    const uint8_t* pb, const uint64_t* tb, uint64_t n, uint32_t k, int sub,
+                    uint8_t* ow, int32_t* oo, uint8_t* os, uint64_t sign_cap, uint8_t* op,
+                    uint64_t payload_cap, uint64_t* otoff, void* scratch, uint32_t* err, void* ws,
+                    uint64_t ws_bytes, void* stream) {
+  if (!wa || !oa || !sa || !pa || !ta || !wb || !ob || !sb || !pb || !tb || !ow || !oo || !os ||
+      !op || !otoff || !err || !ws || !scratch || n == 0 || k == 0)
+    return HSZ_EINVAL;
+  if (ws_bytes < hsz_workspace_size(n, k)) return HSZ_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t nb = ceil_div(n, k);
+  const uint64_t nt = ceil_div(nb, kTileBlocks);
+  int64_t* bins = static_cast<int64_t*>(scratch);
+  // bins(a) (+|-) bins(b) modulo 2^64, then one re-encode: outliers a0 (+|-) b0
+  // under the int32 guard, residuals ra (+|-) rb
+  const gen::GStream A{wa, oa, sa, pa, ta, n, k, nb};
+  const gen::GStream B{wb, ob, sb, pb, tb, n, k, nb};
+  gen::decode_kernel<k32::SinkBins><<<static_cast<unsigned>(nt), gen::kThreads, 0, st>>>(
+      A, k32::SinkBins{bins}, err);
+  gen::decode_kernel<ops::SinkCombineBins><<<static_cast<unsigned>(nt), gen::kThreads, 0, st>>>(
+      B, ops::SinkCombineBins{bins, sub}, err);
+  if (k == 32) {
+    const k32::EncodeOut out{ow, oo, os, sign_cap, op, payload_cap, otoff, err, ws};
+    return launch_encode32(k32::SrcBins{bins, n}, out, n, st);
+  }
   return launch_encode_generic(gen::GBins{bins}, n, k, ow, oo, os, sign_cap, op, payload_cap, otoff,
                                err, ws, st);
 }

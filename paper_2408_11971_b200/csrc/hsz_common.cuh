@@ -84,7 +84,20 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 
+#ifndef HSZ_CMP_SLEEP_MAX
+#define HSZ_CMP_SLEEP_MAX 0
+#endif
+__device__ __forceinline__ bool mbar_test_parity(uint64_t* bar, uint32_t parity);
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+#if HSZ_CMP_SLEEP_MAX > 0
+  if (mbar_test_parity(bar, parity)) return;
+  unsigned ns = 16;
+  while (!mbar_test_parity(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < HSZ_CMP_SLEEP_MAX ? 2 * ns : HSZ_CMP_SLEEP_MAX;
+  }
+  return;
+#endif
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
@@ -94,16 +107,37 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
       : "memory");
 }
 
-// wait for a phase without hogging issue slots: try_wait with a suspend-time
-// hint parks the warp until the phase completes (or the hint elapses)
-__device__ __forceinline__ void mbar_wait_parity_sleep(uint64_t* bar, uint32_t parity) {
+// non-blocking probe of a phase
+__device__ __forceinline__ bool mbar_test_parity(uint64_t* bar, uint32_t parity) {
+  uint32_t r;
   asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAITS_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
-      "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(r)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+  return r != 0;
+}
+
+// service-warp wait (TMA issue, placement): poll with an exponential
+// nanosleep back-off.  A parked try_wait is woken by every mbarrier event of
+// the SM, so a waiting producer would otherwise spin through hundreds of
+// wake-ups per tile and steal issue slots from the compute warps.
+#ifndef HSZ_SVC_SLEEP_MAX
+#define HSZ_SVC_SLEEP_MAX 0
+#endif
+__device__ __forceinline__ void mbar_wait_parity_sleep(uint64_t* bar, uint32_t parity) {
+#if HSZ_SVC_SLEEP_MAX > 0
+  if (mbar_test_parity(bar, parity)) return;
+  unsigned ns = 32;
+  while (!mbar_test_parity(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < HSZ_SVC_SLEEP_MAX ? 2 * ns : HSZ_SVC_SLEEP_MAX;
+  }
+#else
+  mbar_wait_parity(bar, parity);
+#endif
 }
 
 // global -> shared bulk copy; dst/src 16-byte aligned, bytes % 16 == 0

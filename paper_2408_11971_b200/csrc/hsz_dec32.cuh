@@ -24,7 +24,10 @@ constexpr int K = 32;
 constexpr int TB = kTileBlocks;
 constexpr int kCompute = e32::kCompute;
 constexpr uint32_t kSignCap = TB * 4 + 32;   // staged sign bytes (+ 16-byte alignment slack)
-constexpr uint32_t kPayCap = 16384;          // staged payload bytes
+#ifndef HSZ_PAYCAP
+#define HSZ_PAYCAP 16384
+#endif
+constexpr uint32_t kPayCap = HSZ_PAYCAP;     // staged payload bytes
 constexpr int kFastW = 24;                   // register decode: widths <= 24, |outlier| < 2^29
 
 struct StreamIn {

@@ -7,6 +7,7 @@ ScalarBin           ops.py:51-74           (host: exact Python float/int)
 negate              ops.py:88-109          hsz_negate
 scalar_add / _sub   ops.py:112-125         hsz_scalar_add
 scalar_mul          ops.py:199-225         hsz_scalar_mul (fused decode/encode)
+elementwise_add/sub ops.py:163-192         hsz_elementwise
 mean                ops.py:360-363         hsz_moments + host finalize
 variance / stddev   ops.py:382-397         hsz_moments(want_sq) + finalize
 apply_stream_op     ops.py:520-538         dispatch
@@ -18,9 +19,10 @@ Q = sum(bins^2) (uint192) and the final float64 arithmetic is the
 reference's own Python expression on Python ints, so mean / variance are
 bit-identical to the reference, not merely within tolerance.
 
-The bivariate operations of the reference (elementwise add/sub, hadamard,
-covariance, ssim) are not on this hot path; the dispatch
-tables keep their names and report them as not implemented here.
+elementwise_add / elementwise_sub (ops.py:163-192) are the first of the
+bivariate operations.  The others (hadamard,
+covariance, ssim) are not on this hot path; the dispatch tables keep their
+names and report them as not implemented here.
 """
 
 from __future__ import annotations
@@ -33,7 +35,7 @@ import numpy as np
 from . import _native as N
 from .codec import _as_device_stream
 from .device import DeviceStream, ptr, run_encoder, torch
-from .errors import QuantOverflow
+from .errors import ParamsMismatch, QuantOverflow
 from .model import CompressedStream
 
 _I64_MAX = 2 ** 63 - 1
@@ -53,7 +55,7 @@ STREAM_OPS = {
 REDUCTIONS = {"mean": 1, "variance": 1, "stddev": 1, "covariance": 2, "ssim": 2}
 
 #: the subset implemented by this B200 hot path
-HOT_STREAM_OPS = ("neg", "sadd", "ssub", "smul")
+HOT_STREAM_OPS = ("neg", "sadd", "ssub", "smul", "eadd", "esub")
 HOT_REDUCTIONS = ("mean", "variance", "stddev")
 
 
@@ -128,6 +130,52 @@ def scalar_sub(c, s: float):
     """ops.py:121-125."""
     eps = c.params.eps
     return _shift_outliers(c, -ScalarBin.of(s, eps).bin, "scalar_sub")
+
+
+# ---------------------------------------------------------------------------
+# residual-space operations on two streams
+
+def _check_params(a, b):
+    """ops.py:77-81."""
+    if a.params != b.params:
+        raise ParamsMismatch(f"operand params differ: {a.params} vs {b.params}")
+
+
+def _elementwise(a, b, sub: bool, what: str):
+    """ops.py:163-182: outliers combine (int32 guard on the result), signed
+    residuals combine element by element, the result is re-encoded."""
+    _check_params(a, b)
+    da = _as_device_stream(a)
+    db = _as_device_stream(b)
+    ctx = da.ctx
+    lib = ctx.lib
+    p = da.params
+    n, k = p.element_count, p.block_len
+    wsp, wsb = ctx.workspace(n, k)
+    scratch_bytes = int(lib.hsz_elementwise_scratch_size(n, k))
+    scratch = ctx.empty(scratch_bytes, torch().uint8) if scratch_bytes else None
+    sp = ptr(scratch) if scratch is not None else None
+    wa, oa, sa, pa, ta = da.pointers()
+    wb, ob, sb, pb, tb = db.pointers()
+
+    def launch(ow, oo, os_, scap, op, pcap, otoff):
+        N.check(lib.hsz_elementwise(wa, oa, sa, pa, ta, wb, ob, sb, pb, tb, n, k, 1 if sub else 0,
+                                    ptr(ow), ptr(oo), ptr(os_), scap, ptr(op), pcap, ptr(otoff), sp,
+                                    ctx.err_ptr, wsp, wsb, ctx.handle), "hsz_elementwise")
+
+    out = run_encoder(ctx, p, launch)
+    return _finish(a, out, what)
+
+
+def elementwise_add(a, b, threads: int = 1):
+    """Per block: outliers add, signed residuals add; the result decompresses
+    to the exact sum of the operands' reconstructions (ops.py:185-188)."""
+    return _elementwise(a, b, False, "elementwise_add")
+
+
+def elementwise_sub(a, b, threads: int = 1):
+    """ops.py:191-192."""
+    return _elementwise(a, b, True, "elementwise_sub")
 
 
 # ---------------------------------------------------------------------------
@@ -233,6 +281,10 @@ def apply_stream_op(name: str, streams, scalar=None, threads: int = 1):
         return scalar_sub(streams[0], scalar)
     if name == "smul":
         return scalar_mul(streams[0], scalar, threads)
+    if name == "eadd":
+        return elementwise_add(streams[0], streams[1], threads)
+    if name == "esub":
+        return elementwise_sub(streams[0], streams[1], threads)
     raise NotImplementedError(f"stream op {name!r} is outside the B200 hot path "
                               f"(implemented: {', '.join(HOT_STREAM_OPS)})")
 
@@ -252,6 +304,7 @@ def apply_reduction(name: str, streams, threads: int = 1) -> float:
 
 __all__ = [
     "STREAM_OPS", "REDUCTIONS", "ScalarBin", "negate", "scalar_add", "scalar_sub", "scalar_mul",
+    "elementwise_add", "elementwise_sub",
     "mean", "variance", "stddev", "exact_moments", "apply_stream_op", "apply_reduction",
     "CompressedStream",
 ]

@@ -28,7 +28,8 @@ def lib():
 def test_header_declares_the_hot_path():
     names = _declared()
     for must in ("hsz_compress", "hsz_decode", "hsz_negate", "hsz_scalar_add", "hsz_scalar_mul",
-                 "hsz_moments", "hsz_minmax", "hsz_tile_offsets", "hsz_encode_bins"):
+                 "hsz_moments", "hsz_minmax", "hsz_tile_offsets", "hsz_encode_bins",
+                 "hsz_elementwise"):
         assert must in names
 
 

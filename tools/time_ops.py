@@ -88,6 +88,7 @@ def main():
         "mean": lambda: O.moments_device(z, False),
         "variance": lambda: O.moments_device(z, True),
         "decompress": lambda: H.decompress(z),
+        "elementwise_add": lambda: H.elementwise_add(s, z0),
     }
     if a.ops:
         fns = {k: v for k, v in fns.items() if k in a.ops.split(",")}
