@@ -608,6 +608,31 @@ __global__ void dequant_kernel(const int64_t* bins, uint64_t n, Sink sink, uint3
 using namespace hsz;
 
 // ===========================================================================
+// persistent re-encoding kernel (scalar multiply, element-wise add / sub):
+// one CTA per resident slot, tiles by ticket
+template <int kOp>
+static int launch_recode(const d32::StreamIn& a, const d32::StreamIn& b, const d32::SmulParams& sp,
+                         const k32::EncodeOut& out, uint64_t nt, cudaStream_t st) {
+  constexpr int smem = static_cast<int>(d32::recode_smem_bytes<kOp>());
+  auto kern = d32::recode_kernel<kOp>;
+  static int resident = 0, resident_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (resident_dev != dev) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, e32::kThreadsWS, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    resident = (per_sm > 0 ? per_sm : 1) * sms;
+    resident_dev = dev;
+  }
+  const uint64_t grid = nt < static_cast<uint64_t>(resident) ? nt : static_cast<uint64_t>(resident);
+  kern<<<static_cast<unsigned>(grid), e32::kThreadsWS, smem, st>>>(a, b, sp, out);
+  return launch_status();
+}
+
 extern "C" {
 
 const char* hsz_version(void) { return "hsz_b200 1.0 sm_100a"; }
@@ -912,23 +937,7 @@ int hsz_scalar_mul(const uint8_t* widths, const int32_t* outliers, const uint8_t
     sp.rsd = static_cast<double>(rs);
     sp.small_rs = (rs > -(1ll << 23) && rs < (1ll << 23)) ? 1 : 0;
     const k32::EncodeOut out{ow, oo, os, sign_cap, op, payload_cap, otoff, err, ws};
-    constexpr int smem = static_cast<int>(d32::kSmulSmemBytes);
-    static int resident = 0, resident_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (resident_dev != dev) {
-      cudaFuncSetAttribute(d32::smul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      cudaFuncSetAttribute(d32::smul_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           cudaSharedmemCarveoutMaxShared);
-      int per_sm = 0, sms = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d32::smul_kernel, e32::kThreadsWS, smem);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      resident = (per_sm > 0 ? per_sm : 1) * sms;
-      resident_dev = dev;
-    }
-    const uint64_t grid = nt < static_cast<uint64_t>(resident) ? nt : static_cast<uint64_t>(resident);
-    d32::smul_kernel<<<static_cast<unsigned>(grid), e32::kThreadsWS, smem, st>>>(in, sp, out);
-    return launch_status();
+    return launch_recode<d32::kOpSmul>(in, in, sp, out, nt, st);
   }
   if (!scratch) return HSZ_EINVAL;
   int64_t* bins = static_cast<int64_t*>(scratch);
@@ -939,7 +948,7 @@ int hsz_scalar_mul(const uint8_t* widths, const int32_t* outliers, const uint8_t
                                err, ws, st);
 }
 
-uint64_t hsz_elementwise_scratch_size(uint64_t n, uint32_t k) { return k ? 8 * n : 0; }
+uint64_t hsz_elementwise_scratch_size(uint64_t n, uint32_t k) { return (k && k != 32) ? 8 * n : 0; }
 
 int hsz_elementwise(const uint8_t* wa, const int32_t* oa, const uint8_t* sa, const uint8_t* pa,
                     const uint64_t* ta, const uint8_t* wb, const int32_t* ob, const uint8_t* sb,
@@ -948,12 +957,24 @@ int hsz_elementwise(const uint8_t* wa, const int32_t* oa, const uint8_t* sa, con
                     uint64_t payload_cap, uint64_t* otoff, void* scratch, uint32_t* err, void* ws,
                     uint64_t ws_bytes, void* stream) {
   if (!wa || !oa || !sa || !pa || !ta || !wb || !ob || !sb || !pb || !tb || !ow || !oo || !os ||
-      !op || !otoff || !err || !ws || !scratch || n == 0 || k == 0)
+      !op || !otoff || !err || !ws || n == 0 || k == 0)
     return HSZ_EINVAL;
   if (ws_bytes < hsz_workspace_size(n, k)) return HSZ_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t nb = ceil_div(n, k);
   const uint64_t nt = ceil_div(nb, kTileBlocks);
+  if (k == 32) {
+    // one fused pass: both operands' tiles staged, decoded into the same
+    // registers, re-encoded and placed by look-back
+    const uint32_t tl = tail_len_of(n, 32);
+    const d32::StreamIn A{wa, oa, sa, pa, ta, n, nb, nt, tl};
+    const d32::StreamIn B{wb, ob, sb, pb, tb, n, nb, nt, tl};
+    const d32::SmulParams sp{0, 0.0, 0.0, 0};
+    const k32::EncodeOut out{ow, oo, os, sign_cap, op, payload_cap, otoff, err, ws};
+    return sub ? launch_recode<d32::kOpSub>(A, B, sp, out, nt, st)
+               : launch_recode<d32::kOpAdd>(A, B, sp, out, nt, st);
+  }
+  if (!scratch) return HSZ_EINVAL;
   int64_t* bins = static_cast<int64_t*>(scratch);
   // bins(a) (+|-) bins(b) modulo 2^64, then one re-encode: outliers a0 (+|-) b0
   // under the int32 guard, residuals ra (+|-) rb

@@ -42,9 +42,11 @@ struct StreamIn {
   uint32_t tail_len;
 };
 
-struct InTile {
+template <uint32_t kCap>
+struct InTileT {
+  static constexpr uint32_t kPayBytes = kCap;
   alignas(16) unsigned char sgn[kSignCap];
-  alignas(16) unsigned char pay[kPayCap];
+  alignas(16) unsigned char pay[kCap];
   alignas(16) int32_t o[TB];
   alignas(16) uint8_t w[TB];
   uint64_t tile;       // >= ntiles: no more tiles
@@ -53,6 +55,7 @@ struct InTile {
   uint32_t poff;       // offset of that payload byte within pay[] (staged tiles)
   uint32_t staged;     // payload staged (else read in place from global memory)
 };
+using InTile = InTileT<kPayCap>;
 
 __device__ __forceinline__ void bulk_g2s_(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -74,7 +77,8 @@ __device__ __forceinline__ uint64_t prefetch_toff(const StreamIn& s, uint64_t t)
 // prefetched tile-offset entries.  Full tiles arrive by four bulk copies
 // (widths, outliers, sign bytes, payload bytes); the stream's last tile
 // loads its widths / outliers with plain loads.
-__device__ __forceinline__ void stage_tile(const StreamIn& s, uint64_t t, uint64_t tv, InTile& it,
+template <class IT>
+__device__ __forceinline__ void stage_tile(const StreamIn& s, uint64_t t, uint64_t tv, IT& it,
                                            uint64_t* bar) {
   const int lane = threadIdx.x & 31;
   if (t >= s.ntiles) {
@@ -110,7 +114,7 @@ __device__ __forceinline__ void stage_tile(const StreamIn& s, uint64_t t, uint64
     const uint64_t p_lo = p0 & ~15ull, p_hi = (p1 + 15) & ~15ull;
     const uint32_t sbytes = static_cast<uint32_t>(s_hi - s_lo);
     const uint32_t pbytes = static_cast<uint32_t>(p_hi - p_lo);
-    const bool staged = pbytes <= kPayCap && sbytes <= kSignCap;
+    const bool staged = pbytes <= IT::kPayBytes && sbytes <= kSignCap;
     it.tile = t;
     it.gs0 = s0;
     it.gp0 = p0;
@@ -138,7 +142,15 @@ __device__ __forceinline__ void stage_tile(const StreamIn& s, uint64_t t, uint64
 // int32 (|bin| < 2^30).  kFull: a full block (len == 32, no tail checks);
 // otherwise elements past `len` replicate the last live bin.  Fields are read
 // G at a time (G * w <= 32): one window refill check per G fields.
-template <bool kFull, int G>
+// kAcc: 0 q[i] = bin_i, 1 q[i] += bin_i, 2 q[i] -= bin_i (modulo 2^32)
+template <int kAcc>
+__device__ __forceinline__ void put_bin(int32_t& qi, int32_t v) {
+  if (kAcc == 0) qi = v;
+  else if (kAcc == 1) qi = static_cast<int32_t>(static_cast<uint32_t>(qi) + static_cast<uint32_t>(v));
+  else qi = static_cast<int32_t>(static_cast<uint32_t>(qi) - static_cast<uint32_t>(v));
+}
+
+template <bool kFull, int G, int kAcc = 0>
 __device__ __forceinline__ void decode_block_t(const unsigned char* sgn, const unsigned char* pay,
                                                uint32_t w, int32_t o, int len, int32_t (&q)[K]) {
   const uint32_t sw = bswap32(*reinterpret_cast<const uint32_t*>(sgn));
@@ -149,7 +161,7 @@ __device__ __forceinline__ void decode_block_t(const unsigned char* sgn, const u
   int nb = 0;   // valid bits at the bottom of win
   int wi = 0;
   int32_t P = o;
-  q[0] = o;
+  put_bin<kAcc>(q[0], o);
 #pragma unroll
   for (int c = 0; c < K / G; ++c) {
     if (nb < wg) {
@@ -166,39 +178,53 @@ __device__ __forceinline__ void decode_block_t(const unsigned char* sgn, const u
       int32_t d = (mag ^ neg) - neg;
       if (!kFull) d = (i < len) ? d : 0;
       P += d;
-      q[i] = P;
+      put_bin<kAcc>(q[i], P);
     }
   }
 }
 
 // all 32 lanes of the warp call this (the field grouping is warp-uniform)
+template <int kAcc = 0>
 __device__ __forceinline__ void decode_block(const unsigned char* sgn, const unsigned char* pay,
                                              uint32_t w, int32_t o, int len, int32_t (&q)[K]) {
   const uint32_t wmax = __reduce_max_sync(kFull, w);
   if (w == 0) {
 #pragma unroll
-    for (int i = 0; i < K; ++i) q[i] = o;
+    for (int i = 0; i < K; ++i) put_bin<kAcc>(q[i], o);
     return;
   }
   if (len != K) {
-    decode_block_t<false, 1>(sgn, pay, w, o, len, q);
+    decode_block_t<false, 1, kAcc>(sgn, pay, w, o, len, q);
   } else if (wmax <= 8) {
-    decode_block_t<true, 4>(sgn, pay, w, o, len, q);
+    decode_block_t<true, 4, kAcc>(sgn, pay, w, o, len, q);
   } else if (wmax <= 16) {
-    decode_block_t<true, 2>(sgn, pay, w, o, len, q);
+    decode_block_t<true, 2, kAcc>(sgn, pay, w, o, len, q);
   } else {
-    decode_block_t<true, 1>(sgn, pay, w, o, len, q);
+    decode_block_t<true, 1, kAcc>(sgn, pay, w, o, len, q);
   }
 }
 
 // ---------------------------------------------------------------------------
-// scalar multiply
+// re-encoding operations: scalar multiply (kOp 0) and element-wise add / sub
+// of two streams (kOp 1 / 2, ops.py:163-192) share one persistent kernel --
+// decode front (one or two staged input tiles), per-element transform in
+// registers, the encoder back half of hsz_enc32.cuh.
 
-struct SmulSmem {
-  InTile in;
-  unsigned char pk[2][e32::kBufBytes];
+constexpr int kOpSmul = 0, kOpAdd = 1, kOpSub = 2;
+constexpr uint32_t kEwPayCap = 8192;   // per operand (two staged tiles: 4 CTAs per SM)
+
+struct EmptyTile {};
+
+template <int kOp>
+struct RecodeSmem {
+  static constexpr bool kTwo = kOp != kOpSmul;
+  using Tile = InTileT<kTwo ? kEwPayCap : kPayCap>;
+  Tile in;
+  std::conditional_t<kTwo, Tile, EmptyTile> in2;   // second operand (element-wise ops)
+  alignas(16) unsigned char pk[2][e32::kBufBytes];
   alignas(16) uint32_t sgn[2][TB];
   uint32_t bes[TB], bep[TB];      // per-block offsets within the input tile (exact path)
+  uint32_t bes2[kTwo ? TB : 1], bep2[kTwo ? TB : 1];
   uint64_t bar, in_empty, st_full[2], st_empty[2];
   uint64_t excl_s[2], excl_p[2];
   uint32_t agg_ts[2], agg_tp[2];
@@ -207,6 +233,7 @@ struct SmulSmem {
   uint32_t scan[4];
   uint32_t wsb[4], wpb[4];
 };
+using SmulSmem = RecodeSmem<kOpSmul>;
 
 // exact (64/128-bit) bins of the output for the warp-per-block fallback: the
 // input block is decoded from global memory
@@ -225,7 +252,28 @@ struct SrcSmulExact {
   }
 };
 
-__device__ __forceinline__ void smul_copy_staged(SmulSmem& S, const k32::EncodeOut& out,
+// element-wise: bin_a (+|-) bin_b modulo 2^64 -- the fallback encoder's
+// residuals are then the operands' residual sums (ops.py:171-176)
+template <int kOp>
+struct SrcEwExact {
+  StreamIn a, b;
+  const RecodeSmem<kOp>* S;
+  __device__ __forceinline__ int64_t lane_bin(int lb, int lane, int len, uint32_t* flags) {
+    uint32_t f = 0;
+    const int64_t qa = k32::decode_lane(a.signs, a.payload, S->in.w[lb], S->in.o[lb],
+                                        S->in.gs0 + S->bes[lb], S->in.gp0 + S->bep[lb], len, lane, &f);
+    const int64_t qb = k32::decode_lane(b.signs, b.payload, S->in2.w[lb], S->in2.o[lb],
+                                        S->in2.gs0 + S->bes2[lb], S->in2.gp0 + S->bep2[lb], len,
+                                        lane, &f);
+    *flags |= f;
+    if (f || lane >= len) return 0;
+    const uint64_t ua = static_cast<uint64_t>(qa), ub = static_cast<uint64_t>(qb);
+    return static_cast<int64_t>(kOp == kOpSub ? ua - ub : ua + ub);
+  }
+};
+
+template <class SM>
+__device__ __forceinline__ void smul_copy_staged(SM& S, const k32::EncodeOut& out,
                                                  uint32_t ts, uint32_t tp, int par, uint32_t rank,
                                                  uint32_t nthr) {
   const uint64_t es = S.excl_s[par], ep = S.excl_p[par];
@@ -249,7 +297,8 @@ __device__ __forceinline__ void smul_copy_staged(SmulSmem& S, const k32::EncodeO
   if (rest < nw) dst[rest] = pbuf[e32::swz_word(rest)];
 }
 
-__device__ __forceinline__ void smul_resolve(SmulSmem& S, const k32::EncodeOut& out, uint64_t tile,
+template <class SM>
+__device__ __forceinline__ void smul_resolve(SM& S, const k32::EncodeOut& out, uint64_t tile,
                                              uint64_t epoch, uint64_t ntiles, uint32_t ts,
                                              uint32_t tp, int par) {
   const int lane = threadIdx.x & 31;
@@ -276,20 +325,35 @@ struct SmulParams {
   int small_rs;  // |rs| < 2^23: every register-path product is exact in float64
 };
 
+// in-tile (sign, payload) byte offsets of this thread's block: one CTA scan
+__device__ __forceinline__ void block_offsets(uint32_t w, int len, uint32_t* scan, uint32_t* es,
+                                              uint32_t* ep) {
+  const uint32_t isb = w ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
+  const uint32_t ipb = (static_cast<uint32_t>(len) * w + 7u) >> 3;
+  uint32_t itot;
+  const uint32_t iex = e32::cta_scan(isb | (ipb << 10), scan, &itot);
+  *es = iex & 1023u;
+  *ep = iex >> 10;
+}
+
 // Persistent, warp-specialised like the compressor: warps 0-3 decode +
-// rescale + code + pack, warp 4 stages input tiles, warp 5 places output
-// tiles (look-back + copy).
+// transform + code + pack, warp 4 stages input tiles (both operands' for the
+// element-wise ops, on one mbarrier), warp 5 places output tiles
+// (look-back + copy).
+template <int kOp>
 __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
-    smul_kernel(StreamIn in, SmulParams sp, k32::EncodeOut out) {
+    recode_kernel(StreamIn in, StreamIn in2, SmulParams sp, k32::EncodeOut out) {
+  constexpr bool kTwo = kOp != kOpSmul;
+  using SM = RecodeSmem<kOp>;
   extern __shared__ unsigned char smraw[];
   const uint32_t a0 = smem_u32(smraw);
-  SmulSmem& S = *reinterpret_cast<SmulSmem*>(smraw + (((a0 + 1023u) & ~1023u) - a0));
+  SM& S = *reinterpret_cast<SM*>(smraw + (((a0 + 1023u) & ~1023u) - a0));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t ntiles = in.ntiles, nblocks = in.nblocks;
   LookbackWs lw = LookbackWs::bind(out.ws, ntiles);
   const uint64_t last_draw = ntiles + gridDim.x - 1;
   if (tid == kCompute) {
-    mbar_init(&S.bar, 1);
+    mbar_init(&S.bar, kTwo ? 2 : 1);
     mbar_init(&S.in_empty, kCompute / 32);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&S.st_full[b], kCompute / 32);
@@ -319,14 +383,18 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
     t = __shfl_sync(kFull, t, 0);
     ahead = __shfl_sync(kFull, ahead, 0);
     stage_tile(in, t, prefetch_toff(in, t), S.in, &S.bar);
+    if constexpr (kTwo) stage_tile(in2, t, prefetch_toff(in2, t), S.in2, &S.bar);
     uint64_t tv = prefetch_toff(in, ahead);
+    uint64_t tv2 = kTwo ? prefetch_toff(in2, ahead) : 0ull;
     for (uint32_t k = 0; t < ntiles; ++k) {
       const uint64_t nx = ahead;
       if (lane == 0 && nx < ntiles) ahead = draw();
       ahead = __shfl_sync(kFull, ahead, 0);
       mbar_wait_parity_sleep(&S.in_empty, k & 1u);
       stage_tile(in, nx, tv, S.in, &S.bar);
+      if constexpr (kTwo) stage_tile(in2, nx, tv2, S.in2, &S.bar);
       tv = prefetch_toff(in, ahead);
+      if (kTwo) tv2 = prefetch_toff(in2, ahead);
       t = nx;
     }
     return;
@@ -372,39 +440,60 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
     const int len = !active ? 0 : (gb == nblocks - 1 ? static_cast<int>(in.tail_len) : K);
     uint32_t w = S.in.w[tid];
     const int32_t o = S.in.o[tid];
-    bool bad = w > 64;
-    if (bad) {
+    if (w > 64) {
       flags |= HSZ_ERR_BAD_WIDTH;
       w = 0;
     }
-    const uint32_t isb = w ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
-    const uint32_t ipb = (static_cast<uint32_t>(len) * w + 7u) >> 3;
-    uint32_t itot;
-    const uint32_t iex = e32::cta_scan(isb | (ipb << 10), S.scan, &itot);
-    const uint32_t ies = iex & 1023u, iep = iex >> 10;
+    uint32_t ies, iep;
+    block_offsets(w, len, S.scan, &ies, &iep);
     S.bes[tid] = ies;
     S.bep[tid] = iep;
-    const bool fast_in = S.in.staged && w <= static_cast<uint32_t>(kFastW) && o > -(1 << 29) && o < (1 << 29);
+    bool fast_in = S.in.staged && w <= static_cast<uint32_t>(kFastW) && o > -(1 << 29) && o < (1 << 29);
+    uint32_t w2 = 0, ies2 = 0, iep2 = 0;
+    int32_t o2 = 0;
+    if constexpr (kTwo) {
+      w2 = S.in2.w[tid];
+      o2 = S.in2.o[tid];
+      if (w2 > 64) {
+        flags |= HSZ_ERR_BAD_WIDTH;
+        w2 = 0;
+      }
+      block_offsets(w2, len, S.scan, &ies2, &iep2);
+      S.bes2[tid] = ies2;
+      S.bep2[tid] = iep2;
+      fast_in = fast_in && S.in2.staged && w2 <= static_cast<uint32_t>(kFastW) && o2 > -(1 << 29) &&
+                o2 < (1 << 29);
+    }
     // CTA-uniform: the register decode is warp-collective (decode_block)
-    bool exact = e32::bar_or_compute(!fast_in || !sp.small_rs);
+    bool exact = e32::bar_or_compute(!fast_in || (kOp == kOpSmul && !sp.small_rs));
     trace_tile(cur, 2);
     uint32_t qb[K];
     if (!exact) {
       int32_t q[K];
-      decode_block(S.in.sgn + S.in.soff + ies, S.in.pay + S.in.poff + iep, w, o, len, q);
-      // rescale: |bin| < 2^30, |rs| < 2^23 -> bin * rs exact in float64;
-      // then ops.py:199-208 verbatim
+      decode_block<0>(S.in.sgn + S.in.soff + ies, S.in.pay + S.in.poff + iep, w, o, len, q);
+      if constexpr (kOp == kOpSmul) {
+        // rescale: |bin| < 2^30, |rs| < 2^23 -> bin * rs exact in float64;
+        // then ops.py:199-208 verbatim
 #pragma unroll
-      for (int i = 0; i < K; ++i) {
-        const double pd = __dmul_rn(i32_to_double(q[i]), sp.rsd);
-        const double tt = __dmul_rn(sp.d, pd);
-        const double mag = floor(__dadd_rn(fabs(tt), 0.5));
-        exact |= !(mag < 1073741823.0);
-        const int32_t mi = __double2loint(__dadd_rn(mag, 6755399441055744.0));
-        qb[i] = static_cast<uint32_t>(tt < 0.0 ? -mi : mi);
+        for (int i = 0; i < K; ++i) {
+          const double pd = __dmul_rn(i32_to_double(q[i]), sp.rsd);
+          const double tt = __dmul_rn(sp.d, pd);
+          const double mag = floor(__dadd_rn(fabs(tt), 0.5));
+          exact |= !(mag < 1073741823.0);
+          const int32_t mi = __double2loint(__dadd_rn(mag, 6755399441055744.0));
+          qb[i] = static_cast<uint32_t>(tt < 0.0 ? -mi : mi);
+        }
+      } else {
+        // |bin_a|, |bin_b| < 2^30: the sum fits int32 and every residual
+        // sum fits 25 bits (the encoder's register path)
+        decode_block<kOp == kOpSub ? 2 : 1>(S.in2.sgn + S.in2.soff + ies2,
+                                             S.in2.pay + S.in2.poff + iep2, w2, o2, len, q);
+#pragma unroll
+        for (int i = 0; i < K; ++i) qb[i] = static_cast<uint32_t>(q[i]);
       }
     }
-    exact = e32::bar_or_compute(exact);   // ... every read of S.in's staged bytes is done
+    if (kOp == kOpSmul) exact = e32::bar_or_compute(exact);   // ... every read of S.in's staged bytes is done
+    else e32::bar_sync_n(1, kCompute);
     trace_tile(cur, 3);
     if (!exact) mbar_arrive_warp(&S.in_empty);
     if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);
@@ -436,8 +525,13 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
       trace_tile(cur, 5);
     } else {
       // exact warp-per-block path, decoding from global memory; places itself
-      SrcSmulExact src{in, &S, sp.rs, sp.d};
-      flags |= k32::fallback_sizes(src, out, cur, nblocks, in.tail_len, S.wsb, S.wpb);
+      if constexpr (kOp == kOpSmul) {
+        SrcSmulExact src{in, &S, sp.rs, sp.d};
+        flags |= k32::fallback_sizes(src, out, cur, nblocks, in.tail_len, S.wsb, S.wpb);
+      } else {
+        SrcEwExact<kOp> src{in, in2, &S};
+        flags |= k32::fallback_sizes(src, out, cur, nblocks, in.tail_len, S.wsb, S.wpb);
+      }
       e32::bar_sync_n(1, kCompute);
       ts = S.wsb[0] + S.wsb[1] + S.wsb[2] + S.wsb[3];
       tp = S.wpb[0] + S.wpb[1] + S.wpb[2] + S.wpb[3];
@@ -456,8 +550,15 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
           gs += S.wsb[i];
           gp += S.wpb[i];
         }
-        k32::fallback_pack(src, out, cur, nblocks, in.tail_len, gs, gp,
-                           reinterpret_cast<uint32_t*>(S.pk[par]) + warp * 64);
+        if constexpr (kOp == kOpSmul) {
+          SrcSmulExact src{in, &S, sp.rs, sp.d};
+          k32::fallback_pack(src, out, cur, nblocks, in.tail_len, gs, gp,
+                             reinterpret_cast<uint32_t*>(S.pk[par]) + warp * 64);
+        } else {
+          SrcEwExact<kOp> src{in, in2, &S};
+          k32::fallback_pack(src, out, cur, nblocks, in.tail_len, gs, gp,
+                             reinterpret_cast<uint32_t*>(S.pk[par]) + warp * 64);
+        }
       }
       e32::bar_sync_n(1, kCompute);
       mbar_arrive_warp(&S.in_empty);   // the per-block offsets in S.bes/bep are no longer needed
@@ -470,7 +571,9 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
   if (lane == 0 && flags) atomicOr(out.err, flags);
 }
 
-constexpr uint32_t kSmulSmemBytes = sizeof(SmulSmem) + 1024;
+template <int kOp>
+constexpr uint32_t recode_smem_bytes() { return sizeof(RecodeSmem<kOp>) + 1024; }
+constexpr uint32_t kSmulSmemBytes = recode_smem_bytes<kOpSmul>();
 
 // ---------------------------------------------------------------------------
 // Decode pipeline (moments, decompress to float32): persistent CTAs of 4
