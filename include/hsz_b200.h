@@ -182,6 +182,9 @@ int hsz_moments(const uint8_t* widths, const int32_t* outliers, const uint8_t* s
  * Used to fetch a reduction's limbs and the error word in one round trip. */
 int hsz_copy_d2h(void* host, const void* dev, uint64_t bytes, void* stream);
 int hsz_stream_sync(void* stream);
+/* copy + wait in one call: the round trip of a reduction whose result and
+ * error word share one small device record */
+int hsz_fetch(void* host, const void* dev, uint64_t bytes, void* stream);
 
 /* library identification (for the loader's sanity check) */
 const char* hsz_version(void);

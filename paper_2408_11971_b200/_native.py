@@ -57,6 +57,7 @@ SIGNATURES = {
     "hsz_moments": (_int, [_vp, _vp, _vp, _vp, _vp, _u64, _u32, _int, _vp, _vp, _vp, _u64, _vp]),
     "hsz_copy_d2h": (_int, [_vp, _vp, _u64, _vp]),
     "hsz_stream_sync": (_int, [_vp]),
+    "hsz_fetch": (_int, [_vp, _vp, _u64, _vp]),
 }
 
 _LIB = None

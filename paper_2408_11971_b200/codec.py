@@ -119,12 +119,11 @@ class RawArray:
         ctx = context()
         x = self.device_values(ctx)
         lib = ctx.lib
-        out = ctx.empty(2, torch().float64)
         wsp, wsb = ctx.workspace(1, 1)
         n = x.numel()
-        N.check(lib.hsz_minmax(ptr(x), DTYPE_CODE[self.dtype], n, ptr(out), ctx.err_ptr, wsp,
-                               wsb, ctx.handle), "hsz_minmax")
-        (mm,) = ctx.fetch_checked([out], "RawArray")
+        N.check(lib.hsz_minmax(x.data_ptr(), DTYPE_CODE[self.dtype], n, ctx.result_ptr,
+                               ctx.err_ptr, wsp, wsb, ctx.handle), "hsz_minmax")
+        mm = ctx.fetch_result(16, "RawArray").view(np.float64)
         lo, hi = float(mm[0]), float(mm[1])
         self._range = (lo, hi)
 
@@ -231,8 +230,8 @@ def compress_device(x, params: QuantParams, ctx=None) -> DeviceStream:
     code = DTYPE_CODE[params.dtype]
 
     def launch(w, o, s, scap, p, pcap, toff):
-        N.check(lib.hsz_compress(xp, code, n, k, params.eps, ptr(w), ptr(o), ptr(s), scap,
-                                 ptr(p), pcap, ptr(toff), ctx.err_ptr, wsp, wsb, ctx.handle),
+        N.check(lib.hsz_compress(xp, code, n, k, params.eps, w, o, s, scap,
+                                 p, pcap, toff, ctx.err_ptr, wsp, wsb, ctx.handle),
                 "hsz_compress")
 
     return run_encoder(ctx, params, launch)
@@ -295,8 +294,8 @@ def encode_from_quant(q: QuantArray, threads: int = 1):
     lib = ctx.lib
 
     def launch(w, o, s, scap, py, pcap, toff):
-        N.check(lib.hsz_encode_bins(ptr(bins), n, k, ptr(w), ptr(o), ptr(s), scap, ptr(py), pcap,
-                                    ptr(toff), ctx.err_ptr, wsp, wsb, ctx.handle),
+        N.check(lib.hsz_encode_bins(ptr(bins), n, k, w, o, s, scap, py, pcap,
+                                    toff, ctx.err_ptr, wsp, wsb, ctx.handle),
                 "hsz_encode_bins")
 
     ds = run_encoder(ctx, p, launch)

@@ -697,6 +697,12 @@ int hsz_copy_d2h(void* host, const void* dev, uint64_t bytes, void* stream) {
              : HSZ_ECUDA;
 }
 
+int hsz_fetch(void* host, const void* dev, uint64_t bytes, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess) return HSZ_ECUDA;
+  return cudaStreamSynchronize(st) == cudaSuccess ? HSZ_OK : HSZ_ECUDA;
+}
+
 int hsz_stream_sync(void* stream) {
   return cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) == cudaSuccess ? HSZ_OK : HSZ_ECUDA;
 }

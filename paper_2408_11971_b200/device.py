@@ -89,9 +89,16 @@ class Context:
         self.ws_bytes = 0
         self.ws_uses = 0
         with t.cuda.device(self.device):
-            self.err = t.zeros(4, dtype=t.int32, device=self.device)
-        self.err_ptr = ptr(self.err)
+            # one small device record: [0, 16) the sticky error word(s),
+            # [16, 64) the result slot of value-range / moment reductions, so a
+            # reduction comes back with its error word in ONE copy
+            self.small = t.zeros(8, dtype=t.int64, device=self.device)
+        self.err = self.small[:2].view(t.int32)
+        self.err_ptr = self.small.data_ptr()
+        self.result_ptr = self.err_ptr + 16
         self._scratch = t.empty(1 << 12, dtype=t.uint8, pin_memory=True)   # small fetches
+        self._scratch_np = self._scratch.numpy()
+        self._scratch_ptr = self._scratch.data_ptr()
 
     def workspace(self, n: int, k: int):
         need = geometry(n, k)[3]
@@ -124,6 +131,20 @@ class Context:
 
     def check(self, what: str = "") -> None:
         raise_for_flags(self.read_flags(), what)
+
+    def fetch_result(self, nbytes: int, what: str = ""):
+        """Wait for the result slot (``result_ptr``, ``nbytes`` <= 48) and the
+        error word: one copy + synchronize; raise the reference's exception
+        for a set error word.  Returns a numpy uint8 copy of the result."""
+        N.check(self.lib.hsz_fetch(self._scratch_ptr, self.err_ptr, 16 + nbytes, self.handle),
+                "fetch")
+        host = self._scratch_np
+        flags = int(host[:4].view(np.int32)[0])
+        if flags:
+            self.err.zero_()
+            self.stream.synchronize()
+            raise_for_flags(flags, what)
+        return host[16:16 + nbytes].copy()
 
     def fetch_checked(self, tensors, what: str = ""):
         """Download (small) `tensors` together with the sticky error word in
@@ -201,23 +222,48 @@ def payload_capacity(lib, n: int, k: int) -> int:
 
 
 class DeviceStream:
-    """A compressed stream resident in HBM (see module docstring)."""
+    """A compressed stream resident in HBM (see module docstring).
 
-    __slots__ = ("params", "widths", "outliers", "signs", "payload", "toff", "ctx",
-                 "sign_cap", "payload_cap", "_totals")
+    Sections are held as (base tensor, byte offset, bytes, dtype) and
+    materialised as torch views only when asked for (``widths`` ...); the
+    launch path works on raw pointers (base pointer + offset), so an op costs
+    one device allocation and no tensor slicing on the host."""
+
+    __slots__ = ("params", "_sec", "_views", "ctx", "sign_cap", "payload_cap", "_totals", "_ptrs")
+
+    _NAMES = ("widths", "outliers", "signs", "payload", "toff")
 
     def __init__(self, params: QuantParams, widths, outliers, signs, payload, toff, ctx: Context,
                  sign_cap: int, payload_cap: int):
         self.params = params
-        self.widths = widths
-        self.outliers = outliers
-        self.signs = signs
-        self.payload = payload
-        self.toff = toff
+        secs = (widths, outliers, signs, payload, toff)
+        self._sec = secs
+        self._views = [x if not isinstance(x, tuple) else None for x in secs]
         self.ctx = ctx
         self.sign_cap = int(sign_cap)
         self.payload_cap = int(payload_cap)
         self._totals = None
+        self._ptrs = None
+
+    def section(self, i):
+        """Section i as an aliasable descriptor (tensor or (base, off, bytes, dtype))."""
+        return self._sec[i]
+
+    def _view(self, i):
+        v = self._views[i]
+        if v is None:
+            base, off, nb, dt = self._sec[i]
+            v = base[off:off + nb]
+            if dt is not None:
+                v = v.view(dt)
+            self._views[i] = v
+        return v
+
+    widths = property(lambda self: self._view(0))
+    outliers = property(lambda self: self._view(1))
+    signs = property(lambda self: self._view(2))
+    payload = property(lambda self: self._view(3))
+    toff = property(lambda self: self._view(4))
 
     # -- geometry ---------------------------------------------------------
     @property
@@ -233,8 +279,10 @@ class DeviceStream:
         return geometry(self.n, self.k)[0]
 
     def pointers(self):
-        return (ptr(self.widths), ptr(self.outliers), ptr(self.signs), ptr(self.payload),
-                ptr(self.toff))
+        if self._ptrs is None:
+            self._ptrs = tuple((x[0].data_ptr() + x[1]) if isinstance(x, tuple) else x.data_ptr()
+                               for x in self._sec)
+        return self._ptrs
 
     # -- host materialisation ------------------------------------------------
     def check(self) -> "DeviceStream":
@@ -377,7 +425,8 @@ def download_into(tensors, arena, ctx: Context = None):
 
 def new_stream_buffers(ctx: Context, params: QuantParams, payload_cap: int = None):
     """Allocate output sections for an encoder writing `params`-shaped data:
-    ONE device allocation carved into 256-byte aligned sections."""
+    ONE device allocation carved into 256-byte aligned sections (returned as
+    section descriptors; no views are made here)."""
     t = torch()
     n, k = params.element_count, params.block_len
     B = params.block_count
@@ -388,27 +437,29 @@ def new_stream_buffers(ctx: Context, params: QuantParams, payload_cap: int = Non
     def up(v):
         return (v + 255) & ~255
 
-    o_w, o_o = 0, up(B)
+    o_o = up(B)
     o_s = o_o + up(4 * B)
     o_p = o_s + up(scap + N.HSZ_SECTION_SLACK)
     o_t = o_p + up(pcap + N.HSZ_SECTION_SLACK)
     total = o_t + 16 * (T + 1)
     buf = ctx.empty(total, t.uint8)
-    widths = buf[o_w:o_w + B]
-    outliers = buf[o_o:o_o + 4 * B].view(t.int32)
-    signs = buf[o_s:o_s + scap + N.HSZ_SECTION_SLACK]
-    payload = buf[o_p:o_p + pcap + N.HSZ_SECTION_SLACK]
-    toff = buf[o_t:o_t + 16 * (T + 1)].view(t.int64)
-    return widths, outliers, signs, payload, toff, scap, pcap
+    secs = ((buf, 0, B, None), (buf, o_o, 4 * B, t.int32),
+            (buf, o_s, scap + N.HSZ_SECTION_SLACK, None),
+            (buf, o_p, pcap + N.HSZ_SECTION_SLACK, None), (buf, o_t, 16 * (T + 1), t.int64))
+    base = buf.data_ptr()
+    ptrs = (base, base + o_o, base + o_s, base + o_p, base + o_t)
+    return secs, ptrs, scap, pcap
 
 
 def run_encoder(ctx: Context, params: QuantParams, launch) -> DeviceStream:
-    """Run an encoder launch(widths, outliers, signs, scap, payload, pcap, toff);
-    retry once with the exact payload size if the capacity policy undershot."""
+    """Run an encoder launch(widths, outliers, signs, scap, payload, pcap, toff)
+    (device pointers); retry once with the exact payload size if the
+    capacity policy undershot."""
     n, k = params.element_count, params.block_len
-    w, o, s, p, toff, scap, pcap = new_stream_buffers(ctx, params)
+    secs, (w, o, s, p, toff), scap, pcap = new_stream_buffers(ctx, params)
     launch(w, o, s, scap, p, pcap, toff)
-    ds = DeviceStream(params, w, o, s, p, toff, ctx, scap, pcap)
+    ds = DeviceStream(params, *secs, ctx, scap, pcap)
+    ds._ptrs = (w, o, s, p, toff)
     if pcap >= geometry(n, k)[2]:
         return ds                       # overflow impossible: stay asynchronous
     flags = ctx.read_flags()
@@ -416,10 +467,11 @@ def run_encoder(ctx: Context, params: QuantParams, launch) -> DeviceStream:
         raise_for_flags(flags & ~(1 << 6))
     if flags & (1 << 6):
         T = geometry(n, k)[0]
-        need = int(toff[2 * T + 1].item())
-        w, o, s, p, toff, scap, pcap = new_stream_buffers(ctx, params, payload_cap=need)
+        need = int(ds.toff[2 * T + 1].item())
+        secs, (w, o, s, p, toff), scap, pcap = new_stream_buffers(ctx, params, payload_cap=need)
         launch(w, o, s, scap, p, pcap, toff)
-        ds = DeviceStream(params, w, o, s, p, toff, ctx, scap, pcap)
+        ds = DeviceStream(params, *secs, ctx, scap, pcap)
+        ds._ptrs = (w, o, s, p, toff)
         flags = ctx.read_flags()
         if flags:
             if flags & (1 << 6):

@@ -95,14 +95,18 @@ def negate(c):
     ds = _as_device_stream(c)
     ctx = ds.ctx
     t = torch()
-    outl = ctx.empty(ds.outliers.numel(), t.int32)
-    signs = ctx.empty(ds.signs.numel(), t.uint8)
     p = ds.params
-    N.check(ctx.lib.hsz_negate(ptr(ds.widths), ptr(ds.outliers), ptr(outl), ptr(ds.signs),
-                               ptr(signs), ptr(ds.toff), p.element_count, p.block_len,
+    B = p.block_count
+    ns = ds.sign_cap + N.HSZ_SECTION_SLACK
+    o_s = (4 * B + 255) & ~255
+    buf = ctx.empty(o_s + ns, t.uint8)              # one allocation: outliers | signs
+    base = buf.data_ptr()
+    w, o, sg, py, toff = ds.pointers()
+    N.check(ctx.lib.hsz_negate(w, o, base, sg, base + o_s, toff, p.element_count, p.block_len,
                                ctx.err_ptr, ctx.handle), "hsz_negate")
-    out = DeviceStream(p, ds.widths, outl, signs, ds.payload, ds.toff, ctx, ds.sign_cap,
-                       ds.payload_cap)
+    out = DeviceStream(p, ds.section(0), (buf, 0, 4 * B, t.int32), (buf, o_s, ns, None),
+                       ds.section(3), ds.section(4), ctx, ds.sign_cap, ds.payload_cap)
+    out._ptrs = (w, base, base + o_s, py, toff)
     out._totals = ds._totals
     return _finish(c, out, "negate")
 
@@ -111,11 +115,14 @@ def _shift_outliers(c, rs: int, what: str):
     ds = _as_device_stream(c)
     ctx = ds.ctx
     t = torch()
-    outl = ctx.empty(ds.outliers.numel(), t.int32)
-    N.check(ctx.lib.hsz_scalar_add(ptr(ds.outliers), ptr(outl), ds.params.block_count, rs,
-                                   ctx.err_ptr, ctx.handle), "hsz_scalar_add")
-    out = DeviceStream(ds.params, ds.widths, outl, ds.signs, ds.payload, ds.toff, ctx,
-                       ds.sign_cap, ds.payload_cap)
+    B = ds.params.block_count
+    outl = ctx.empty(B, t.int32)
+    w, o, sg, py, toff = ds.pointers()
+    po = outl.data_ptr()
+    N.check(ctx.lib.hsz_scalar_add(o, po, B, rs, ctx.err_ptr, ctx.handle), "hsz_scalar_add")
+    out = DeviceStream(ds.params, ds.section(0), outl, ds.section(2), ds.section(3), ds.section(4),
+                       ctx, ds.sign_cap, ds.payload_cap)
+    out._ptrs = (w, po, sg, py, toff)
     out._totals = ds._totals
     return _finish(c, out, what)
 
@@ -160,7 +167,7 @@ def _elementwise(a, b, sub: bool, what: str):
 
     def launch(ow, oo, os_, scap, op, pcap, otoff):
         N.check(lib.hsz_elementwise(wa, oa, sa, pa, ta, wb, ob, sb, pb, tb, n, k, 1 if sub else 0,
-                                    ptr(ow), ptr(oo), ptr(os_), scap, ptr(op), pcap, ptr(otoff), sp,
+                                    ow, oo, os_, scap, op, pcap, otoff, sp,
                                     ctx.err_ptr, wsp, wsb, ctx.handle), "hsz_elementwise")
 
     out = run_encoder(ctx, p, launch)
@@ -197,8 +204,8 @@ def scalar_mul(c, s: float, threads: int = 1):
     w, o, sg, py, toff = ds.pointers()
 
     def launch(ow, oo, os_, scap, op, pcap, otoff):
-        N.check(lib.hsz_scalar_mul(w, o, sg, py, toff, n, k, p.eps, rs, ptr(ow), ptr(oo),
-                                   ptr(os_), scap, ptr(op), pcap, ptr(otoff), sp, ctx.err_ptr,
+        N.check(lib.hsz_scalar_mul(w, o, sg, py, toff, n, k, p.eps, rs, ow, oo,
+                                   os_, scap, op, pcap, otoff, sp, ctx.err_ptr,
                                    wsp, wsb, ctx.handle), "hsz_scalar_mul")
 
     out = run_encoder(ctx, p, launch)
@@ -234,9 +241,14 @@ def unpack_moments(limbs) -> tuple:
 def exact_moments(c, want_sq: bool = True):
     """Exact (sum(bins), sum(bins^2)) of a stream (ops.py:313-357)."""
     ds = _as_device_stream(c)
-    out = moments_device(ds, want_sq)
-    (limbs,) = ds.ctx.fetch_checked([out], "moments")
-    return unpack_moments(limbs)
+    ctx = ds.ctx
+    p = ds.params
+    n, k = p.element_count, p.block_len
+    wsp, wsb = ctx.workspace(n, k)
+    w, o, sg, py, toff = ds.pointers()
+    N.check(ctx.lib.hsz_moments(w, o, sg, py, toff, n, k, 1 if want_sq else 0, ctx.result_ptr,
+                                ctx.err_ptr, wsp, wsb, ctx.handle), "hsz_moments")
+    return unpack_moments(ctx.fetch_result(40, "moments").view(np.uint64))
 
 
 def mean_from(S: int, n: int, eps: float) -> float:
