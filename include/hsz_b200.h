@@ -186,6 +186,21 @@ int hsz_stream_sync(void* stream);
  * error word share one small device record */
 int hsz_fetch(void* host, const void* dev, uint64_t bytes, void* stream);
 
+/* Host-mapped mailbox variants of the two reductions the host waits on:
+ * `mailbox` = pinned host memory (u64[8], device-accessible through UVA);
+ * the kernel's last CTA writes [1..nres] = the result words (minmax: 2 f64
+ * bit patterns, moments: the 5 u64 limbs), [1 + nres] = the error word, then
+ * [0] = seq.  hsz_mailbox_wait polls word 0 for `seq`; it returns HSZ_OK,
+ * HSZ_ECUDA (the stream faulted) or HSZ_EINVAL (the stream drained without
+ * a post -- fetch with hsz_fetch instead). */
+int hsz_minmax_mb(const void* x, int dtype, uint64_t n, double* minmax, uint32_t* err, void* ws,
+                  uint64_t ws_bytes, uint64_t* mailbox, uint64_t seq, void* stream);
+int hsz_moments_mb(const uint8_t* widths, const int32_t* outliers, const uint8_t* signs,
+                   const uint8_t* payload, const uint64_t* tile_offsets, uint64_t n,
+                   uint32_t block_len, int want_sq, uint64_t* out, uint32_t* err, void* ws,
+                   uint64_t ws_bytes, uint64_t* mailbox, uint64_t seq, void* stream);
+int hsz_mailbox_wait(const uint64_t* mailbox, uint64_t seq, void* stream);
+
 /* library identification (for the loader's sanity check) */
 const char* hsz_version(void);
 

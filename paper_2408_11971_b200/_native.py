@@ -14,6 +14,8 @@ import os
 from . import build as _build
 
 HSZ_OK = 0
+HSZ_EINVAL = -1
+HSZ_ECUDA = -2
 HSZ_F32, HSZ_F64 = 0, 1
 HSZ_OUT_F32, HSZ_OUT_F64, HSZ_OUT_BINS = 0, 1, 2
 HSZ_TILE_BLOCKS = 128
@@ -58,6 +60,10 @@ SIGNATURES = {
     "hsz_copy_d2h": (_int, [_vp, _vp, _u64, _vp]),
     "hsz_stream_sync": (_int, [_vp]),
     "hsz_fetch": (_int, [_vp, _vp, _u64, _vp]),
+    "hsz_minmax_mb": (_int, [_vp, _int, _u64, _vp, _vp, _vp, _u64, _vp, _u64, _vp]),
+    "hsz_moments_mb": (_int, [_vp, _vp, _vp, _vp, _vp, _u64, _u32, _int, _vp, _vp, _vp, _u64, _vp,
+                              _u64, _vp]),
+    "hsz_mailbox_wait": (_int, [_vp, _u64, _vp]),
 }
 
 _LIB = None

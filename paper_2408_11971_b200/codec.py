@@ -121,9 +121,11 @@ class RawArray:
         lib = ctx.lib
         wsp, wsb = ctx.workspace(1, 1)
         n = x.numel()
-        N.check(lib.hsz_minmax(x.data_ptr(), DTYPE_CODE[self.dtype], n, ctx.result_ptr,
-                               ctx.err_ptr, wsp, wsb, ctx.handle), "hsz_minmax")
-        mm = ctx.fetch_result(16, "RawArray").view(np.float64)
+        seq = ctx.next_seq()
+        N.check(lib.hsz_minmax_mb(x.data_ptr(), DTYPE_CODE[self.dtype], n, ctx.result_ptr,
+                                  ctx.err_ptr, wsp, wsb, ctx.mailbox_ptr, seq, ctx.handle),
+                "hsz_minmax")
+        mm = ctx.mailbox_result(seq, 2, "RawArray").view(np.float64)
         lo, hi = float(mm[0]), float(mm[1])
         self._range = (lo, hi)
 

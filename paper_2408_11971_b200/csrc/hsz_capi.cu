@@ -135,7 +135,8 @@ __global__ void __launch_bounds__(kThreads) minmax_kernel(const T* x, uint64_t n
 #endif
 constexpr int kMmThreads = HSZ_MM_THREADS;
 __global__ void __launch_bounds__(kMmThreads) minmax_f32_kernel(const float* __restrict__ x, uint64_t n,
-                                                                double* out, uint32_t* err, void* ws) {
+                                                                double* out, uint32_t* err, void* ws,
+                                                                Mailbox mb) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t nv = n / 4;
@@ -220,6 +221,9 @@ __global__ void __launch_bounds__(kMmThreads) minmax_f32_kernel(const float* __r
   out[0] = lo;
   out[1] = hi;
   st_relaxed(done, 0);
+  const uint64_t res[2] = {static_cast<uint64_t>(__double_as_longlong(lo)),
+                           static_cast<uint64_t>(__double_as_longlong(hi))};
+  mailbox_post(mb, res, 2, err);
 }
 
 // ---- K4 for block_len 32: every stored sign byte flips (full blocks have 4
@@ -456,7 +460,7 @@ static bool make_rows_map_f32(const float* x, uint64_t n, CUtensorMap* map) {
 
 template <int kMode>
 static int launch_decode_pipe(const d32::StreamIn& in, float* out, double d, uint64_t* mout,
-                              void* ws, uint32_t* err, cudaStream_t st) {
+                              void* ws, uint32_t* err, cudaStream_t st, Mailbox mb = Mailbox{nullptr, 0}) {
   CUtensorMap map;
   std::memset(&map, 0, sizeof(map));
   int use_tma = 0;
@@ -478,7 +482,7 @@ static int launch_decode_pipe(const d32::StreamIn& in, float* out, double d, uin
   }
   const uint64_t grid = in.ntiles < static_cast<uint64_t>(resident) ? in.ntiles : static_cast<uint64_t>(resident);
   const d32::DecF32Sink fs{out, d, d * 0x1p33 >= 3.4028234663852886e38};
-  const d32::MomentsSink ms{mout, ws};
+  const d32::MomentsSink ms{mout, ws, mb};
   kern<<<static_cast<unsigned>(grid), d32::kDecThreads, smem, st>>>(map, in, fs, ms, use_tma, err);
   return launch_status();
 }
@@ -633,6 +637,17 @@ static int launch_recode(const d32::StreamIn& a, const d32::StreamIn& b, const d
   return launch_status();
 }
 
+namespace hsz {
+namespace ops {
+// mailbox post for reduction paths that do not post in-kernel
+__global__ void mailbox_post_kernel(Mailbox mb, const uint64_t* res, int nres, const uint32_t* err) {
+  uint64_t r[5];
+  for (int i = 0; i < nres; ++i) r[i] = res[i];
+  mailbox_post(mb, r, nres, err);
+}
+}  // namespace ops
+}  // namespace hsz
+
 extern "C" {
 
 const char* hsz_version(void) { return "hsz_b200 1.0 sm_100a"; }
@@ -738,22 +753,33 @@ int hsz_workspace_init(void* ws, uint64_t ws_bytes, void* stream) {
 
 uint64_t hsz_scalar_mul_scratch_size(uint64_t n, uint32_t k) { return k == 32 ? 0 : 8 * n; }
 
-int hsz_minmax(const void* x, int dtype, uint64_t n, double* minmax, uint32_t* err, void* ws,
-               uint64_t ws_bytes, void* stream) {
+int hsz_minmax_mb(const void* x, int dtype, uint64_t n, double* minmax, uint32_t* err, void* ws,
+                  uint64_t ws_bytes, uint64_t* mailbox, uint64_t seq, void* stream) {
   if (!x || !minmax || !err || !ws || n == 0) return HSZ_EINVAL;
   if (ws_bytes < 8 * kWsFlagsOff) return HSZ_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const unsigned g = static_cast<unsigned>(grid_for(n, dtype == HSZ_F32 ? 16 : 8, ops::kThreads, ops::kMinmaxCtas));
   if (dtype == HSZ_F32 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0) {
     const unsigned g2 = static_cast<unsigned>(grid_for(n, 32, ops::kMmThreads, ops::kMinmaxCtas));
-    ops::minmax_f32_kernel<<<g2, ops::kMmThreads, 0, st>>>(static_cast<const float*>(x), n, minmax, err, ws);
-  } else if (dtype == HSZ_F32)
-    ops::minmax_kernel<float><<<g, ops::kThreads, 0, st>>>(static_cast<const float*>(x), n, minmax, err, ws);
-  else if (dtype == HSZ_F64)
-    ops::minmax_kernel<double><<<g, ops::kThreads, 0, st>>>(static_cast<const double*>(x), n, minmax, err, ws);
-  else
-    return HSZ_EINVAL;
+    ops::minmax_f32_kernel<<<g2, ops::kMmThreads, 0, st>>>(static_cast<const float*>(x), n, minmax, err, ws,
+                                                           Mailbox{mailbox, seq});
+  } else {
+    if (dtype == HSZ_F32)
+      ops::minmax_kernel<float><<<g, ops::kThreads, 0, st>>>(static_cast<const float*>(x), n, minmax, err, ws);
+    else if (dtype == HSZ_F64)
+      ops::minmax_kernel<double><<<g, ops::kThreads, 0, st>>>(static_cast<const double*>(x), n, minmax, err, ws);
+    else
+      return HSZ_EINVAL;
+    if (mailbox)
+      ops::mailbox_post_kernel<<<1, 1, 0, st>>>(Mailbox{mailbox, seq},
+                                                reinterpret_cast<const uint64_t*>(minmax), 2, err);
+  }
   return launch_status();
+}
+
+int hsz_minmax(const void* x, int dtype, uint64_t n, double* minmax, uint32_t* err, void* ws,
+               uint64_t ws_bytes, void* stream) {
+  return hsz_minmax_mb(x, dtype, n, minmax, err, ws, ws_bytes, nullptr, 0, stream);
 }
 
 int hsz_compress(const void* x, int dtype, uint64_t n, uint32_t k, double eps, uint8_t* widths,
@@ -998,9 +1024,10 @@ int hsz_elementwise(const uint8_t* wa, const int32_t* oa, const uint8_t* sa, con
                                err, ws, st);
 }
 
-int hsz_moments(const uint8_t* widths, const int32_t* outliers, const uint8_t* signs,
-                const uint8_t* payload, const uint64_t* toff, uint64_t n, uint32_t k, int want_sq,
-                uint64_t* out, uint32_t* err, void* ws, uint64_t ws_bytes, void* stream) {
+int hsz_moments_mb(const uint8_t* widths, const int32_t* outliers, const uint8_t* signs,
+                   const uint8_t* payload, const uint64_t* toff, uint64_t n, uint32_t k, int want_sq,
+                   uint64_t* out, uint32_t* err, void* ws, uint64_t ws_bytes, uint64_t* mailbox,
+                   uint64_t seq, void* stream) {
   if (!widths || !outliers || !signs || !payload || !toff || !out || !err || !ws || n == 0 || k == 0)
     return HSZ_EINVAL;
   if (ws_bytes < hsz_workspace_size(n, k)) return HSZ_EINVAL;
@@ -1009,12 +1036,48 @@ int hsz_moments(const uint8_t* widths, const int32_t* outliers, const uint8_t* s
   const uint64_t nt = ceil_div(nb, kTileBlocks);
   if (k == 32) {
     const d32::StreamIn in{widths, outliers, signs, payload, toff, n, nb, nt, tail_len_of(n, 32)};
-    if (want_sq) return launch_decode_pipe<1>(in, nullptr, 0.0, out, ws, err, st);
-    return launch_decode_pipe<0>(in, nullptr, 0.0, out, ws, err, st);
+    const Mailbox mb{mailbox, seq};
+    if (want_sq) return launch_decode_pipe<1>(in, nullptr, 0.0, out, ws, err, st, mb);
+    return launch_decode_pipe<0>(in, nullptr, 0.0, out, ws, err, st, mb);
   }
   const gen::GStream s{widths, outliers, signs, payload, toff, n, k, nb};
   ops::gen_moments_kernel<<<static_cast<unsigned>(nt), gen::kThreads, 0, st>>>(s, want_sq, out, err, ws);
+  if (mailbox) ops::mailbox_post_kernel<<<1, 1, 0, st>>>(Mailbox{mailbox, seq}, out, 5, err);
   return launch_status();
+}
+
+int hsz_moments(const uint8_t* widths, const int32_t* outliers, const uint8_t* signs,
+                const uint8_t* payload, const uint64_t* toff, uint64_t n, uint32_t k, int want_sq,
+                uint64_t* out, uint32_t* err, void* ws, uint64_t ws_bytes, void* stream) {
+  return hsz_moments_mb(widths, outliers, signs, payload, toff, n, k, want_sq, out, err, ws, ws_bytes,
+                        nullptr, 0, stream);
+}
+
+int hsz_mailbox_wait(const uint64_t* mailbox, uint64_t seq, void* stream) {
+  // poll the host word the kernel posts; every 4096 polls ask whether the
+  // stream died (error) or drained without posting (caller falls back)
+  const volatile uint64_t* w = mailbox;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (uint64_t it = 1;; ++it) {
+    if (*w == seq) {
+      __atomic_thread_fence(__ATOMIC_ACQUIRE);
+      return HSZ_OK;
+    }
+    if ((it & 4095u) == 0) {
+      const cudaError_t e = cudaStreamQuery(st);
+      if (e == cudaSuccess) {
+        if (*w == seq) {
+          __atomic_thread_fence(__ATOMIC_ACQUIRE);
+          return HSZ_OK;
+        }
+        return HSZ_EINVAL;   // drained without a post: fall back to a copy
+      }
+      if (e != cudaErrorNotReady) return HSZ_ECUDA;
+    }
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
 }
 
 }  // extern "C"

@@ -219,6 +219,25 @@ constexpr uint64_t kMinmaxCtasMax = 148 * 4;
 constexpr uint64_t kWsMinmaxOff = 64;
 constexpr uint64_t kWsFlagsOff = kWsMinmaxOff + 2 * kMinmaxCtasMax;
 
+// Host-mapped mailbox of a reduction (pinned host memory, UVA): the
+// kernel's last CTA writes the result words and a snapshot of the error word
+// straight into host memory, then (after a system-scope fence) the sequence
+// number in word 0 -- the host polls word 0 instead of a D2H copy + stream
+// synchronisation.  Layout (u64): [0] seq, [1..] results, [1 + nres] error word.
+struct Mailbox {
+  uint64_t* host;   // nullptr: no mailbox
+  uint64_t seq;
+};
+
+__device__ __forceinline__ void mailbox_post(const Mailbox& mb, const uint64_t* res, int nres,
+                                             const uint32_t* err) {
+  if (!mb.host) return;
+  for (int i = 0; i < nres; ++i) mb.host[1 + i] = res[i];
+  mb.host[1 + nres] = *reinterpret_cast<const volatile uint32_t*>(err);
+  __threadfence_system();
+  *reinterpret_cast<volatile uint64_t*>(mb.host) = mb.seq;
+}
+
 struct LookbackWs {
   uint64_t* ticket;
   uint64_t* epoch;

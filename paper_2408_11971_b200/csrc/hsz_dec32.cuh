@@ -619,7 +619,8 @@ __device__ __forceinline__ uint32_t exact_tile(const StreamIn& in, const InTile&
 
 // exact moments of this CTA's compute threads -> the carry-save counters
 // (same protocol as k32::finish_moments, over the 128 compute threads)
-__device__ __forceinline__ void finish_moments_compute(k32::Acc acc, void* ws, uint64_t* out) {
+__device__ __forceinline__ void finish_moments_compute(k32::Acc acc, void* ws, uint64_t* out,
+                                                       const Mailbox& mb, const uint32_t* err) {
   __shared__ k32::Acc s_acc[4];
   __shared__ bool s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -656,6 +657,8 @@ __device__ __forceinline__ void finish_moments_compute(k32::Acc acc, void* ws, u
       out[4] = Q[2];
       for (int k = 0; k < 10; ++k) st_relaxed(cs + k, 0);
       st_relaxed(done, 0);
+      const uint64_t res[5] = {S[0], S[1], Q[0], Q[1], Q[2]};
+      mailbox_post(mb, res, 5, err);
     }
   }
 }
@@ -663,6 +666,7 @@ __device__ __forceinline__ void finish_moments_compute(k32::Acc acc, void* ws, u
 struct MomentsSink {
   uint64_t* out;
   void* ws;
+  Mailbox mb;
 };
 struct DecF32Sink {
   float* out;
@@ -841,9 +845,9 @@ __global__ void __launch_bounds__(kDecThreads, HSZ_DEC_CTAS)
     }
   }
   if (kMode == 2 && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  if (kMode != 2) finish_moments_compute(acc, ms.ws, ms.out);
   flags = __reduce_or_sync(kFull, flags);
-  if (lane == 0 && flags) atomicOr(err, flags);
+  if (lane == 0 && flags) atomicOr(err, flags);   // before the completion count: the last CTA reports it
+  if (kMode != 2) finish_moments_compute(acc, ms.ws, ms.out, ms.mb, err);
 }
 
 }  // namespace d32

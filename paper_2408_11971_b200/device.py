@@ -99,6 +99,12 @@ class Context:
         self._scratch = t.empty(1 << 12, dtype=t.uint8, pin_memory=True)   # small fetches
         self._scratch_np = self._scratch.numpy()
         self._scratch_ptr = self._scratch.data_ptr()
+        # host-mapped mailbox (pinned, device-visible through UVA) the
+        # reduction kernels post their result + error word into
+        self._mailbox = t.zeros(8, dtype=t.int64, pin_memory=True)
+        self.mailbox_ptr = self._mailbox.data_ptr()
+        self._mailbox_np = self._mailbox.numpy().view(np.uint64)
+        self.mailbox_seq = 0
 
     def workspace(self, n: int, k: int):
         need = geometry(n, k)[3]
@@ -131,6 +137,29 @@ class Context:
 
     def check(self, what: str = "") -> None:
         raise_for_flags(self.read_flags(), what)
+
+    def next_seq(self) -> int:
+        self.mailbox_seq += 1
+        return self.mailbox_seq
+
+    def mailbox_result(self, seq: int, nwords: int, what: str = ""):
+        """Wait for the reduction that posts `seq` into the mailbox; returns
+        its `nwords` result words (numpy uint64 copy).  Raises the reference's
+        exception for a set error word; falls back to a copy of the result
+        slot if the stream drained without a post."""
+        rc = self.lib.hsz_mailbox_wait(self.mailbox_ptr, seq, self.handle)
+        if rc != N.HSZ_OK:
+            if rc == N.HSZ_EINVAL:
+                return self.fetch_result(8 * nwords, what).view(np.uint64)
+            self.stream.synchronize()            # surfaces the CUDA error
+            raise RuntimeError(f"{what}: stream failed while waiting for the result")
+        mb = self._mailbox_np
+        flags = int(mb[1 + nwords]) & 0xFFFFFFFF
+        if flags:
+            self.err.zero_()
+            self.stream.synchronize()
+            raise_for_flags(flags, what)
+        return mb[1:1 + nwords].copy()
 
     def fetch_result(self, nbytes: int, what: str = ""):
         """Wait for the result slot (``result_ptr``, ``nbytes`` <= 48) and the

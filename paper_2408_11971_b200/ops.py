@@ -246,9 +246,11 @@ def exact_moments(c, want_sq: bool = True):
     n, k = p.element_count, p.block_len
     wsp, wsb = ctx.workspace(n, k)
     w, o, sg, py, toff = ds.pointers()
-    N.check(ctx.lib.hsz_moments(w, o, sg, py, toff, n, k, 1 if want_sq else 0, ctx.result_ptr,
-                                ctx.err_ptr, wsp, wsb, ctx.handle), "hsz_moments")
-    return unpack_moments(ctx.fetch_result(40, "moments").view(np.uint64))
+    seq = ctx.next_seq()
+    N.check(ctx.lib.hsz_moments_mb(w, o, sg, py, toff, n, k, 1 if want_sq else 0, ctx.result_ptr,
+                                   ctx.err_ptr, wsp, wsb, ctx.mailbox_ptr, seq, ctx.handle),
+            "hsz_moments")
+    return unpack_moments(ctx.mailbox_result(seq, 5, "moments"))
 
 
 def mean_from(S: int, n: int, eps: float) -> float:
