@@ -58,6 +58,13 @@ static_assert(kTileBlocks % kCtaWarps == 0, "tile must split evenly over warps")
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
 
+// 0xFFFFFFFF if the top bit of byte b of x is set, else 0 (PRMT sign mode)
+__device__ __forceinline__ uint32_t prmt_sign(uint32_t x, int b) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(x), "r"((8 + b) * 0x1111));
+  return r;
+}
+
 __device__ __forceinline__ void set_err(uint32_t* err, uint32_t bits) {
   if (bits) atomicOr(err, bits);
 }

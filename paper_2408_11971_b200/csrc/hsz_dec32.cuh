@@ -154,6 +154,11 @@ template <bool kFull, int G, int kAcc = 0>
 __device__ __forceinline__ void decode_block_t(const unsigned char* sgn, const unsigned char* pay,
                                                uint32_t w, int32_t o, int len, int32_t (&q)[K]) {
   const uint32_t sw = bswap32(*reinterpret_cast<const uint32_t*>(sgn));
+  // sign of element i = bit 31 - i of sw = the top bit of byte 3 - i/8 of
+  // (sw << i%8): one PRMT with sign replication per element
+  uint32_t sh[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) sh[k] = sw << k;
   const uint32_t* pw = reinterpret_cast<const uint32_t*>(pay);
   const uint32_t mask = (1u << w) - 1u;
   const int wg = G * static_cast<int>(w);
@@ -163,7 +168,7 @@ __device__ __forceinline__ void decode_block_t(const unsigned char* sgn, const u
   int32_t P = o;
   put_bin<kAcc>(q[0], o);
 #pragma unroll
-  for (int c = 0; c < K / G; ++c) {
+  for (int c = 0; c < (K + G - 1) / G; ++c) {
     if (nb < wg) {
       win = (win << 32) | bswap32(pw[wi++]);
       nb += 32;
@@ -171,10 +176,11 @@ __device__ __forceinline__ void decode_block_t(const unsigned char* sgn, const u
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int i = c * G + g;
+      if (i >= K) break;
       nb -= static_cast<int>(w);
       if (i == 0) continue;   // slot 0: the outlier's zero field
       const int32_t mag = static_cast<int32_t>(static_cast<uint32_t>(win >> nb) & mask);
-      const int32_t neg = static_cast<int32_t>(sw << i) >> 31;   // element i's sign bit
+      const int32_t neg = static_cast<int32_t>(prmt_sign(sh[i & 7], 3 - (i >> 3)));
       int32_t d = (mag ^ neg) - neg;
       if (!kFull) d = (i < len) ? d : 0;
       P += d;
@@ -197,6 +203,8 @@ __device__ __forceinline__ void decode_block(const unsigned char* sgn, const uns
     decode_block_t<false, 1, kAcc>(sgn, pay, w, o, len, q);
   } else if (wmax <= 8) {
     decode_block_t<true, 4, kAcc>(sgn, pay, w, o, len, q);
+  } else if (wmax <= 10) {
+    decode_block_t<true, 3, kAcc>(sgn, pay, w, o, len, q);
   } else if (wmax <= 16) {
     decode_block_t<true, 2, kAcc>(sgn, pay, w, o, len, q);
   } else {

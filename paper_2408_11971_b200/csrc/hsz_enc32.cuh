@@ -220,6 +220,10 @@ __device__ __forceinline__ void block_code(uint32_t (&qb)[K], int len, BlockCode
   bc.w = 32u - __clz(mx);
 }
 
+#ifndef HSZ_PACK_G3
+#define HSZ_PACK_G3 0
+#endif
+
 // MSB-first w-bit fields, G fields combined per step (G * w < 32)
 template <int G>
 __device__ __forceinline__ void pack_fields(const BlockCode& bc, uint32_t a, uint32_t* pbuf) {
@@ -228,12 +232,15 @@ __device__ __forceinline__ void pack_fields(const BlockCode& bc, uint32_t a, uin
   uint32_t acc = 0;
   int nbm = -32;   // pending bits - 32
 #pragma unroll
-  for (int c = 0; c < K / G; ++c) {
+  for (int c = 0; c < (K + G - 1) / G; ++c) {
+    constexpr int kLast = K - ((K + G - 1) / G - 1) * G;   // fields in the last group
+    const int gn = (c == (K + G - 1) / G - 1) ? kLast : G;
     uint32_t chunk = bc.mg[c * G];
 #pragma unroll
-    for (int g = 1; g < G; ++g) chunk = chunk * pw + bc.mg[c * G + g];
-    const uint64_t t = static_cast<uint64_t>(acc) * pg + chunk;
-    nbm += G * static_cast<int>(w);
+    for (int g = 1; g < G; ++g)
+      if (g < gn) chunk = chunk * pw + bc.mg[c * G + g];
+    const uint64_t t = static_cast<uint64_t>(acc) * (gn == G ? pg : (1u << (gn * w))) + chunk;
+    nbm += gn * static_cast<int>(w);
     if (nbm >= 0) {
       pbuf[swz_word(a)] = bswap32(static_cast<uint32_t>(t >> nbm));
       ++a;
@@ -251,6 +258,10 @@ __device__ __forceinline__ void pack_block(const BlockCode& bc, uint32_t wmax, u
   if (bc.w == 0) return;
   if (wmax <= 7) {
     pack_fields<4>(bc, a, pbuf);
+#if HSZ_PACK_G3
+  } else if (wmax <= 10) {
+    pack_fields<3>(bc, a, pbuf);
+#endif
   } else if (wmax <= 15) {
     pack_fields<2>(bc, a, pbuf);
   } else {
