@@ -51,6 +51,8 @@ extern "C" {
 #define HSZ_OUT_F32 0   /* float32 values   (codec.py:112-115, f32 streams)   */
 #define HSZ_OUT_F64 1   /* float64 grid     (codec.py:107-109, 511-513)       */
 #define HSZ_OUT_BINS 2  /* int64 bins       (codec.py:517-520 decode_to_quant) */
+#define HSZ_OUT_BINS_ADD 3  /* out[i] += bin_i (int64, modulo 2^64): N-way folds  */
+#define HSZ_OUT_BINS_SUB 4  /* out[i] -= bin_i (distsim.py:80-103)                 */
 
 /* return codes */
 #define HSZ_OK 0

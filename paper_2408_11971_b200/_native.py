@@ -18,6 +18,7 @@ HSZ_EINVAL = -1
 HSZ_ECUDA = -2
 HSZ_F32, HSZ_F64 = 0, 1
 HSZ_OUT_F32, HSZ_OUT_F64, HSZ_OUT_BINS = 0, 1, 2
+HSZ_OUT_BINS_ADD, HSZ_OUT_BINS_SUB = 3, 4
 HSZ_TILE_BLOCKS = 128
 HSZ_SECTION_SLACK = 16
 

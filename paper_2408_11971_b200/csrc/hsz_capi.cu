@@ -870,6 +870,13 @@ int hsz_decode(const uint8_t* widths, const int32_t* outliers, const uint8_t* si
   const uint64_t nb = ceil_div(n, k);
   const uint64_t nt = ceil_div(nb, kTileBlocks);
   const double d = 2.0 * eps;
+  if (out_kind == HSZ_OUT_BINS_ADD || out_kind == HSZ_OUT_BINS_SUB) {
+    // accumulate into existing int64 bins (folds of several streams)
+    const gen::GStream s{widths, outliers, signs, payload, toff, n, k, nb};
+    gen::decode_kernel<ops::SinkCombineBins><<<static_cast<unsigned>(nt), gen::kThreads, 0, st>>>(
+        s, ops::SinkCombineBins{static_cast<int64_t*>(out), out_kind == HSZ_OUT_BINS_SUB ? 1 : 0}, err);
+    return launch_status();
+  }
   if (k == 32) {
     const k32::StreamIn s{widths, outliers, signs, payload, toff, n, nb, tail_len_of(n, 32)};
     const unsigned g = static_cast<unsigned>(nt);

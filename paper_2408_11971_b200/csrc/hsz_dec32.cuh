@@ -486,10 +486,12 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
         for (int i = 0; i < K; ++i) {
           const double pd = __dmul_rn(i32_to_double(q[i]), sp.rsd);
           const double tt = __dmul_rn(sp.d, pd);
-          const double mag = floor(__dadd_rn(fabs(tt), 0.5));
-          exact |= !(mag < 1073741823.0);
-          const int32_t mi = __double2loint(__dadd_rn(mag, 6755399441055744.0));
-          qb[i] = static_cast<uint32_t>(tt < 0.0 ? -mi : mi);
+          // floor(RN(|t| + 1/2)): RN(|t| + 1/2) is exact here (|t| < 2^31), and
+          // adding 2^52 rounding toward -inf leaves floor() in the low word
+          const uint32_t mi = static_cast<uint32_t>(
+              __double2loint(__dadd_rd(__dadd_rn(fabs(tt), 0.5), 4503599627370496.0)));
+          exact |= mi >= 1073741823u;
+          qb[i] = tt < 0.0 ? 0u - mi : mi;
         }
       } else {
         // |bin_a|, |bin_b| < 2^30: the sum fits int32 and every residual

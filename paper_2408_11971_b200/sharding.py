@@ -13,6 +13,11 @@ exchange.  Only three tiny, latency-bound collectives exist:
 * C3 ``global_moments`` -- allgather of the exact per-shard (S, Q) limbs and
   an exact host sum, so mean / variance are bit-identical for any GPU count.
 
+A second pattern -- every rank holds a whole stream of the same geometry
+(ensemble members, time steps) and all want their sum -- is
+``allreduce_streams``: one all_gather of the serialized (compressed) streams,
+then the residual-domain fold of distsim.py:80-103 (``distsim.py`` here).
+
 The shard's sections, concatenated in rank order at the C2 offsets, are
 byte-identical to the single-GPU stream of the whole field (tested in
 tests/test_sharding_gloo.py and tests/test_gpu_sharding.py).
@@ -107,6 +112,35 @@ class Collectives:
             tot_s += s
             tot_q += q
         return tot_s, tot_q
+
+    # -- reduce compressed streams (distsim.py:80-103 across ranks) ---------
+    def gather_streams(self, stream):
+        """Every rank's stream (same params) on every rank, in rank order, as
+        host CompressedStreams: the serialized bytes (FORMAT.md) of each
+        rank travel through one padded all_gather -- compressed, so a
+        fraction of the raw field's size."""
+        from .device import DeviceStream
+        from .model import deserialize, serialize
+
+        host = stream.to_host() if isinstance(stream, DeviceStream) else stream
+        blob = serialize(host)
+        sizes = [r[0] for r in self._allgather_i64([len(blob)])]
+        t = self.torch
+        buf = t.zeros(max(sizes), dtype=t.uint8)
+        buf[:len(blob)] = t.frombuffer(bytearray(blob), dtype=t.uint8)
+        buf = buf.to(self.device)
+        out = [t.empty_like(buf) for _ in range(self.world)]
+        self.dist.all_gather(out, buf, group=self.group)
+        return [deserialize(bytes(o[:sz].cpu().numpy().tobytes())) for o, sz in zip(out, sizes)]
+
+    def allreduce_streams(self, stream, fold=None):
+        """Every rank gets the homomorphic sum of all ranks' streams (the
+        residual-domain fold of distsim.py:80-103, on this rank's GPU by
+        default; `fold` overrides it, e.g. with the CPU oracle in tests)."""
+        streams = self.gather_streams(stream)
+        if fold is None:
+            from .distsim import aggregate_homomorphic as fold
+        return fold(streams)
 
     def barrier(self):
         self.dist.barrier(group=self.group)

@@ -89,3 +89,17 @@ def test_elementwise_params_mismatch(H):
     b = H.encode_from_quant(H.QuantArray(np.arange(64, dtype=np.int64), p2))
     with pytest.raises(H.ParamsMismatch):
         H.elementwise_add(a, b)
+
+
+@pytest.mark.parametrize("j", range(int(_Z["agg_count"][0])))
+def test_aggregate_golden(H, j):
+    """N-way homomorphic aggregation (distsim.py:80-103) against the
+    reference's own output, host and device-resident operands."""
+    from paper_2408_11971_b200 import distsim
+
+    cnt = int(_Z[f"agg{j}_count"][0])
+    ss = [H.deserialize(_Z[f"agg{j}_in{m}"].tobytes()) for m in range(cnt)]
+    want = _Z[f"agg{j}_out"].tobytes()
+    assert H.serialize(distsim.aggregate_homomorphic(ss)) == want
+    dev = [H.DeviceStream.from_host(s) for s in ss]
+    assert H.serialize(distsim.aggregate_homomorphic(dev).to_host()) == want

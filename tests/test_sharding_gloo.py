@@ -121,3 +121,50 @@ def test_limb_packing_round_trip():
 
     for S, Q in ((0, 0), (-5, 7), (-(2 ** 120), 2 ** 191 - 1), (2 ** 126, 2 ** 64)):
         assert _from_limbs(_to_limbs(S, Q)) == (S, Q)
+
+
+def _stream_worker(rank, world, port, outdir):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import torch.distributed as dist
+
+    import hoszp_oracle as O
+    import paper_2408_11971_b200 as H
+    from paper_2408_11971_b200.sharding import Collectives
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        coll = Collectives()
+        n = 32 * 300 + 7
+        x = _field(n, seed=10 + rank)
+        mine = H.deserialize(O.serialize(O.compress(x, 0.01, (n,), 32, "f32")))
+
+        def oracle_fold(streams):
+            return O.aggregate_homomorphic([O.deserialize(H.serialize(s)) for s in streams])
+
+        got = coll.allreduce_streams(mine, fold=oracle_fold)
+        parts = [None] * world
+        dist.all_gather_object(parts, O.serialize(got))
+        if rank == 0:
+            np.save(os.path.join(outdir, "agg.npy"), np.array(parts, dtype=object), allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_allreduce_streams(tmp_path, world):
+    """Every rank ends with the homomorphic sum of all ranks' streams; the
+    gathered operands arrive byte-exact and in rank order."""
+    import torch.multiprocessing as mp
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import hoszp_oracle as O
+
+    mp.spawn(_stream_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    parts = list(np.load(tmp_path / "agg.npy", allow_pickle=True))
+    n = 32 * 300 + 7
+    streams = [O.compress(_field(n, seed=10 + r), 0.01, (n,), 32, "f32") for r in range(world)]
+    want = O.serialize(O.aggregate_homomorphic(streams))
+    assert all(p == want for p in parts)
