@@ -169,6 +169,33 @@ int hsz_elementwise(const uint8_t* a_widths, const int32_t* a_outliers, const ui
                     uint64_t payload_cap, uint64_t* out_tile_offsets, void* scratch, uint32_t* err,
                     void* ws, uint64_t ws_bytes, void* stream);
 
+/* ---- bivariate quantized-domain operations (ops.py:226-240, 400-513) and
+ * per-block means (ops.py:366-379): the operands decode to int64 bins in
+ * `scratch` (hsz_bivariate_scratch_size bytes), then
+ *   hsz_hadamard    bins = round-half-away(RN(2eps * RN(a*b))), re-encoded;
+ *   hsz_pair_stats  exact sums for covariance / ssim_global into out
+ *                   (u64[52]: 24 carry-save counters of 32-bit chunks, two
+ *                   words each -- SA+ SA- SB+ SB- (2 chunks), QA QB SAB+ SAB-
+ *                   (4 chunks) -- then min a, max a, min b, max b as int64);
+ *   hsz_block_means out (device f64[B]) = 2eps * sum(block bins) / length. */
+uint64_t hsz_bivariate_scratch_size(uint64_t n, uint32_t block_len);
+int hsz_hadamard(const uint8_t* a_widths, const int32_t* a_outliers, const uint8_t* a_signs,
+                 const uint8_t* a_payload, const uint64_t* a_tile_offsets, const uint8_t* b_widths,
+                 const int32_t* b_outliers, const uint8_t* b_signs, const uint8_t* b_payload,
+                 const uint64_t* b_tile_offsets, uint64_t n, uint32_t block_len, double eps,
+                 uint8_t* out_widths, int32_t* out_outliers, uint8_t* out_signs, uint64_t sign_cap,
+                 uint8_t* out_payload, uint64_t payload_cap, uint64_t* out_tile_offsets,
+                 void* scratch, uint32_t* err, void* ws, uint64_t ws_bytes, void* stream);
+int hsz_pair_stats(const uint8_t* a_widths, const int32_t* a_outliers, const uint8_t* a_signs,
+                   const uint8_t* a_payload, const uint64_t* a_tile_offsets,
+                   const uint8_t* b_widths, const int32_t* b_outliers, const uint8_t* b_signs,
+                   const uint8_t* b_payload, const uint64_t* b_tile_offsets, uint64_t n,
+                   uint32_t block_len, uint64_t* out, void* scratch, uint32_t* err, void* stream);
+int hsz_block_means(const uint8_t* widths, const int32_t* outliers, const uint8_t* signs,
+                    const uint8_t* payload, const uint64_t* tile_offsets, uint64_t n,
+                    uint32_t block_len, double eps, double* out, void* scratch, uint32_t* err,
+                    void* stream);
+
 /* ---- K7: exact moments (ops.py:249-357) -------------------------------------
  * out (device u64[5]) = S as signed 128-bit (lo, hi) and, if want_sq,
  * Q = sum(bins^2) as unsigned 192-bit (limb0, limb1, limb2).  The host

@@ -39,8 +39,12 @@ from .ops import (
     ScalarBin,
     apply_reduction,
     apply_stream_op,
+    block_means,
+    covariance,
     elementwise_add,
     elementwise_sub,
+    hadamard,
+    ssim_global,
     mean,
     negate,
     scalar_add,

@@ -57,6 +57,12 @@ SIGNATURES = {
     "hsz_elementwise_scratch_size": (_u64, [_u64, _u32]),
     "hsz_elementwise": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _u64, _u32, _int,
                                _vp, _vp, _vp, _u64, _vp, _u64, _vp, _vp, _vp, _vp, _u64, _vp]),
+    "hsz_bivariate_scratch_size": (_u64, [_u64, _u32]),
+    "hsz_hadamard": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _u64, _u32, _dbl,
+                            _vp, _vp, _vp, _u64, _vp, _u64, _vp, _vp, _vp, _vp, _u64, _vp]),
+    "hsz_pair_stats": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _u64, _u32, _vp,
+                              _vp, _vp, _vp]),
+    "hsz_block_means": (_int, [_vp, _vp, _vp, _vp, _vp, _u64, _u32, _dbl, _vp, _vp, _vp, _vp]),
     "hsz_moments": (_int, [_vp, _vp, _vp, _vp, _vp, _u64, _u32, _int, _vp, _vp, _vp, _u64, _vp]),
     "hsz_copy_d2h": (_int, [_vp, _vp, _u64, _vp]),
     "hsz_stream_sync": (_int, [_vp]),

@@ -16,7 +16,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "_lib")
 LIB = os.environ.get("HSZ_B200_LIB") or os.path.join(LIB_DIR, "libhsz_b200.so")
 SOURCES = ["hsz_capi.cu"]
-HEADERS = ["hsz_common.cuh", "hsz_quant.cuh", "hsz_k32.cuh", "hsz_generic.cuh", "hsz_enc32.cuh", "hsz_dec32.cuh"]
+HEADERS = ["hsz_common.cuh", "hsz_quant.cuh", "hsz_k32.cuh", "hsz_generic.cuh", "hsz_enc32.cuh", "hsz_dec32.cuh",
+           "hsz_bivar.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -12,6 +12,7 @@
 
 #include "hsz_common.cuh"
 #include "hsz_dec32.cuh"
+#include "hsz_bivar.cuh"
 #include "hsz_enc32.cuh"
 #include "hsz_generic.cuh"
 #include "hsz_k32.cuh"
@@ -1029,6 +1030,71 @@ int hsz_elementwise(const uint8_t* wa, const int32_t* oa, const uint8_t* sa, con
   }
   return launch_encode_generic(gen::GBins{bins}, n, k, ow, oo, os, sign_cap, op, payload_cap, otoff,
                                err, ws, st);
+}
+
+uint64_t hsz_bivariate_scratch_size(uint64_t n, uint32_t k) { return k ? 16 * n : 0; }
+
+// decode both operands to int64 bins: a -> bins[0, n), b -> bins[n, 2n)
+static int decode_pair_bins(const uint8_t* wa, const int32_t* oa, const uint8_t* sa,
+                            const uint8_t* pa, const uint64_t* ta, const uint8_t* wb,
+                            const int32_t* ob, const uint8_t* sb, const uint8_t* pb,
+                            const uint64_t* tb, uint64_t n, uint32_t k, int64_t* bins,
+                            uint32_t* err, void* stream) {
+  int rc = hsz_decode(wa, oa, sa, pa, ta, n, k, 1.0, HSZ_OUT_BINS, bins, err, stream);
+  if (rc != HSZ_OK) return rc;
+  return hsz_decode(wb, ob, sb, pb, tb, n, k, 1.0, HSZ_OUT_BINS, bins + n, err, stream);
+}
+
+static unsigned bv_grid(uint64_t items) {
+  const uint64_t g = ceil_div(items, bv::kThreads);
+  return static_cast<unsigned>(g < 148 * 8 ? (g ? g : 1) : 148 * 8);
+}
+
+int hsz_hadamard(const uint8_t* wa, const int32_t* oa, const uint8_t* sa, const uint8_t* pa,
+                 const uint64_t* ta, const uint8_t* wb, const int32_t* ob, const uint8_t* sb,
+                 const uint8_t* pb, const uint64_t* tb, uint64_t n, uint32_t k, double eps,
+                 uint8_t* ow, int32_t* oo, uint8_t* os, uint64_t sign_cap, uint8_t* op,
+                 uint64_t payload_cap, uint64_t* otoff, void* scratch, uint32_t* err, void* ws,
+                 uint64_t ws_bytes, void* stream) {
+  if (!scratch || !err || !ws || n == 0 || k == 0) return HSZ_EINVAL;
+  if (ws_bytes < hsz_workspace_size(n, k)) return HSZ_EINVAL;
+  int64_t* bins = static_cast<int64_t*>(scratch);
+  int rc = decode_pair_bins(wa, oa, sa, pa, ta, wb, ob, sb, pb, tb, n, k, bins, err, stream);
+  if (rc != HSZ_OK) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  bv::hadamard_kernel<<<bv_grid(n), bv::kThreads, 0, st>>>(bins, bins + n, n, 2.0 * eps, err);
+  rc = launch_status();
+  if (rc != HSZ_OK) return rc;
+  return hsz_encode_bins(bins, n, k, ow, oo, os, sign_cap, op, payload_cap, otoff, err, ws,
+                         ws_bytes, stream);
+}
+
+int hsz_pair_stats(const uint8_t* wa, const int32_t* oa, const uint8_t* sa, const uint8_t* pa,
+                   const uint64_t* ta, const uint8_t* wb, const int32_t* ob, const uint8_t* sb,
+                   const uint8_t* pb, const uint64_t* tb, uint64_t n, uint32_t k, uint64_t* out,
+                   void* scratch, uint32_t* err, void* stream) {
+  if (!out || !scratch || !err || n == 0 || k == 0) return HSZ_EINVAL;
+  if (n >= (1ull << 32)) return HSZ_EINVAL;   // carry-save counter headroom
+  int64_t* bins = static_cast<int64_t*>(scratch);
+  int rc = decode_pair_bins(wa, oa, sa, pa, ta, wb, ob, sb, pb, tb, n, k, bins, err, stream);
+  if (rc != HSZ_OK) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  bv::pair_stats_init<<<1, 64, 0, st>>>(out);
+  bv::pair_stats_kernel<<<bv_grid(n), bv::kThreads, 0, st>>>(bins, bins + n, n, out);
+  return launch_status();
+}
+
+int hsz_block_means(const uint8_t* widths, const int32_t* outliers, const uint8_t* signs,
+                    const uint8_t* payload, const uint64_t* toff, uint64_t n, uint32_t k,
+                    double eps, double* out, void* scratch, uint32_t* err, void* stream) {
+  if (!out || !scratch || !err || n == 0 || k == 0) return HSZ_EINVAL;
+  int64_t* bins = static_cast<int64_t*>(scratch);
+  int rc = hsz_decode(widths, outliers, signs, payload, toff, n, k, 1.0, HSZ_OUT_BINS, bins, err, stream);
+  if (rc != HSZ_OK) return rc;
+  const uint64_t nb = ceil_div(n, k);
+  bv::block_means_kernel<<<bv_grid(nb), bv::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      bins, widths, outliers, n, k, nb, 2.0 * eps, out);
+  return launch_status();
 }
 
 int hsz_moments_mb(const uint8_t* widths, const int32_t* outliers, const uint8_t* signs,

@@ -19,10 +19,10 @@ Q = sum(bins^2) (uint192) and the final float64 arithmetic is the
 reference's own Python expression on Python ints, so mean / variance are
 bit-identical to the reference, not merely within tolerance.
 
-elementwise_add / elementwise_sub (ops.py:163-192) are the first of the
-bivariate operations.  The others (hadamard,
-covariance, ssim) are not on this hot path; the dispatch tables keep their
-names and report them as not implemented here.
+elementwise_add / elementwise_sub (ops.py:163-192)
+run as one fused pass for block_len 32; hadamard, covariance, ssim_global
+and block_means (§8(f) row 3) decode their operands to int64 bins and
+reduce / rescale them exactly (hsz_bivar.cuh).
 """
 
 from __future__ import annotations
@@ -54,9 +54,9 @@ STREAM_OPS = {
 #: scalar-returning reductions: name -> operand streams  (ops.py:48)
 REDUCTIONS = {"mean": 1, "variance": 1, "stddev": 1, "covariance": 2, "ssim": 2}
 
-#: the subset implemented by this B200 hot path
-HOT_STREAM_OPS = ("neg", "sadd", "ssub", "smul", "eadd", "esub")
-HOT_REDUCTIONS = ("mean", "variance", "stddev")
+#: the subset implemented by this B200 hot path (all of them)
+HOT_STREAM_OPS = ("neg", "sadd", "ssub", "smul", "eadd", "esub", "hadamard")
+HOT_REDUCTIONS = ("mean", "variance", "stddev", "covariance", "ssim")
 
 
 @dataclass(frozen=True)
@@ -213,6 +213,111 @@ def scalar_mul(c, s: float, threads: int = 1):
 
 
 # ---------------------------------------------------------------------------
+# bivariate quantized-domain operations
+
+def _bivar_scratch(ctx, n, k):
+    return ctx.empty(int(ctx.lib.hsz_bivariate_scratch_size(n, k)), torch().uint8)
+
+
+def hadamard(a, b, threads: int = 1):
+    """Element-wise product via the quantized domain: the scalar-multiply
+    rescale rule with b's bins as the scalars (ops.py:226-240)."""
+    _check_params(a, b)
+    da, db = _as_device_stream(a), _as_device_stream(b)
+    ctx = da.ctx
+    p = da.params
+    n, k = p.element_count, p.block_len
+    wsp, wsb = ctx.workspace(n, k)
+    scratch = _bivar_scratch(ctx, n, k)
+    sp = ptr(scratch)
+    wa, oa, sa, pa, ta = da.pointers()
+    wb, ob, sb, pb, tb = db.pointers()
+
+    def launch(ow, oo, os_, scap, op, pcap, otoff):
+        N.check(ctx.lib.hsz_hadamard(wa, oa, sa, pa, ta, wb, ob, sb, pb, tb, n, k, p.eps, ow, oo,
+                                     os_, scap, op, pcap, otoff, sp, ctx.err_ptr, wsp, wsb,
+                                     ctx.handle), "hsz_hadamard")
+
+    out = run_encoder(ctx, p, launch)
+    return _finish(a, out, "hadamard")
+
+
+def _bank(c, j0, nchunks) -> int:
+    return sum(c[j0 + j] << (32 * j) for j in range(nchunks))
+
+
+def pair_stats(a, b):
+    """Exact integer (S_a, Q_a, min_a, max_a, S_b, Q_b, min_b, max_b, S_ab)
+    over the bins of two streams -- the sums behind covariance and
+    ssim_global (ops.py:313-357, 361-450)."""
+    _check_params(a, b)
+    da, db = _as_device_stream(a), _as_device_stream(b)
+    ctx = da.ctx
+    p = da.params
+    n, k = p.element_count, p.block_len
+    scratch = _bivar_scratch(ctx, n, k)
+    out = ctx.empty(52, torch().int64)
+    N.check(ctx.lib.hsz_pair_stats(*da.pointers(), *db.pointers(), n, k, ptr(out), ptr(scratch),
+                                   ctx.err_ptr, ctx.handle), "hsz_pair_stats")
+    (w,) = ctx.fetch_checked([out], "pair_stats")
+    u = [int(x) for x in np.asarray(w).view(np.uint64)]
+    c = [u[2 * j] + (u[2 * j + 1] << 32) for j in range(24)]
+    mm = [int(x) for x in np.asarray(w)[48:52]]
+    sa = _bank(c, 0, 2) - _bank(c, 2, 2)
+    sb = _bank(c, 4, 2) - _bank(c, 6, 2)
+    return (sa, _bank(c, 8, 4), mm[0], mm[1], sb, _bank(c, 12, 4), mm[2], mm[3],
+            _bank(c, 16, 4) - _bank(c, 20, 4))
+
+
+def covariance(a, b, *, shortcut: bool = True, threads: int = 1) -> float:
+    """Population covariance via exact integer sums (ops.py:453-462)."""
+    _check_params(a, b)
+    n = a.params.element_count
+    sa, _, _, _, sb, _, _, _, sab = pair_stats(a, b)
+    return (2.0 * a.params.eps) ** 2 * float(n * sab - sa * sb) / (n * n)
+
+
+def ssim_global(a, b, *, threads: int = 1) -> float:
+    """Single global SSIM from the exact quantized-domain sums, with the
+    reference's float expressions (ops.py:465-487)."""
+    _check_params(a, b)
+    n = a.params.element_count
+    eps2 = 2.0 * a.params.eps
+    sa, sqa, lo_a, hi_a, sb, sqb, lo_b, hi_b, sab = pair_stats(a, b)
+    mu_a = eps2 * sa / n
+    mu_b = eps2 * sb / n
+    var_a = eps2**2 * float(n * sqa - sa * sa) / (n * n)
+    var_b = eps2**2 * float(n * sqb - sb * sb) / (n * n)
+    cov = eps2**2 * float(n * sab - sa * sb) / (n * n)
+    value_range = eps2 * max(hi_a - lo_a, hi_b - lo_b)
+    c1 = (0.01 * value_range) ** 2
+    c2 = (0.03 * value_range) ** 2
+    num = (2.0 * mu_a * mu_b + c1) * (2.0 * cov + c2)
+    den = (mu_a * mu_a + mu_b * mu_b + c1) * (var_a + var_b + c2)
+    if den == 0.0:
+        raise ValueError("SSIM is undefined: degenerate zero-range operands")
+    return num / den
+
+
+def block_means(c, threads: int = 1):
+    """Per-block means 2 eps * sum(block bins) / block length
+    (ops.py:366-379); numpy float64[B] for a host stream, a device tensor for
+    a DeviceStream."""
+    ds = _as_device_stream(c)
+    ctx = ds.ctx
+    p = ds.params
+    n, k = p.element_count, p.block_len
+    out = ctx.empty(p.block_count, torch().float64)
+    scratch = ctx.empty(8 * n, torch().uint8)
+    N.check(ctx.lib.hsz_block_means(*ds.pointers(), n, k, p.eps, ptr(out), ptr(scratch),
+                                    ctx.err_ptr, ctx.handle), "hsz_block_means")
+    if isinstance(c, DeviceStream):
+        return out
+    (v,) = ctx.fetch_checked([out], "block_means")
+    return np.asarray(v, dtype=np.float64)
+
+
+# ---------------------------------------------------------------------------
 # reductions
 
 def moments_device(ds: DeviceStream, want_sq: bool):
@@ -299,6 +404,8 @@ def apply_stream_op(name: str, streams, scalar=None, threads: int = 1):
         return elementwise_add(streams[0], streams[1], threads)
     if name == "esub":
         return elementwise_sub(streams[0], streams[1], threads)
+    if name == "hadamard":
+        return hadamard(streams[0], streams[1], threads)
     raise NotImplementedError(f"stream op {name!r} is outside the B200 hot path "
                               f"(implemented: {', '.join(HOT_STREAM_OPS)})")
 
@@ -312,13 +419,18 @@ def apply_reduction(name: str, streams, threads: int = 1) -> float:
         return variance(streams[0], threads=threads)
     if name == "stddev":
         return stddev(streams[0], threads=threads)
+    if name == "covariance":
+        return covariance(streams[0], streams[1], threads=threads)
+    if name == "ssim":
+        return ssim_global(streams[0], streams[1], threads=threads)
     raise NotImplementedError(f"reduction {name!r} is outside the B200 hot path "
                               f"(implemented: {', '.join(HOT_REDUCTIONS)})")
 
 
 __all__ = [
     "STREAM_OPS", "REDUCTIONS", "ScalarBin", "negate", "scalar_add", "scalar_sub", "scalar_mul",
-    "elementwise_add", "elementwise_sub",
+    "elementwise_add", "elementwise_sub", "hadamard", "covariance", "ssim_global", "block_means",
+    "pair_stats",
     "mean", "variance", "stddev", "exact_moments", "apply_stream_op", "apply_reduction",
     "CompressedStream",
 ]

@@ -103,3 +103,48 @@ def test_aggregate_golden(H, j):
     assert H.serialize(distsim.aggregate_homomorphic(ss)) == want
     dev = [H.DeviceStream.from_host(s) for s in ss]
     assert H.serialize(distsim.aggregate_homomorphic(dev).to_host()) == want
+
+
+def _float_or_err(fn):
+    try:
+        return fn().hex()
+    except Exception as exc:
+        return "!" + type(exc).__name__
+
+
+@pytest.mark.parametrize("case", range(_N))
+def test_bivariate_golden(H, case):
+    """hadamard / covariance / ssim_global / block_means through the C ABI
+    against the reference's own outputs (bit-exact bytes and floats)."""
+    a = H.deserialize(_Z[f"c{case}_a"].tobytes())
+    b = H.deserialize(_Z[f"c{case}_b"].tobytes())
+    err = str(_Z[f"c{case}_had_err"][0])
+    if err:
+        with pytest.raises(Exception) as ei:
+            H.hadamard(a, b)
+        assert type(ei.value).__name__ == err
+    else:
+        assert H.serialize(H.hadamard(a, b)) == _Z[f"c{case}_had"].tobytes()
+    assert _float_or_err(lambda: H.covariance(a, b)) == str(_Z[f"c{case}_cov"][0])
+    assert _float_or_err(lambda: H.ssim_global(a, b)) == str(_Z[f"c{case}_ssim"][0])
+    assert H.block_means(a).tobytes() == _Z[f"c{case}_bmeans"].tobytes()
+    if not str(_Z[f"c{case}_cov"][0]).startswith("!"):
+        assert H.apply_reduction("covariance", [a, b]).hex() == str(_Z[f"c{case}_cov"][0])
+
+
+def test_bivariate_device_resident(H):
+    """Device-resident operands at a realistic size against the oracle."""
+    import torch
+
+    rng = np.random.default_rng(77)
+    n = 300_000 + 11
+    xa, xb = _field(rng, n, 0), _field(rng, n, 1)
+    p = H.QuantParams(1e-3 * float(max(xa.max(), xb.max()) - min(xa.min(), xb.min())), (n,), 32, "f32")
+    sa = H.compress(H.RawArray(torch.from_numpy(xa).cuda(), (n,), "f32"), p)
+    sb = H.compress(H.RawArray(torch.from_numpy(xb).cuda(), (n,), "f32"), p)
+    oa = O.deserialize(H.serialize(sa.to_host()))
+    ob = O.deserialize(H.serialize(sb.to_host()))
+    assert H.serialize(H.hadamard(sa, sb).to_host()) == O.serialize(O.hadamard(oa, ob))
+    assert H.covariance(sa, sb) == O.covariance(oa, ob)
+    assert H.ssim_global(sa, sb) == O.ssim_global(oa, ob)
+    assert H.block_means(sa).cpu().numpy().tobytes() == O.block_means(oa).tobytes()
