@@ -33,6 +33,7 @@ from .codec import (
     write_raw,
 )
 from .device import DeviceStream
+from .hszio import read_hsz, serialize_device, write_hsz
 from .ops import (
     REDUCTIONS,
     STREAM_OPS,

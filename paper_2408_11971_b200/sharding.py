@@ -142,6 +142,40 @@ class Collectives:
             from .distsim import aggregate_homomorphic as fold
         return fold(streams)
 
+    def write_sharded(self, path, params, layout: ShardLayout, stream):
+        """Every rank writes its shard's sections straight into one ``.hsz``
+        file at the global offsets (FORMAT.md; C2 layout) -- no gather.
+        `params` = the whole field's QuantParams, `stream` = this rank's shard
+        (host or device)."""
+        import os
+
+        from .device import DeviceStream
+        from .model import header_bytes
+
+        host = stream.to_host() if isinstance(stream, DeviceStream) else stream
+        hdr = header_bytes(params)
+        h, B = len(hdr), params.block_count
+        total = h + 5 * B + layout.sign_total + layout.payload_total
+        if self.rank == 0:
+            with open(path, "wb") as f:
+                f.truncate(total)
+                f.write(hdr)
+        self.barrier()
+        fd = os.open(path, os.O_WRONLY)
+        try:
+            b0 = layout.block0
+            os.pwrite(fd, np.asarray(host.widths, dtype=np.uint8).tobytes(), h + b0)
+            os.pwrite(fd, np.asarray(host.outliers, dtype="<i4").tobytes(), h + B + 4 * b0)
+            if len(host.sign_planes):
+                os.pwrite(fd, bytes(host.sign_planes), h + 5 * B + layout.sign_offset)
+            if len(host.payload):
+                os.pwrite(fd, bytes(host.payload),
+                          h + 5 * B + layout.sign_total + layout.payload_offset)
+        finally:
+            os.close(fd)
+        self.barrier()
+        return total
+
     def barrier(self):
         self.dist.barrier(group=self.group)
 

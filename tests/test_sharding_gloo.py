@@ -168,3 +168,48 @@ def test_allreduce_streams(tmp_path, world):
     streams = [O.compress(_field(n, seed=10 + r), 0.01, (n,), 32, "f32") for r in range(world)]
     want = O.serialize(O.aggregate_homomorphic(streams))
     assert all(p == want for p in parts)
+
+
+def _write_worker(rank, world, port, path):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import torch.distributed as dist
+
+    import hoszp_oracle as O
+    import paper_2408_11971_b200 as H
+    from paper_2408_11971_b200.sharding import Collectives, element_range
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        coll = Collectives()
+        n, k = 32 * 700 + 9, 32
+        x = _field(n, seed=5)
+        e0, e1 = element_range(n, k, rank, world)
+        xs = x[e0:e1]
+        lo, hi = coll.global_range(float(xs.min()), float(xs.max()))
+        eps = 1e-4 * (hi - lo)
+        shard = H.deserialize(O.serialize(O.compress(xs, eps, (xs.size,), k, "f32")))
+        lay = coll.global_offsets(e0 // k, len(shard.sign_planes), len(shard.payload))
+        coll.write_sharded(path, H.QuantParams(eps, (n,), k, "f32"), lay, shard)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_write_sharded_equals_serialize(tmp_path, world):
+    """Per-rank pwrites at the C2 offsets produce exactly the single-process
+    .hsz bytes (FORMAT.md) of the whole field."""
+    import torch.multiprocessing as mp
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import hoszp_oracle as O
+
+    path = str(tmp_path / "field.hsz")
+    mp.spawn(_write_worker, args=(world, _free_port(), path), nprocs=world, join=True)
+    n = 32 * 700 + 9
+    x = _field(n, seed=5)
+    eps = 1e-4 * (float(x.max()) - float(x.min()))
+    want = O.serialize(O.compress(x, eps, (n,), 32, "f32"))
+    assert open(path, "rb").read() == want
