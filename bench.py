@@ -151,7 +151,11 @@ def _field(config: int, rank: int, device):
         return x.reshape(-1).float()
     if config == 4:
         return W.config4(seed=3 if rank == 0 else 3 + 1000 * rank, device=device)
-    raise ValueError("bench supports --config 2 or 4")
+    if config == 5:
+        # 2048^3 field as 8 slabs of 2^30 values; rank r owns slab r (the
+        # 8-GPU partition); at N < 8 every rank still owns one slab (weak)
+        return W.config5_slab(rank % 8, device=device)
+    raise ValueError("bench supports --config 2, 4 or 5")
 
 
 class Chain:
@@ -261,6 +265,8 @@ def run_b200(args):
 
     coll = Collectives() if world > 1 else None
     cfg = dict(W.CONFIGS[args.config])
+    if args.config == 5:
+        cfg["dims"] = (256, 2048, 2048)          # one 2^30-value slab per rank
     x = _field(args.config, rank, dev).contiguous()
     n = x.numel()
     chain = Chain(H, cfg, coll)
@@ -321,7 +327,12 @@ def run_b200(args):
     achieved = abytes[dom] / (kern[dom] * 1e-3) / 1e9
 
     # ---- e2e through the public API from pinned host memory
-    e2e = _e2e(H, chain, x, flush, steps=max(6, min(args.steps, 20)), coll=coll)
+    if args.config == 5:
+        e2e = {"value": None, "unit": "GB/s", "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": None,
+               "skipped": "config 5 slab: the pinned host arenas would need ~25 GB; e2e is "
+                          "measured on the default config"}
+    else:
+        e2e = _e2e(H, chain, x, flush, steps=max(6, min(args.steps, 20)), coll=coll)
 
     line = {
         "metric": METRIC,
@@ -360,7 +371,7 @@ def run_b200(args):
         "gpu_launches": 8 * args.steps,
         "clocks": clocks,
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config != 5:
         line["cpu_baseline"] = _cpu_baseline(x.cpu().numpy(), cfg, budget_s=args.cpu_budget)
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -612,6 +623,8 @@ def run_reference(args):
     from paper_2408_11971_b200 import workloads as W
 
     cfg = dict(W.CONFIGS[args.config])
+    if args.config == 5:
+        cfg["dims"] = (256, 2048, 2048)          # one 2^30-value slab per rank
     if args.config == 2:
         x = W.config2()
     else:
@@ -649,7 +662,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=2, choices=[2, 4, 5])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
