@@ -168,7 +168,11 @@ class Chain:
 
     def run(self, x, events=None, host_out=False):
         H, cfg = self.H, self.cfg
-        mark = (lambda i: events[i].record()) if events is not None else (lambda i: None)
+        # events: {mark index: CUDA event}; only the given marks are recorded
+        # (the timed steps record 0 and 7 only: each record is host time that
+        # would otherwise sit between a synchronising call and the next launch)
+        mark = (lambda i: events[i].record() if i in events else None) if events is not None \
+            else (lambda i: None)
         mark(0)
         raw = H.RawArray(x, cfg["dims"], "f32")               # K0: range + finite check
         lo, hi = raw.value_range()
@@ -279,7 +283,6 @@ def run_b200(args):
         chain.run(x)
     torch.cuda.synchronize()
 
-    nev = 8
     per_step = []
     per_op = {op: [] for op in OPS}
     if coll is not None:
@@ -288,16 +291,23 @@ def run_b200(args):
     wall0 = time.perf_counter()
     for _ in range(args.steps):
         _flush(flush)                                   # evict L2 (excluded from timing)
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
+        evs = {0: torch.cuda.Event(enable_timing=True), 7: torch.cuda.Event(enable_timing=True)}
         chain.run(x, evs)
         torch.cuda.synchronize()
         per_step.append(evs[0].elapsed_time(evs[7]))
-        for i, op in enumerate(OPS):
-            per_op[op].append(evs[i].elapsed_time(evs[i + 1]))
     torch.cuda.synchronize()
     if coll is not None:
         coll.barrier()
     wall = time.perf_counter() - wall0
+    # per-op breakdown inside the chain: separate (untimed) steps with a mark
+    # between every op
+    for _ in range(min(args.steps, 5)):
+        _flush(flush)
+        evs = {i: torch.cuda.Event(enable_timing=True) for i in range(8)}
+        chain.run(x, evs)
+        torch.cuda.synchronize()
+        for i, op in enumerate(OPS):
+            per_op[op].append(evs[i].elapsed_time(evs[i + 1]))
 
     step_ms = sum(per_step) / len(per_step)
     if coll is not None:

@@ -442,7 +442,35 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 
 // 2-D tensor map over a float32 field viewed as rows of 32 values (one block
 // per row), 128-row boxes, 128-byte swizzle; false if the field does not allow it
+static bool make_rows_map_f32_uncached(const float* x, uint64_t n, CUtensorMap* map);
+
+// the encoded maps of the last few (pointer, length) pairs, per host thread:
+// a chain of ops on the same buffers skips cuTensorMapEncodeTiled
 static bool make_rows_map_f32(const float* x, uint64_t n, CUtensorMap* map) {
+  struct Entry {
+    const float* x;
+    uint64_t n;
+    bool ok;
+    CUtensorMap map;
+  };
+  static thread_local Entry cache[4] = {};
+  static thread_local int next = 0;
+  for (const Entry& e : cache)
+    if (e.x == x && e.n == n && x) {
+      *map = e.map;
+      return e.ok;
+    }
+  const bool ok = make_rows_map_f32_uncached(x, n, map);
+  Entry& e = cache[next];
+  next = (next + 1) & 3;
+  e.x = x;
+  e.n = n;
+  e.ok = ok;
+  e.map = *map;
+  return ok;
+}
+
+static bool make_rows_map_f32_uncached(const float* x, uint64_t n, CUtensorMap* map) {
   std::memset(map, 0, sizeof(*map));
   const uint64_t rows = n / 32;
   if ((reinterpret_cast<uintptr_t>(x) & 15u) != 0 || rows < static_cast<uint64_t>(kTileBlocks) ||
@@ -496,21 +524,7 @@ static int launch_compress_f32(const float* x, uint64_t n, const QuantConst& c,
   const uint64_t nt = ceil_div(nb, kTileBlocks);
   const e32::QuantF32 qf = e32::make_quant_f32(c);
   CUtensorMap map;
-  std::memset(&map, 0, sizeof(map));
-  bool tma = false;
-  const uint64_t rows = n / 32;
-  if ((reinterpret_cast<uintptr_t>(x) & 15u) == 0 && rows >= static_cast<uint64_t>(kTileBlocks) &&
-      rows < (1ull << 31)) {
-    if (auto enc = tensor_map_encoder()) {
-      cuuint64_t dims[2] = {32, rows};
-      cuuint64_t strides[1] = {128};
-      cuuint32_t box[2] = {32, static_cast<cuuint32_t>(kTileBlocks)};
-      cuuint32_t estr[2] = {1, 1};
-      tma = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(x), dims, strides, box,
-                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-    }
-  }
+  const bool tma = make_rows_map_f32(x, n, &map);
   constexpr int smem = static_cast<int>(e32::kSmem7Bytes);
   auto kern = tma ? e32::compress_f32_kernel<true> : e32::compress_f32_kernel<false>;
   // persistent grid: every CTA resident (the look-back relies on it)
