@@ -467,95 +467,6 @@ struct SrcBins {
   }
 };
 
-// scalar multiply: decode the input stream tile, rescale (ops.py:199-225)
-struct SrcSmul {
-  StreamIn in;
-  int64_t rs;
-  double d;
-  double rsd;      // (double) rs
-  bool small_rs;   // |rs| < 2^21: |bin * rs| < 2^53 for every fast-path bin
-  TileIn t;
-  static constexpr uint32_t kStageBytes = kStageFast;
-  static constexpr int kMinBlocks = 4;
-
-  // load block metadata, scan, and (fast tiles) bulk-copy the tile's bytes
-  __device__ __forceinline__ void issue(uint64_t tile, unsigned char* stage, Stager& st,
-                                        uint32_t* s_tmp, uint32_t* flags) {
-    const uint64_t b = tile * TB + threadIdx.x;
-    uint32_t w = 0;
-    int32_t o = 0;
-    int len = 0;
-    if (b < in.nblocks) {
-      w = in.widths[b];
-      o = in.outliers[b];
-      len = (b == in.nblocks - 1) ? static_cast<int>(in.tail_len) : K;
-    }
-    if (w > 64) {
-      *flags |= HSZ_ERR_BAD_WIDTH;
-      w = 0;
-    }
-    const uint32_t sb = w ? (len + 7) / 8 : 0;
-    const uint32_t pb = (len * w + 7) / 8;
-    uint32_t es, ep, ts, tp;
-    scan2(sb, pb, &es, &ep, &ts, &tp, s_tmp);
-    const uint64_t g_s0 = in.toff[2 * tile], g_p0 = in.toff[2 * tile + 1];
-    const bool fast = grp_and(w <= kFastW);
-    t.w = w;
-    t.o = o;
-    t.len = len;
-    t.fast = fast;
-    st.bulk = fast;
-    if (fast) {
-      const uint64_t s_lo = g_s0 & ~15ull, s_hi = (g_s0 + ts + 15) & ~15ull;
-      const uint64_t p_lo = g_p0 & ~15ull, p_hi = (g_p0 + tp + 15) & ~15ull;
-      const uint32_t sbytes = static_cast<uint32_t>(s_hi - s_lo);
-      const uint32_t pbytes = static_cast<uint32_t>(p_hi - p_lo);
-      if (threadIdx.x == 0) {
-        st.arm(sbytes + pbytes);
-        if (sbytes) bulk_g2s(stage, in.signs + s_lo, sbytes, st.bar);
-        if (pbytes) bulk_g2s(stage + kStageSign, in.payload + p_lo, pbytes, st.bar);
-      }
-      t.sgn = stage;
-      t.pay = stage + kStageSign;
-      t.soff = (g_s0 - s_lo) + es;
-      t.poff = (g_p0 - p_lo) + ep;
-    } else {
-      t.sgn = in.signs;
-      t.pay = in.payload;
-      t.soff = g_s0 + es;
-      t.poff = g_p0 + ep;
-    }
-  }
-  __device__ __forceinline__ bool rows(const unsigned char*, Stager& st, int32_t* rows,
-                                       uint32_t* flags) {
-    st.wait();
-    if (!t.fast || !small_rs) return false;      // CTA-uniform
-    bool ok = true;
-    int32_t* row = rows + threadIdx.x * kRow;
-    // |bin| < 2^32 and |rs| < 2^21: bin * rs is exact in float64, so
-    // RN(f64(p)) == f64(bin) * f64(rs); then ops.py:199-208 verbatim.
-    // (Larger scalars take the exact 128-bit fallback.)
-    const double od = static_cast<double>(t.o);
-    decode_row_fast(t, [&](int i, int32_t P) {
-      const double pd = __dmul_rn(__dadd_rn(od, i32_to_double(P)), rsd);
-      const double tt = __dmul_rn(d, pd);
-      const double mag = floor(__dadd_rn(fabs(tt), 0.5));
-      ok &= mag < static_cast<double>(kWideLimit - 1);
-      const int32_t mi = __double2loint(__dadd_rn(mag, 6755399441055744.0));
-      row[i] = tt < 0.0 ? -mi : mi;
-    });
-    (void)flags;
-    return grp_and(ok);
-  }
-  __device__ __forceinline__ int64_t lane_bin(int lb, int lane, int len, uint32_t* flags) {
-    const LaneBlock m = lane_block(t, lb & (BPW - 1));
-    uint32_t f = 0;
-    const int64_t q = decode_lane(t.sgn, t.pay, m.w, m.o, m.soff, m.poff, len, lane, &f);
-    *flags |= f;
-    if (f || lane >= len) return 0;
-    return rescale1(product_rn(q, rs), d, flags);
-  }
-};
 
 // ---------------------------------------------------------------------------
 // packing of one block's residual magnitudes (fallback path, lane per element)
@@ -1182,66 +1093,6 @@ __device__ __forceinline__ void finish_moments(Acc acc, uint64_t, void* ws, uint
       st_relaxed(done, 0);   // rearm for the next launch on this workspace
     }
   }
-}
-
-__device__ __noinline__ uint32_t fallback_moments(TileIn t, Acc* acc, bool want_sq) {
-  const int lane = threadIdx.x & 31;
-  uint32_t flags = 0;
-  for (int j = 0; j < BPW; ++j) {
-    const LaneBlock m = lane_block(t, j);
-    if (m.len == 0) break;
-    const int64_t q = decode_lane(t.sgn, t.pay, m.w, m.o, m.soff, m.poff, m.len, lane, &flags);
-    if (lane < m.len) acc->add(q, want_sq);
-  }
-  return flags;
-}
-
-template <bool kWantSq>
-__global__ void __launch_bounds__(kThreads) moments_kernel(StreamIn s, uint64_t* out,
-                                                           uint32_t* err, void* ws) {
-  extern __shared__ __align__(16) unsigned char sm[];
-  __shared__ uint64_t s_bar;
-  __shared__ uint32_t s_tmp[8];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t tile = blockIdx.x;
-  uint32_t flags = 0;
-  TileIn t;
-  stage_tile_in(s, tile, sm, &s_bar, s_tmp, &t, &flags);
-  Acc acc;
-  acc.s = 0;
-  acc.q = 0;
-  acc.q2 = 0;
-  if (t.fast) {
-    // block: S_b = len*O + sum P_i ; Q_b = len*O^2 + 2*O*sum P_i + sum P_i^2
-    int64_t sp = 0;       // |sum P| < 32 * 2^31
-    uint64_t sp2 = 0;     // sum P^2 < 32 * 2^62: 67 bits, carry kept in sp2_hi
-    uint64_t sp2_hi = 0;
-    const int len = t.len;
-    decode_row_fast(t, [&](int i, int32_t P) {
-      if (i < len) {
-        sp += P;
-        if (kWantSq) {
-          const uint64_t p2 = static_cast<uint64_t>(static_cast<int64_t>(P) * P);
-          const uint64_t n2 = sp2 + p2;
-          sp2_hi += n2 < sp2 ? 1u : 0u;
-          sp2 = n2;
-        }
-      }
-    });
-    const __int128 o = t.o;
-    acc.s = o * len + sp;
-    if (kWantSq) {
-      const unsigned __int128 psq = (static_cast<unsigned __int128>(sp2_hi) << 64) | sp2;
-      const __int128 tot = o * o * len + 2 * o * sp + static_cast<__int128>(psq);  // = sum bin^2 >= 0
-      acc.q = static_cast<unsigned __int128>(tot);
-    }
-  } else {
-    flags |= fallback_moments(t, &acc, kWantSq);
-  }
-  flags = __reduce_or_sync(kFull, flags);
-  if (lane == 0 && flags) atomicOr(err, flags);
-  (void)warp;
-  finish_moments(acc, gridDim.x, ws, out);
 }
 
 }  // namespace k32
