@@ -142,6 +142,10 @@ __device__ __forceinline__ void stage_tile(const StreamIn& s, uint64_t t, uint64
 // int32 (|bin| < 2^30).  kFull: a full block (len == 32, no tail checks);
 // otherwise elements past `len` replicate the last live bin.  Fields are read
 // G at a time (G * w <= 32): one window refill check per G fields.
+#ifndef HSZ_REFILL_AHEAD
+#define HSZ_REFILL_AHEAD 1
+#endif
+
 // kAcc: 0 q[i] = bin_i, 1 q[i] += bin_i, 2 q[i] -= bin_i (modulo 2^32)
 template <int kAcc>
 __device__ __forceinline__ void put_bin(int32_t& qi, int32_t v) {
@@ -164,13 +168,27 @@ __device__ __forceinline__ void decode_block_t(const unsigned char* sgn, const u
   const int wg = G * static_cast<int>(w);
   uint64_t win = 0;
   int nb = 0;   // valid bits at the bottom of win
+  // software-pipelined refill: the next payload word is loaded one refill
+  // ahead, so its shared-memory latency overlaps the fields extracted in
+  // between instead of stalling the chain (the read may run one word past
+  // the block -- still inside the staging buffer)
+#if HSZ_REFILL_AHEAD
+  uint32_t nxt = pw[0];
+  int wi = 1;
+#else
   int wi = 0;
+#endif
   int32_t P = o;
   put_bin<kAcc>(q[0], o);
 #pragma unroll
   for (int c = 0; c < (K + G - 1) / G; ++c) {
     if (nb < wg) {
+#if HSZ_REFILL_AHEAD
+      win = (win << 32) | bswap32(nxt);
+      nxt = pw[wi++];
+#else
       win = (win << 32) | bswap32(pw[wi++]);
+#endif
       nb += 32;
     }
 #pragma unroll
@@ -209,6 +227,69 @@ __device__ __forceinline__ void decode_block(const unsigned char* sgn, const uns
     decode_block_t<true, 2, kAcc>(sgn, pay, w, o, len, q);
   } else {
     decode_block_t<true, 1, kAcc>(sgn, pay, w, o, len, q);
+  }
+}
+
+// Register-light block sums for the moment kernels: the same field walk as
+// decode_block_t, but the prefix sums P_i are accumulated on the fly
+// (sum P_i, and sum P_i^2 for kSq) instead of being kept as 32 bins.
+template <bool kFull, int G, bool kSq>
+__device__ __forceinline__ void decode_sum_t(const unsigned char* sgn, const unsigned char* pay,
+                                             uint32_t w, int len, int64_t* sp_out, uint64_t* sp2_out) {
+  const uint32_t sw = bswap32(*reinterpret_cast<const uint32_t*>(sgn));
+  const uint32_t* pw = reinterpret_cast<const uint32_t*>(pay);
+  const uint32_t mask = (1u << w) - 1u;
+  const int wg = G * static_cast<int>(w);
+  uint64_t win = 0;
+  int nb = 0;
+  int wi = 0;
+  int32_t P = 0;
+  int32_t sp = 0;     // |sum P| < 32 * 2^29
+  uint64_t sp2 = 0;   // sum P^2 < 32 * 2^58
+#pragma unroll
+  for (int c = 0; c < (K + G - 1) / G; ++c) {
+    if (nb < wg) {
+      win = (win << 32) | bswap32(pw[wi++]);
+      nb += 32;
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int i = c * G + g;
+      if (i >= K) break;
+      nb -= static_cast<int>(w);
+      if (i == 0) continue;
+      const int32_t mag = static_cast<int32_t>(static_cast<uint32_t>(win >> nb) & mask);
+      const int32_t neg = static_cast<int32_t>(sw << i) >> 31;
+      int32_t d = (mag ^ neg) - neg;
+      if (!kFull) d = (i < len) ? d : 0;
+      P += d;
+      if (kFull || i < len) {
+        sp += P;
+        if (kSq) sp2 += static_cast<uint64_t>(static_cast<int64_t>(P) * P);
+      }
+    }
+  }
+  *sp_out = sp;
+  *sp2_out = sp2;
+}
+
+template <bool kSq>
+__device__ __forceinline__ void decode_sum(const unsigned char* sgn, const unsigned char* pay,
+                                           uint32_t w, int len, int64_t* sp, uint64_t* sp2) {
+  const uint32_t wmax = __reduce_max_sync(kFull, w);
+  *sp = 0;
+  *sp2 = 0;
+  if (w == 0) return;
+  if (len != K) {
+    decode_sum_t<false, 1, kSq>(sgn, pay, w, len, sp, sp2);
+  } else if (wmax <= 8) {
+    decode_sum_t<true, 4, kSq>(sgn, pay, w, len, sp, sp2);
+  } else if (wmax <= 10) {
+    decode_sum_t<true, 3, kSq>(sgn, pay, w, len, sp, sp2);
+  } else if (wmax <= 16) {
+    decode_sum_t<true, 2, kSq>(sgn, pay, w, len, sp, sp2);
+  } else {
+    decode_sum_t<true, 1, kSq>(sgn, pay, w, len, sp, sp2);
   }
 }
 
@@ -590,9 +671,20 @@ constexpr uint32_t kSmulSmemBytes = recode_smem_bytes<kOpSmul>();
 // compute warps + 1 TMA warp; tiles by grid stride (no ordering needed),
 // input double-buffered.
 
+// the moment kernels keep no bins in registers (decode_sum below), so they
+// fit more CTAs per SM; their staging is sized for widths <= 16 (8 KB per
+// tile, wider tiles take the in-place exact path)
+#ifndef HSZ_SUM_PAYCAP
+#define HSZ_SUM_PAYCAP 8192
+#endif
+#ifndef HSZ_SUM_CTAS
+#define HSZ_SUM_CTAS 8
+#endif
+
 template <int kMode>
 struct DecSmem {
-  InTile in[2];
+  using Tile = InTileT<kMode == 2 ? kPayCap : HSZ_SUM_PAYCAP>;
+  Tile in[2];
   alignas(1024) unsigned char out[kMode == 2 ? e32::kBufBytes : 16];   // decompress: value tile
   uint64_t full[2], empty[2];
   uint32_t scan[4];
@@ -604,8 +696,8 @@ constexpr int kDecThreads = kCompute + 32;
 // the 32-lane exact decode of one tile's blocks (any width up to 64, any
 // outlier), reading the sections in place; calls f(local block, lane, bin,
 // live) for every element
-template <class F>
-__device__ __forceinline__ uint32_t exact_tile(const StreamIn& in, const InTile& it, uint32_t es,
+template <class IT, class F>
+__device__ __forceinline__ uint32_t exact_tile(const StreamIn& in, const IT& it, uint32_t es,
                                                uint32_t ep, uint32_t w, int32_t o, int len, F&& f) {
   k32::TileIn t;
   t.w = w;
@@ -697,7 +789,7 @@ template <int kMode>
 #ifndef HSZ_DEC_CTAS
 #define HSZ_DEC_CTAS 5
 #endif
-__global__ void __launch_bounds__(kDecThreads, HSZ_DEC_CTAS)
+__global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_SUM_CTAS)
     decode_pipe_kernel(const __grid_constant__ CUtensorMap omap, StreamIn in, DecF32Sink fs,
                        MomentsSink ms, int use_tma, uint32_t* err) {
   extern __shared__ unsigned char smraw[];
@@ -737,7 +829,7 @@ __global__ void __launch_bounds__(kDecThreads, HSZ_DEC_CTAS)
   for (;; ++i) {
     const int b = i & 1;
     mbar_wait_parity(&S.full[b], (i >> 1) & 1u);
-    const InTile& it = S.in[b];
+    const auto& it = S.in[b];
     const uint64_t cur = it.tile;
     if (cur >= ntiles) break;
     const uint64_t gb = cur * TB + tid;
@@ -761,7 +853,22 @@ __global__ void __launch_bounds__(kDecThreads, HSZ_DEC_CTAS)
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
     if (kMode == 2) e32::bar_sync_n(1, kCompute);
-    if (fast) {
+    if (fast && kMode != 2) {
+      int64_t sp;
+      uint64_t sp2;
+      decode_sum<kMode == 1>(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, len, &sp, &sp2);
+      mbar_arrive_warp(&S.empty[b]);          // staged bytes consumed
+      if (len > 0) {
+        const __int128 oo = o;
+        acc.s += oo * len + sp;
+        if (kMode == 1) {
+          const __int128 tot = oo * oo * len + 2 * oo * sp + static_cast<__int128>(sp2);
+          const unsigned __int128 nq = acc.q + static_cast<unsigned __int128>(tot);
+          acc.q2 += nq < acc.q ? 1u : 0u;
+          acc.q = nq;
+        }
+      }
+    } else if (fast) {
       int32_t q[K];
       decode_block(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, o, len, q);
       mbar_arrive_warp(&S.empty[b]);          // staged bytes consumed
