@@ -293,6 +293,71 @@ __device__ __forceinline__ void decode_sum(const unsigned char* sgn, const unsig
   }
 }
 
+// Decompress without keeping the block's bins: every value is converted as
+// soon as its bin is known (RN32(RN64(2eps * bin)), codec.py:107-115) and
+// written four at a time into the block's swizzled 128-byte row.
+template <bool kFull, int G>
+__device__ __forceinline__ void decode_f32_t(const unsigned char* sgn, const unsigned char* pay,
+                                             uint32_t w, int32_t o, int len, double dd,
+                                             unsigned char* row, uint32_t rsw, bool may_overflow,
+                                             uint32_t* flags) {
+  // a constant block has no sign bytes: its offset may be unaligned (after
+  // the stream's partial last block), so the word is read only when w > 0
+  const uint32_t sw = w ? bswap32(*reinterpret_cast<const uint32_t*>(sgn)) : 0u;
+  const uint32_t* pw = reinterpret_cast<const uint32_t*>(pay);
+  const uint32_t mask = (1u << w) - 1u;
+  const int wg = G * static_cast<int>(w);
+  uint64_t win = 0;
+  int nb = 0;
+  int wi = 0;
+  int32_t P = o;
+  float v[4];
+  bool bad = false;
+#pragma unroll
+  for (int c = 0; c < (K + G - 1) / G; ++c) {
+    if (w && nb < wg) {
+      win = (win << 32) | bswap32(pw[wi++]);
+      nb += 32;
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int i = c * G + g;
+      if (i >= K) break;
+      nb -= static_cast<int>(w);
+      if (i > 0 && w) {
+        const int32_t mag = static_cast<int32_t>(static_cast<uint32_t>(win >> nb) & mask);
+        const int32_t neg = static_cast<int32_t>(sw << i) >> 31;
+        int32_t d = (mag ^ neg) - neg;
+        if (!kFull) d = (i < len) ? d : 0;
+        P += d;
+      }
+      v[i & 3] = __double2float_rn(__dmul_rn(dd, i32_to_double(P)));
+      if (may_overflow) bad |= !isfinite(v[i & 3]);
+      if ((i & 3) == 3)
+        *reinterpret_cast<float4*>(row + (((i >> 2) ^ rsw) << 4)) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+  }
+  if (bad) *flags |= HSZ_ERR_OUTPUT_NONFINITE;
+}
+
+__device__ __forceinline__ void decode_f32(const unsigned char* sgn, const unsigned char* pay,
+                                           uint32_t w, int32_t o, int len, double dd,
+                                           unsigned char* row, uint32_t rsw, bool may_overflow,
+                                           uint32_t* flags) {
+  const uint32_t wmax = __reduce_max_sync(kFull, w);
+  if (len != K) {
+    decode_f32_t<false, 1>(sgn, pay, w, o, len, dd, row, rsw, may_overflow, flags);
+  } else if (wmax <= 8) {
+    decode_f32_t<true, 4>(sgn, pay, w, o, len, dd, row, rsw, may_overflow, flags);
+  } else if (wmax <= 10) {
+    decode_f32_t<true, 3>(sgn, pay, w, o, len, dd, row, rsw, may_overflow, flags);
+  } else if (wmax <= 16) {
+    decode_f32_t<true, 2>(sgn, pay, w, o, len, dd, row, rsw, may_overflow, flags);
+  } else {
+    decode_f32_t<true, 1>(sgn, pay, w, o, len, dd, row, rsw, may_overflow, flags);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // re-encoding operations: scalar multiply (kOp 0) and element-wise add / sub
 // of two streams (kOp 1 / 2, ops.py:163-192) share one persistent kernel --
@@ -674,6 +739,12 @@ constexpr uint32_t kSmulSmemBytes = recode_smem_bytes<kOpSmul>();
 // the moment kernels keep no bins in registers (decode_sum below), so they
 // fit more CTAs per SM; their staging is sized for widths <= 16 (8 KB per
 // tile, wider tiles take the in-place exact path)
+#ifndef HSZ_F32_STREAM
+#define HSZ_F32_STREAM 1
+#endif
+#ifndef HSZ_F32_PAYCAP
+#define HSZ_F32_PAYCAP 8192
+#endif
 #ifndef HSZ_SUM_PAYCAP
 #define HSZ_SUM_PAYCAP 8192
 #endif
@@ -683,7 +754,7 @@ constexpr uint32_t kSmulSmemBytes = recode_smem_bytes<kOpSmul>();
 
 template <int kMode>
 struct DecSmem {
-  using Tile = InTileT<kMode == 2 ? kPayCap : HSZ_SUM_PAYCAP>;
+  using Tile = InTileT<kMode == 2 ? HSZ_F32_PAYCAP : HSZ_SUM_PAYCAP>;
   Tile in[2];
   alignas(1024) unsigned char out[kMode == 2 ? e32::kBufBytes : 16];   // decompress: value tile
   uint64_t full[2], empty[2];
@@ -787,7 +858,7 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 // kMode 0: mean (S), 1: variance (S, Q), 2: decompress to float32
 template <int kMode>
 #ifndef HSZ_DEC_CTAS
-#define HSZ_DEC_CTAS 5
+#define HSZ_DEC_CTAS 6
 #endif
 __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_SUM_CTAS)
     decode_pipe_kernel(const __grid_constant__ CUtensorMap omap, StreamIn in, DecF32Sink fs,
@@ -868,6 +939,10 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
           acc.q = nq;
         }
       }
+    } else if (fast && HSZ_F32_STREAM) {
+      decode_f32(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, o, len, fs.d, S.out + tid * 128,
+                 static_cast<uint32_t>(tid & 7), fs.may_overflow, &flags);
+      mbar_arrive_warp(&S.empty[b]);          // staged bytes consumed
     } else if (fast) {
       int32_t q[K];
       decode_block(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, o, len, q);
