@@ -342,7 +342,10 @@ __device__ __forceinline__ void resolve_tile(Smem& S, const k32::EncodeOut& out,
 // payload (4-5 KB typical, 15.9 KB worst case), so up to 4 tiles can wait
 // for their offsets without stalling the compute warps.
 
-constexpr uint32_t kRingBytes = 16384;
+#ifndef HSZ_RING_BYTES
+#define HSZ_RING_BYTES 16384
+#endif
+constexpr uint32_t kRingBytes = HSZ_RING_BYTES;
 constexpr int kSlots = 4;
 
 struct RingRec {
