@@ -50,6 +50,11 @@ def _torch():
 def smooth_field(dims, seed: int = 0, dtype: str = "f32") -> codec.RawArray:
     """A few low-frequency cosine waves per axis, deterministic amplitudes
     and phases (the reference's default bench / distsim field)."""
+    return codec.RawArray(smooth_values(dims, seed), tuple(int(d) for d in dims), dtype)
+
+
+def smooth_values(dims, seed: int = 0) -> np.ndarray:
+    """The float64 values of smooth_field, flattened."""
     rng = np.random.default_rng(seed)
     dims = tuple(int(d) for d in dims)
     fld = np.zeros(dims, dtype=np.float64)
@@ -63,7 +68,7 @@ def smooth_field(dims, seed: int = 0, dtype: str = "f32") -> codec.RawArray:
         shape = [1] * len(dims)
         shape[axis] = d
         fld += wave.reshape(shape)
-    return codec.RawArray(fld.ravel(), dims, dtype)
+    return fld.ravel()
 
 
 # ---------------------------------------------------------------------------
