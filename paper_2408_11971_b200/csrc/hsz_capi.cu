@@ -644,6 +644,9 @@ static int launch_recode(const d32::StreamIn& a, const d32::StreamIn& b, const d
     int per_sm = 0, sms = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, e32::kThreadsWS, smem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    #ifdef HSZ_RECODE_CTAS_CAP
+    if (per_sm > HSZ_RECODE_CTAS_CAP) per_sm = HSZ_RECODE_CTAS_CAP;
+#endif
     resident = (per_sm > 0 ? per_sm : 1) * sms;
     resident_dev = dev;
   }
