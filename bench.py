@@ -635,8 +635,8 @@ def run_reference(args):
     cfg = dict(W.CONFIGS[args.config])
     if args.config == 5:
         cfg["dims"] = (256, 2048, 2048)          # one 2^30-value slab per rank
-    if args.config == 2:
-        x = W.config2()
+    if args.config in (2, 5):
+        x = W.config2()          # config 5 = config 2's spectrum at 2048^3: a bounded sample of it
     else:
         x = W.config4()
     procs = _cpu_cores()
