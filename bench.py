@@ -640,7 +640,7 @@ def run_reference(args):
     else:
         x = W.config4()
     procs = _cpu_cores()
-    sample = min(x.size, 1 << 21)
+    sample = min(x.size, 1 << 25)       # the whole config-2 field (a bounded prefix of larger ones)
     xs = x[:sample]
     for _ in range(args.warmup):
         _cpu_run(xs, cfg, procs)
