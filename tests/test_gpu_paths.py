@@ -159,3 +159,25 @@ def test_chain_device_resident_matches_host(H):
     assert H.mean(z) == O.mean_from(S, n, eps)
     assert H.variance(z) == O.variance_from(S, Q, n, eps)
     assert H.decompress(z).values.cpu().numpy().tobytes() == O.decompress(zr).tobytes()
+
+
+def test_compress_wide_tiles_mixed(H):
+    """Float32 fields whose tiles mix register-path blocks with blocks whose
+    bins reach 2^30 (the compressor's exact warp-per-block path places those
+    tiles itself): stream bytes against the oracle, and the bins re-encode to
+    the same bytes."""
+    import torch
+
+    import hoszp_oracle as O
+
+    rng = np.random.default_rng(5)
+    for _ in range(6):
+        n = 4096 * int(rng.integers(2, 12)) + int(rng.integers(0, 40))
+        x = (rng.normal(0, 1, n) * 10 + 100).astype(np.float32)
+        for t in rng.choice(n // 4096, size=max(1, n // 8192), replace=False):
+            x[t * 4096 + 5: t * 4096 + 300: 7] = 3.0e6      # bins ~1.5e9 inside blocks
+        p = H.QuantParams(1e-3, (n,), 32, "f32")
+        s = H.compress(H.RawArray(torch.from_numpy(x).cuda(), (n,), "f32"), p)
+        want = O.serialize(O.compress(x, 1e-3, (n,), 32, "f32"))
+        assert H.serialize(s.to_host()) == want
+        assert H.serialize(H.encode_from_quant(H.decode_to_quant(s)).to_host()) == want

@@ -14,6 +14,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2408_11971_b200 as H  # noqa: E402
@@ -73,6 +74,7 @@ def main():
     s = H.compress(raw, p)
     z0 = H.scalar_add(H.negate(s), cfg["sadd"])
     z = H.scalar_mul(z0, cfg["smul"])
+    qz = H.decode_to_quant(z)
     ctx = s.ctx
     wsp, wsb = ctx.workspace(1, 1)
     mm = ctx.empty(2, torch.float64)
@@ -89,6 +91,9 @@ def main():
         "variance": lambda: O.moments_device(z, True),
         "decompress": lambda: H.decompress(z),
         "elementwise_add": lambda: H.elementwise_add(s, z0),
+        "decode_to_quant": lambda: H.decode_to_quant(z),
+        "encode_from_quant": lambda: H.encode_from_quant(qz),
+        "decompress_f64": lambda: H.decompress(z, out_dtype=np.float64),
     }
     if a.ops:
         fns = {k: v for k, v in fns.items() if k in a.ops.split(",")}
