@@ -69,3 +69,20 @@ def test_argument_errors_do_not_touch_the_gpu(lib):
                             None, 0, None) == -1
     assert lib.hsz_decode(None, None, None, None, None, 10, 32, 0.1, 0, None, None, None) == -1
     assert lib.hsz_scalar_add(None, None, 0, 1, None, None) == -1
+    z = [None] * 10
+    assert lib.hsz_elementwise(*z, 10, 32, 0, None, None, None, 0, None, 0, None, None, None, None,
+                               0, None) == -1
+    assert lib.hsz_hadamard(*z, 10, 32, 0.1, None, None, None, 0, None, 0, None, None, None, None,
+                            0, None) == -1
+    assert lib.hsz_pair_stats(*z, 10, 32, None, None, None, None) == -1
+    assert lib.hsz_block_means(None, None, None, None, None, 10, 32, 0.1, None, None, None,
+                               None) == -1
+    assert lib.hsz_moments_mb(None, None, None, None, None, 10, 32, 0, None, None, None, 0, None, 1,
+                              None) == -1
+    assert lib.hsz_minmax_mb(None, 0, 10, None, None, None, 0, None, 1, None) == -1
+
+
+def test_scratch_queries(lib):
+    assert lib.hsz_elementwise_scratch_size(1000, 32) == 0        # one fused pass
+    assert lib.hsz_elementwise_scratch_size(1000, 33) == 8000
+    assert lib.hsz_bivariate_scratch_size(1000, 32) == 16000
