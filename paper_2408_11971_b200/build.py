@@ -49,7 +49,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
     extra = os.environ.get("HSZ_NVCC_EXTRA", "").split()   # experiments: -D knobs
-    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", LIB + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]
+    tmp = f"{LIB}.{os.getpid()}.tmp"     # concurrent builders (spawned ranks) do not collide
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)
@@ -57,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if res.returncode != 0:
         sys.stderr.write((res.stdout or "") + (res.stderr or ""))
         raise RuntimeError(f"nvcc failed ({res.returncode}) building {LIB}")
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(tmp, LIB)
     return LIB
 
 

@@ -376,6 +376,37 @@ class DeviceStream:
         ds._totals = (len(cs.sign_planes), len(cs.payload))
         return ds
 
+    @classmethod
+    def from_sections(cls, params: QuantParams, widths, outliers, signs, payload,
+                      ctx: Context = None) -> "DeviceStream":
+        """A stream from its four sections given as device uint8 tensors
+        (e.g. views into a collective's receive buffer): copied into one
+        256-byte aligned allocation with the decoders' slack, tile-offset
+        cache rebuilt on the device.  Asynchronous; the section lengths are
+        the caller's (checked against the widths by the tile-offset totals
+        only when ``totals()`` is asked for)."""
+        t = require_cuda()
+        ctx = ctx or context()
+        n, k = params.element_count, params.block_len
+        B = params.block_count
+        ns, npay = int(signs.numel()), int(payload.numel())
+        secs, (w, o, s, py, toff), scap, pcap = new_stream_buffers(ctx, params, payload_cap=npay)
+        buf = secs[0][0]
+        with t.cuda.stream(ctx.stream):
+            buf[0:B].copy_(widths, non_blocking=True)
+            buf[secs[1][1]:secs[1][1] + 4 * B].copy_(outliers, non_blocking=True)
+            if ns:
+                buf[secs[2][1]:secs[2][1] + ns].copy_(signs, non_blocking=True)
+            if npay:
+                buf[secs[3][1]:secs[3][1] + npay].copy_(payload, non_blocking=True)
+        wsp, wsb = ctx.workspace(n, k)
+        N.check(ctx.lib.hsz_tile_offsets(w, n, k, toff, ctx.err_ptr, wsp, wsb, ctx.handle),
+                "hsz_tile_offsets")
+        ds = cls(params, *secs, ctx, scap, pcap)
+        ds._ptrs = (w, o, s, py, toff)
+        ds._totals = (ns, npay)
+        return ds
+
     def __eq__(self, other):
         if isinstance(other, DeviceStream):
             other = other.to_host()

@@ -41,9 +41,11 @@ def _headroom(streams) -> bool:
     return total <= _I64_MAX
 
 
-def aggregate_homomorphic(streams, threads: int = 1):
+def aggregate_homomorphic(streams, threads: int = 1, *, headroom=None):
     """Left fold of element-wise addition in the residual domain
-    (distsim.py:80-96)."""
+    (distsim.py:80-96).  ``headroom`` overrides the int64-headroom test of
+    distsim.py:106-110 (the multi-GPU fold of block-range slices takes it
+    from the whole streams' widths, so every rank picks the same branch)."""
     streams = list(streams)
     if not streams:
         raise ValueError("need at least one stream")
@@ -51,7 +53,9 @@ def aggregate_homomorphic(streams, threads: int = 1):
         _check_params(streams[0], s)
     if len(streams) == 1:
         return streams[0]
-    if not _headroom(streams):
+    if headroom is None:
+        headroom = _headroom(streams)
+    if not headroom:
         acc = streams[0]
         for s in streams[1:]:
             acc = elementwise_add(acc, s, threads)

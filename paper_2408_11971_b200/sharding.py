@@ -15,8 +15,11 @@ exchange.  Only three tiny, latency-bound collectives exist:
 
 A second pattern -- every rank holds a whole stream of the same geometry
 (ensemble members, time steps) and all want their sum -- is
-``allreduce_streams``: one all_gather of the serialized (compressed) streams,
-then the residual-domain fold of distsim.py:80-103 (``distsim.py`` here).
+``allreduce_streams``: a reduce-scatter over tile-aligned block ranges (one
+all_to_all of compressed slices, each rank folds its range with the
+residual-domain fold of distsim.py:80-103) and an all_gather of the
+compressed partial sums.  ``gather_streams`` (every rank gets every stream)
+stays for callers that want the operands themselves.
 
 The shard's sections, concatenated in rank order at the C2 offsets, are
 byte-identical to the single-GPU stream of the whole field (tested in
@@ -135,12 +138,133 @@ class Collectives:
 
     def allreduce_streams(self, stream, fold=None):
         """Every rank gets the homomorphic sum of all ranks' streams (the
-        residual-domain fold of distsim.py:80-103, on this rank's GPU by
-        default; `fold` overrides it, e.g. with the CPU oracle in tests)."""
-        streams = self.gather_streams(stream)
-        if fold is None:
-            from .distsim import aggregate_homomorphic as fold
-        return fold(streams)
+        residual-domain fold of distsim.py:80-103 across ranks), as a
+        reduce-scatter over tile-aligned block ranges followed by an
+        all-gather of the compressed partial sums:
+
+        1. every rank cuts its stream into ``world`` block-range slices at
+           tile boundaries (offsets from the tile-offset cache: a block range
+           of a stream is itself a stream, FORMAT.md blocks being
+           byte-aligned);
+        2. one ``all_to_all``: rank r receives every rank's slice r;
+        3. rank r folds the ``world`` slices of its range on its GPU (``fold``
+           overrides the fold, e.g. with the CPU oracle in tests).  The
+           int64-headroom branch of distsim.py:106-110 is chosen from the
+           whole streams' widths (allgathered), so every rank takes the
+           branch the single-process fold takes;
+        4. errors are agreed across ranks -- the first failing fold step,
+           then the reference's precedence (errors.raise_for_flags) -- so
+           every rank raises what the single-process fold raises;
+        5. one ``all_gather`` of the partial sums; concatenated in rank order
+           they are the aggregate stream, byte-identical to the single-process
+           fold.
+
+        Per rank: (world-1)/world of one stream out and in, plus the
+        compressed result, and one stream's worth of fold work."""
+        from .device import DeviceStream
+        from .errors import ParamsMismatch
+
+        t = self.torch
+        world, me = self.world, self.rank
+        on_dev = isinstance(stream, DeviceStream)
+        p = stream.params
+        n, k, B = p.element_count, p.block_len, p.block_count
+        cuts, so, po, maxw = _cut_points(stream, world)
+        # exchange: params digest, max width, and the bytes of every slice
+        rows = self._allgather_i64([_params_digest(p), maxw]
+                                   + [so[j + 1] - so[j] for j in range(world)]
+                                   + [po[j + 1] - po[j] for j in range(world)])
+        if any(r[0] != rows[0][0] for r in rows):
+            raise ParamsMismatch("operand params differ across ranks")
+        headroom = sum((1 << r[1]) - 1 for r in rows) <= (1 << 63) - 1
+
+        # 1-2: slices out, my range's slices in
+        secs = _section_bytes(stream)
+        out_parts, in_splits = [], []
+        for j in range(world):
+            b0, b1 = cuts[j], cuts[j + 1]
+            out_parts += [secs[0][b0:b1], secs[1][4 * b0:4 * b1], secs[2][so[j]:so[j + 1]],
+                          secs[3][po[j]:po[j + 1]]]
+            in_splits.append(5 * (b1 - b0) + (so[j + 1] - so[j]) + (po[j + 1] - po[j]))
+        send = t.cat(out_parts).to(self.device)
+        mb0, mb1 = cuts[me], cuts[me + 1]
+        nb = mb1 - mb0
+        sizes = [(rows[i][2 + me], rows[i][2 + world + me]) for i in range(world)]
+        out_splits = [5 * nb + ss + ps for ss, ps in sizes]
+        recv = t.empty(sum(out_splits), dtype=t.uint8, device=self.device)
+        self.dist.all_to_all_single(recv, send, out_splits, in_splits, group=self.group)
+
+        # 3-4: fold my range
+        ctx = stream.ctx if on_dev else None
+        part = None
+        if nb:
+            from .model import QuantParams
+
+            pr = QuantParams(p.eps, (min(mb1 * k, n) - mb0 * k,), k, p.dtype)
+            subs, pos = [], 0
+            for ss, ps in sizes:
+                w, o, sg, py = _split(recv, pos, (nb, 4 * nb, ss, ps))
+                pos += 5 * nb + ss + ps
+                subs.append(_make_stream(pr, w, o, sg, py, ctx))
+        if fold is not None:
+            part = self._agreed(lambda: fold(subs) if nb else None, ctx)
+        elif headroom:
+            from .distsim import aggregate_homomorphic
+
+            part = self._agreed(
+                lambda: aggregate_homomorphic(subs, headroom=True) if nb else None, ctx)
+        else:
+            from .ops import elementwise_add
+
+            part = subs[0] if nb else None
+            for i in range(1, world):
+                part = self._agreed(lambda: elementwise_add(part, subs[i]) if nb else None, ctx)
+
+        # 5: partial sums to everyone, concatenated in rank order
+        if nb:
+            rsec = _section_bytes(part)
+            blob = t.cat(rsec).to(self.device)
+            mine = [int(rsec[2].numel()), int(rsec[3].numel())]
+        else:
+            blob = t.empty(0, dtype=t.uint8, device=self.device)
+            mine = [0, 0]
+        rrows = self._allgather_i64([blob.numel()] + mine)
+        top = max(r[0] for r in rrows)
+        padded = t.zeros(max(top, 1), dtype=t.uint8, device=self.device)
+        padded[:blob.numel()] = blob
+        got = [t.empty_like(padded) for _ in range(world)]
+        self.dist.all_gather(got, padded, group=self.group)
+        cols = [[], [], [], []]
+        for i in range(world):
+            nbi = cuts[i + 1] - cuts[i]
+            for c, x in zip(cols, _split(got[i], 0, (nbi, 4 * nbi, rrows[i][1], rrows[i][2]))):
+                c.append(x)
+        full = [t.cat(c) for c in cols]
+        return _make_stream(p, *full, ctx)
+
+    def _agreed(self, step, ctx):
+        """Run one fold step and agree on its outcome across ranks: if any
+        rank failed, every rank raises the error of highest precedence."""
+        from .errors import HoszpError, raise_for_flags
+
+        err, res = None, None
+        try:
+            res = step()
+            if ctx is not None:
+                flags = ctx.read_flags()
+                if flags:
+                    raise_for_flags(flags, "allreduce_streams")
+        except (HoszpError, ValueError) as e:
+            err = e
+        code = 0 if err is None else _precedence(err)
+        codes = [r[0] for r in self._allgather_i64([code])]
+        bad = [c for c in codes if c]
+        if bad:
+            c = min(bad)
+            if err is not None and code == c:
+                raise err
+            raise _EXC_BY_CODE[c](f"allreduce_streams: fold failed on rank {codes.index(c)}")
+        return res
 
     def write_sharded(self, path, params, layout: ShardLayout, stream):
         """Every rank writes its shard's sections straight into one ``.hsz``
@@ -200,6 +324,117 @@ def _from_limbs(limbs):
         S -= 1 << 128
     Q = u[2] | (u[3] << 64) | (u[4] << 128)
     return S, Q
+
+
+# -- block-range slices of whole streams (allreduce_streams) -------------------
+_TILE_BLOCKS = 128    # blocks per tile of the device tile-offset cache (hsz_b200.h)
+
+
+def tile_block_range(nblocks: int, rank: int, world: int):
+    """Contiguous block range [b0, b1) of `rank`, cut at tile boundaries."""
+    T = -(-nblocks // _TILE_BLOCKS)
+    t0, t1 = block_range(T, rank, world)
+    return min(t0 * _TILE_BLOCKS, nblocks), min(t1 * _TILE_BLOCKS, nblocks)
+
+
+def _cut_points(stream, world):
+    """Block, sign-byte and payload-byte offsets of the world+1 cut points of
+    `stream`, and its maximum width.  Device streams read them from the
+    tile-offset cache (one small copy); host streams from the section sizes."""
+    from .device import DeviceStream
+
+    B = stream.params.block_count
+    cuts = [tile_block_range(B, j, world)[0] for j in range(world)] + [B]
+    if isinstance(stream, DeviceStream):
+        t = __import__("torch")
+        tiles = [-(-b // _TILE_BLOCKS) for b in cuts]
+        idx = t.tensor([2 * x for x in tiles] + [2 * x + 1 for x in tiles], dtype=t.int64,
+                       device=stream.ctx.device)
+        sel = stream.toff.index_select(0, idx)
+        mw = stream.widths.max().to(t.int64).reshape(1)
+        sel_h, mw_h = stream.ctx.fetch_checked([sel, mw], "allreduce_streams")
+        so = [int(v) for v in sel_h[:world + 1]]
+        po = [int(v) for v in sel_h[world + 1:]]
+        return cuts, so, po, int(mw_h[0])
+    cs = np.concatenate([[0], np.cumsum(stream.sign_sizes(), dtype=np.int64)])
+    cp = np.concatenate([[0], np.cumsum(stream.payload_sizes(), dtype=np.int64)])
+    maxw = int(stream.widths.max()) if B else 0
+    return cuts, [int(cs[b]) for b in cuts], [int(cp[b]) for b in cuts], maxw
+
+
+def _section_bytes(stream):
+    """The four sections of a stream as flat uint8 torch tensors (device
+    views for a DeviceStream, CPU tensors for a host stream)."""
+    import torch as t
+
+    from .device import DeviceStream
+
+    if isinstance(stream, DeviceStream):
+        sb, pb = stream.totals()
+        return [stream.widths, stream.outliers.view(t.uint8), stream.signs[:sb],
+                stream.payload[:pb]]
+    return [t.from_numpy(np.ascontiguousarray(stream.widths, dtype=np.uint8).copy()),
+            t.from_numpy(np.ascontiguousarray(stream.outliers, dtype="<i4").view(np.uint8).copy()),
+            t.from_numpy(np.frombuffer(stream.sign_planes, dtype=np.uint8).copy()),
+            t.from_numpy(np.frombuffer(stream.payload, dtype=np.uint8).copy())]
+
+
+def _split(buf, pos, lens):
+    out = []
+    for ln in lens:
+        out.append(buf[pos:pos + ln])
+        pos += ln
+    return out
+
+
+def _make_stream(params, w, o, sg, py, ctx):
+    """A stream of `params` from its four uint8 sections: on `ctx`'s device
+    (ctx given) or on the host."""
+    if ctx is not None:
+        from .device import DeviceStream
+
+        dev = ctx.device
+        return DeviceStream.from_sections(params, w.to(dev), o.to(dev), sg.to(dev), py.to(dev),
+                                          ctx)
+    from .model import CompressedStream
+
+    return CompressedStream(params, w.cpu().numpy(), o.cpu().numpy().view("<i4"),
+                            sg.cpu().numpy().tobytes(), py.cpu().numpy().tobytes())
+
+
+def _params_digest(p) -> int:
+    import hashlib
+
+    key = repr((float(p.eps).hex(), tuple(p.dims), int(p.block_len), p.dtype)).encode()
+    return int.from_bytes(hashlib.sha1(key).digest()[:8], "little", signed=True)
+
+
+def _precedence(err) -> int:
+    """errors.raise_for_flags order (1 = highest)."""
+    from .errors import CapacityExceeded, GeometryMismatch, OutlierOverflow, QuantOverflow
+
+    for code, cls in ((2, GeometryMismatch), (3, QuantOverflow), (4, OutlierOverflow),
+                      (5, CapacityExceeded)):
+        if isinstance(err, cls):
+            return code
+    return 1 if isinstance(err, ValueError) else 6
+
+
+def _exc_by_code():
+    from .errors import (CapacityExceeded, GeometryMismatch, HoszpError, OutlierOverflow,
+                         QuantOverflow)
+
+    return {1: ValueError, 2: GeometryMismatch, 3: QuantOverflow, 4: OutlierOverflow,
+            5: CapacityExceeded, 6: HoszpError}
+
+
+class _LazyCodes(dict):
+    def __missing__(self, code):
+        self.update(_exc_by_code())
+        return dict.__getitem__(self, code)
+
+
+_EXC_BY_CODE = _LazyCodes()
 
 
 def assemble(params, layouts, shards):

@@ -116,6 +116,17 @@ def test_block_ranges_partition_exactly():
     assert all(a % 32 == 0 for a, _ in ranges) and ranges[-1][1] == n
 
 
+def test_tile_block_ranges_partition_exactly():
+    from paper_2408_11971_b200.sharding import tile_block_range
+
+    for nb in (1, 127, 128, 129, 128 * 7 + 3, 100_000):
+        for world in (1, 2, 3, 5, 8):
+            rs = [tile_block_range(nb, r, world) for r in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == nb
+            assert all(rs[i][1] == rs[i + 1][0] for i in range(world - 1))
+            assert all((b0 % 128 == 0 or b0 == nb) and b0 <= b1 for b0, b1 in rs)
+
+
 def test_limb_packing_round_trip():
     from paper_2408_11971_b200.sharding import _from_limbs, _to_limbs
 
@@ -123,7 +134,15 @@ def test_limb_packing_round_trip():
         assert _from_limbs(_to_limbs(S, Q)) == (S, Q)
 
 
-def _stream_worker(rank, world, port, outdir):
+STREAM_CASES = {
+    # name: (n, per-rank field seeds offset, eps)
+    "ragged": (32 * 300 + 7, 10, 0.01),
+    "multi_tile": (32 * 128 * 5 + 19, 20, 0.002),
+    "one_tile": (32 * 50, 30, 0.01),          # fewer tiles than ranks: empty ranges
+}
+
+
+def _stream_worker(rank, world, port, outdir, case):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import torch.distributed as dist
@@ -137,37 +156,95 @@ def _stream_worker(rank, world, port, outdir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         coll = Collectives()
-        n = 32 * 300 + 7
-        x = _field(n, seed=10 + rank)
-        mine = H.deserialize(O.serialize(O.compress(x, 0.01, (n,), 32, "f32")))
+        n, seed, eps = STREAM_CASES[case]
+        x = _field(n, seed=seed + rank)
+        mine = H.deserialize(O.serialize(O.compress(x, eps, (n,), 32, "f32")))
 
         def oracle_fold(streams):
-            return O.aggregate_homomorphic([O.deserialize(H.serialize(s)) for s in streams])
+            agg = O.aggregate_homomorphic([O.deserialize(H.serialize(s)) for s in streams])
+            return H.deserialize(O.serialize(agg))
 
         got = coll.allreduce_streams(mine, fold=oracle_fold)
         parts = [None] * world
-        dist.all_gather_object(parts, O.serialize(got))
+        dist.all_gather_object(parts, H.serialize(got))
         if rank == 0:
             np.save(os.path.join(outdir, "agg.npy"), np.array(parts, dtype=object), allow_pickle=True)
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_allreduce_streams(tmp_path, world):
-    """Every rank ends with the homomorphic sum of all ranks' streams; the
-    gathered operands arrive byte-exact and in rank order."""
+@pytest.mark.parametrize("world,case", [(2, "ragged"), (3, "ragged"), (2, "multi_tile"),
+                                        (3, "multi_tile"), (3, "one_tile")])
+def test_allreduce_streams(tmp_path, world, case):
+    """Reduce-scatter over tile-aligned block ranges + all-gather of the
+    partial sums: every rank ends with the single-process fold's stream,
+    byte for byte (slices folded by the oracle, reassembled here)."""
     import torch.multiprocessing as mp
 
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import hoszp_oracle as O
 
-    mp.spawn(_stream_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_stream_worker, args=(world, _free_port(), str(tmp_path), case), nprocs=world,
+             join=True)
     parts = list(np.load(tmp_path / "agg.npy", allow_pickle=True))
-    n = 32 * 300 + 7
-    streams = [O.compress(_field(n, seed=10 + r), 0.01, (n,), 32, "f32") for r in range(world)]
+    n, seed, eps = STREAM_CASES[case]
+    streams = [O.compress(_field(n, seed=seed + r), eps, (n,), 32, "f32") for r in range(world)]
     want = O.serialize(O.aggregate_homomorphic(streams))
     assert all(p == want for p in parts)
+
+
+def _err_worker(rank, world, port, outdir):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import torch.distributed as dist
+
+    import paper_2408_11971_b200 as H
+    from paper_2408_11971_b200.sharding import Collectives
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        coll = Collectives()
+        n = 32 * 128 * 3
+        p = H.QuantParams(0.5, (n,), 32, "f32")
+        mine = H.CompressedStream(p, np.zeros(n // 32, np.uint8), np.full(n // 32, 7, np.int32),
+                                  b"", b"")
+
+        def failing_fold(streams):
+            # only the rank owning the last tile fails; all ranks must raise
+            if coll.rank == world - 1:
+                raise H.OutlierOverflow("outlier out of signed 32-bit range")
+            return streams[0]
+
+        try:
+            coll.allreduce_streams(mine, fold=failing_fold)
+            outcome = "none"
+        except H.OutlierOverflow:
+            outcome = "OutlierOverflow"
+        q = H.QuantParams(0.25 if rank == 1 else 0.5, (n,), 32, "f32")
+        other = H.CompressedStream(q, mine.widths, mine.outliers, b"", b"")
+        try:
+            coll.allreduce_streams(other)
+            mismatch = "none"
+        except H.ParamsMismatch:
+            mismatch = "ParamsMismatch"
+        parts = [None] * world
+        dist.all_gather_object(parts, (outcome, mismatch))
+        if rank == 0:
+            np.save(os.path.join(outdir, "err.npy"), np.array(parts, dtype=object), allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_allreduce_streams_errors_agree(tmp_path):
+    """A fold error on one rank is raised on every rank (same class); params
+    differing across ranks raise ParamsMismatch everywhere (ops.py:77-81)."""
+    import torch.multiprocessing as mp
+
+    mp.spawn(_err_worker, args=(3, _free_port(), str(tmp_path)), nprocs=3, join=True)
+    parts = list(np.load(tmp_path / "err.npy", allow_pickle=True))
+    assert all(tuple(p) == ("OutlierOverflow", "ParamsMismatch") for p in parts)
 
 
 def _write_worker(rank, world, port, path):
