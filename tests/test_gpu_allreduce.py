@@ -103,3 +103,47 @@ def test_allreduce_streams_device(tmp_path, world, case):
     for blob, m in parts:
         assert blob == ws
         assert m == O.mean_from(S, n, eps)
+
+
+def _nccl_worker(rank, world, port, outdir):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import torch
+    import torch.distributed as dist
+
+    import hoszp_oracle as O
+    import paper_2408_11971_b200 as H
+    from paper_2408_11971_b200.device import DeviceStream
+    from paper_2408_11971_b200.sharding import Collectives
+
+    torch.cuda.set_device(0)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=rank, world_size=world)
+    try:
+        coll = Collectives()
+        assert coll.device.type == "cuda"
+        n, eps = CASES["fields"]
+        mine = DeviceStream.from_host(H.deserialize(O.serialize(_operand("fields", n, eps, 0))))
+        got = coll.allreduce_streams(mine)
+        with open(os.path.join(outdir, "nccl.bin"), "wb") as f:
+            f.write(H.serialize(got.to_host()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_allreduce_streams_nccl_single_rank(tmp_path):
+    """The NCCL code path (device-resident send/receive buffers, no host
+    staging) at world size 1: the aggregate of one stream is the stream."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import torch.multiprocessing as mp
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import hoszp_oracle as O
+
+    mp.spawn(_nccl_worker, args=(1, _free_port(), str(tmp_path)), nprocs=1, join=True)
+    n, eps = CASES["fields"]
+    assert (tmp_path / "nccl.bin").read_bytes() == O.serialize(_operand("fields", n, eps, 0))
