@@ -243,8 +243,11 @@ __device__ __forceinline__ void decode_sum_t(const unsigned char* sgn, const uns
   uint64_t win = 0;
   int nb = 0;
   int wi = 0;
-  int32_t P = 0;
-  int32_t sp = 0;     // |sum P| < 32 * 2^29
+  int32_t P = 0;      // |P| <= 31 * (2^w - 1) < 2^29
+  // sum P <= 496 * (2^w - 1): int32 holds it up to w = 22 (G >= 2 means
+  // w <= 16); the one-field-per-step path serves widths up to kFastW = 24
+  using SumT = std::conditional_t<(G >= 2), int32_t, int64_t>;
+  SumT sp = 0;
   uint64_t sp2 = 0;   // sum P^2 < 32 * 2^58
 #pragma unroll
   for (int c = 0; c < (K + G - 1) / G; ++c) {
@@ -966,7 +969,7 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
         int64_t sp = 0;
         uint64_t sp2 = 0;
         if (len == K) {
-          int32_t sp32 = 0;   // |sum P| < 32 * 2^29
+          int64_t sp32 = 0;   // sum P reaches 496 * 2^24 > 2^31
 #pragma unroll
           for (int k = 1; k < K; ++k) {
             const int32_t P = q[k] - o;   // |P| < 2^29

@@ -181,3 +181,25 @@ def test_compress_wide_tiles_mixed(H):
         want = O.serialize(O.compress(x, 1e-3, (n,), 32, "f32"))
         assert H.serialize(s.to_host()) == want
         assert H.serialize(H.encode_from_quant(H.decode_to_quant(s)).to_host()) == want
+
+
+@pytest.mark.parametrize("w", [17, 20, 22, 24])
+def test_moments_monotone_wide_residuals(H, w):
+    """Register-path block sums at the widest register widths with same-sign
+    residuals: sum_i P_i reaches 496 * 2^w (beyond int32 for w >= 22)."""
+    n = 4096 * 4 + 45
+    rng = np.random.default_rng(w)
+    d = rng.integers(1 << (w - 1), 1 << w, n).astype(np.int64)
+    blk = np.arange(n) // 32
+    d *= rng.choice([-1, 1], blk[-1] + 1)[blk]                 # rising and falling ramps
+    d[::32] = rng.integers(-(1 << 28), 1 << 28, d[::32].size)   # block starts: the outliers
+    bins = np.zeros(n, dtype=np.int64)
+    for b in range(blk[-1] + 1):                               # per-block ramps
+        sl = slice(32 * b, min(32 * b + 32, n))
+        bins[sl] = np.cumsum(d[sl])
+    s, ref = _bins_stream(H, bins, n)
+    assert int(np.asarray(ref["widths"]).max()) == w
+    S, Q = O.moments(ref)
+    assert H.mean(s) == O.mean_from(S, n, 0.01)
+    assert H.variance(s) == O.variance_from(S, Q, n, 0.01)
+    assert np.array_equal(H.decode_to_quant(s).bins, bins)
