@@ -168,3 +168,34 @@ def test_generic_block_length_ramps(H, k, w):
           _run(lambda: O.serialize(O.scalar_mul(ref, -0.75))))
     _same(_run(lambda: H.serialize(H.elementwise_add(s, s))),
           _run(lambda: O.serialize(O.elementwise_add(ref, ref))))
+
+
+@pytest.mark.parametrize("case", ["saw22", "saw24", "saw26", "near_2p31", "near_2p29_starts",
+                                  "huge_small_eps", "mixed_magnitudes"])
+def test_compress_at_fast_path_edges(H, case):
+    """compress (quantize + encode in one pass) on inputs whose bins sit at
+    the encoder's register-path bounds; stream bytes or error class."""
+    import zlib
+
+    rng = np.random.default_rng(zlib.crc32(case.encode()))
+    n = 4096 * 3 + 45
+    eps = 0.01
+    i = np.arange(n)
+    if case.startswith("saw"):
+        step = 2 * eps * (1 << (int(case[3:]) - 1)) * 1.3
+        x = (i % 32) * step * rng.choice([-1, 1], n // 32 + 1)[i // 32]
+    elif case == "near_2p31":
+        x = 2 * eps * ((1 << 31) + rng.integers(-5000, 5000, n)) * rng.choice([-1, 1], n)
+        x[::32] = rng.normal(0, 100, x[::32].size)           # outliers fit; residuals ~2^32
+    elif case == "near_2p29_starts":
+        x = 2 * eps * ((1 << 29) + rng.integers(-40, 40, n)) * rng.choice([-1, 1], n // 32 + 1)[i // 32]
+    elif case == "huge_small_eps":
+        x = rng.normal(0, 1e30, n)
+        eps = 1e-10
+    else:
+        x = rng.normal(0, 1, n) * 10.0 ** rng.integers(-3, 7, n)
+    x = x.astype(np.float32)
+    got = _run(lambda: H.serialize(H.compress(H.RawArray(x, (n,), "f32"),
+                                              H.QuantParams(eps, (n,), 32, "f32"))))
+    want = _run(lambda: O.serialize(O.compress(x, eps, (n,), 32, "f32")))
+    _same(got, want)
