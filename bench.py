@@ -137,7 +137,9 @@ def _dist_init():
     backend = os.environ.get("HSZ_DIST_BACKEND", "nccl")
     if backend != "nccl":
         local = local % max(1, torch.cuda.device_count())
-    if world > 1 and not dist.is_initialized():
+    # HSZ_FORCE_COLL=1 (under torchrun): the collective path even at N = 1,
+    # so the NCCL code (device-resident collective buffers) runs on one GPU
+    if (world > 1 or os.environ.get("HSZ_FORCE_COLL")) and not dist.is_initialized():
         torch.cuda.set_device(local)
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -173,6 +175,7 @@ class Chain:
         self.H = H
         self.cfg = cfg
         self.coll = coll
+        self.layouts = None      # C2 of the last step (multi-rank)
 
     def run(self, x, events=None, host_out=False):
         H, cfg = self.H, self.cfg
@@ -190,20 +193,26 @@ class Chain:
         p = H.QuantParams(eps, cfg["dims"], 32, "f32")
         s = H.compress(raw, p)                                 # K1
         if self.coll is not None:
-            sb, pb = s.totals()
-            self.coll.global_offsets(0, sb, pb)                # C2
+            s.prefetch_totals()        # C2 inputs: copied back asynchronously
         mark(1)
         z = H.negate(s)                                        # K4
         mark(2)
         z = H.scalar_add(z, cfg["sadd"])                       # K5
         mark(3)
         z = H.scalar_mul(z, cfg["smul"])                       # K6
+        if self.coll is not None:
+            z.prefetch_totals()
         mark(4)
-        mean = _global_mean(H, z, self.coll)                   # K7
+        mean = _global_mean(H, z, self.coll)                   # K7 (+ C3)
         mark(5)
         var = _global_var(H, z, self.coll)                     # K7 (+ squares)
         mark(6)
         out = H.decompress(z)                                  # K3
+        if self.coll is not None:
+            # C2 for the compressed field and the result while decompress runs
+            # (their totals were prefetched; nothing in the step waits on it)
+            self.layouts = self.coll.global_offsets_many(
+                self.coll.rank * p.block_count, [s.totals(), z.totals()])
         mark(7)
         if host_out:
             from paper_2408_11971_b200.device import download
@@ -275,7 +284,7 @@ def run_b200(args):
     from paper_2408_11971_b200 import workloads as W
     from paper_2408_11971_b200.sharding import Collectives
 
-    coll = Collectives() if world > 1 else None
+    coll = Collectives() if world > 1 or os.environ.get("HSZ_FORCE_COLL") else None
     cfg = dict(W.CONFIGS[args.config])
     if args.config == 5:
         cfg["dims"] = (256, 2048, 2048)          # one 2^30-value slab per rank

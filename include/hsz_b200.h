@@ -230,6 +230,18 @@ int hsz_moments_mb(const uint8_t* widths, const int32_t* outliers, const uint8_t
                    uint64_t ws_bytes, uint64_t* mailbox, uint64_t seq, void* stream);
 int hsz_mailbox_wait(const uint64_t* mailbox, uint64_t seq, void* stream);
 
+/* ---- node-local host all-gather (multi-GPU plumbing) -----------------------
+ * The small per-step exchanges of sharding.Collectives (C1 value range, C2
+ * section sizes, C3 moment limbs) between the one-process-
+ * per-GPU ranks of ONE node, through a shared memory segment of
+ * hsz_hostcoll_bytes(world) zeroed bytes every rank maps.  Round r (1, 2,
+ * ...; the same on every rank) publishes nvals (<= 40) int64 words of this
+ * rank and gathers world * nvals words in rank order into out.  Returns
+ * HSZ_ECUDA when a peer has not published within timeout_s (> 0). */
+uint64_t hsz_hostcoll_bytes(int world);
+int hsz_hostcoll_allgather(void* shm, int rank, int world, uint64_t round, const int64_t* vals,
+                           int nvals, int64_t* out, double timeout_s);
+
 /* library identification (for the loader's sanity check) */
 const char* hsz_version(void);
 

@@ -71,6 +71,8 @@ SIGNATURES = {
     "hsz_moments_mb": (_int, [_vp, _vp, _vp, _vp, _vp, _u64, _u32, _int, _vp, _vp, _vp, _u64, _vp,
                               _u64, _vp]),
     "hsz_mailbox_wait": (_int, [_vp, _u64, _vp]),
+    "hsz_hostcoll_bytes": (_u64, [_int]),
+    "hsz_hostcoll_allgather": (_int, [_vp, _int, _int, _u64, _vp, _int, _vp, C.c_double]),
 }
 
 _LIB = None

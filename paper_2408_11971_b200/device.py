@@ -105,6 +105,14 @@ class Context:
         self.mailbox_ptr = self._mailbox.data_ptr()
         self._mailbox_np = self._mailbox.numpy().view(np.uint64)
         self.mailbox_seq = 0
+        # pinned ring for asynchronous section-total copies (prefetch_totals):
+        # slot = [sign total, payload total, error word, pad]
+        self._tot = t.zeros(4 * _TOT_SLOTS, dtype=t.int64, pin_memory=True)
+        self._tot_np = self._tot.numpy()
+        self._tot_ptr = self._tot.data_ptr()
+        self._tot_ev = [None] * _TOT_SLOTS
+        self._tot_next = 0
+        self._side = None
 
     def workspace(self, n: int, k: int):
         need = geometry(n, k)[3]
@@ -209,6 +217,26 @@ class Context:
         t = torch()
         return t.empty(int(n), dtype=dtype, device=self.device)
 
+    def side_stream(self):
+        """A second CUDA stream on this context's device (small copies that
+        must not delay the main stream)."""
+        if self._side is None:
+            self._side = torch().cuda.Stream(device=self.device)
+        return self._side
+
+    def totals_slot(self):
+        """Next slot of the pinned totals ring (waits only if the slot's
+        previous copy is still in flight)."""
+        i = self._tot_next
+        self._tot_next = (i + 1) % _TOT_SLOTS
+        if self._tot_ev[i] is not None:
+            self._tot_ev[i].synchronize()
+            self._tot_ev[i] = None
+        return i
+
+
+_TOT_SLOTS = 64
+
 
 _CTX = {}
 _CTX_LOCK = threading.Lock()
@@ -258,7 +286,8 @@ class DeviceStream:
     launch path works on raw pointers (base pointer + offset), so an op costs
     one device allocation and no tensor slicing on the host."""
 
-    __slots__ = ("params", "_sec", "_views", "ctx", "sign_cap", "payload_cap", "_totals", "_ptrs")
+    __slots__ = ("params", "_sec", "_views", "ctx", "sign_cap", "payload_cap", "_totals", "_ptrs",
+                 "_tot_pending")
 
     _NAMES = ("widths", "outliers", "signs", "payload", "toff")
 
@@ -273,6 +302,7 @@ class DeviceStream:
         self.payload_cap = int(payload_cap)
         self._totals = None
         self._ptrs = None
+        self._tot_pending = None
 
     def section(self, i):
         """Section i as an aliasable descriptor (tensor or (base, off, bytes, dtype))."""
@@ -319,8 +349,54 @@ class DeviceStream:
         self.ctx.check()
         return self
 
+    def prefetch_totals(self) -> "DeviceStream":
+        """Start copying the section totals (and the sticky error word) to
+        pinned host memory, asynchronously on the stream; a later
+        ``totals()`` then costs no device round trip once the stream has
+        passed this point (e.g. after any later synchronising call)."""
+        if self._totals is not None or self._tot_pending is not None:
+            return self
+        ctx = self.ctx
+        t = torch()
+        i = ctx.totals_slot()
+        host = ctx._tot_ptr + 32 * i
+        T = self.ntiles
+        # the copies run on a side stream that waits for the producer, so the
+        # main stream's next kernel does not queue behind two DMA latencies
+        side = ctx.side_stream()
+        side.wait_stream(ctx.stream)
+        h = int(side.cuda_stream)
+        N.check(ctx.lib.hsz_copy_d2h(host, self.pointers()[4] + 16 * T, 16, h), "d2h copy")
+        N.check(ctx.lib.hsz_copy_d2h(host + 16, ctx.err_ptr, 4, h), "d2h copy")
+        sec = self._sec[4]
+        (sec[0] if isinstance(sec, tuple) else sec).record_stream(side)
+        ev = t.cuda.Event()
+        ev.record(side)
+        ctx._tot_ev[i] = ev
+        self._tot_pending = (i, ev)
+        return self
+
     def totals(self):
-        """(sign bytes, payload bytes) -- synchronizes."""
+        """(sign bytes, payload bytes) -- synchronizes (unless prefetched)."""
+        if self._totals is None and self._tot_pending is not None:
+            i, ev = self._tot_pending
+            self._tot_pending = None
+            ctx = self.ctx
+            if ctx._tot_ev[i] is ev:             # else: the ring slot was reused; fetch below
+                ev.synchronize()
+                row = ctx._tot_np[4 * i:4 * i + 3].copy()
+                ctx._tot_ev[i] = None
+            else:
+                row = None
+        else:
+            row = None
+        if row is not None:
+            flags = int(row[2]) & 0xFFFFFFFF
+            if flags:
+                ctx.err.zero_()
+                ctx.stream.synchronize()
+                raise_for_flags(flags, "totals")
+            self._totals = (int(row[0]), int(row[1]))
         if self._totals is None:
             T = self.ntiles
             (tt,) = self.ctx.fetch_checked([self.toff[2 * T:2 * T + 2]])

@@ -67,10 +67,87 @@ class ShardLayout:
     payload_total: int
 
 
-class Collectives:
-    """The three collectives over a torch.distributed process group."""
+class HostAllGather:
+    """Node-local all-gather of a few int64 words per rank through a shared
+    memory segment (C ABI ``hsz_hostcoll_allgather``): the small exchanges of
+    the chain (C1-C3) carry host scalars, so between the processes of one
+    node they need no device round trip.  Raises RuntimeError at setup when
+    the ranks are not on one host."""
 
-    def __init__(self, group=None, device=None):
+    MAX_VALS = 40
+
+    def __init__(self, dist, group, rank: int, world: int, timeout_s: float = 300.0):
+        import ctypes
+        import mmap
+        import os
+        import socket
+        import tempfile
+        import uuid
+
+        from . import _native as N
+
+        self.lib = N.load()
+        self.rank, self.world, self.timeout = rank, world, float(timeout_s)
+        info = [None] * world
+        dist.all_gather_object(info, (socket.gethostname(), uuid.uuid4().hex), group=group)
+        if len({h for h, _ in info}) != 1:
+            raise RuntimeError("ranks span several hosts")
+        root = "/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir()
+        path = os.path.join(root, f"hsz_coll_{info[0][1]}")
+        size = int(self.lib.hsz_hostcoll_bytes(world))
+        if rank == 0:
+            fd = os.open(path, os.O_CREAT | os.O_EXCL | os.O_RDWR, 0o600)
+            os.ftruncate(fd, size)
+            os.close(fd)
+        dist.barrier(group=group)
+        fd = os.open(path, os.O_RDWR)
+        self._mm = mmap.mmap(fd, size)
+        os.close(fd)
+        dist.barrier(group=group)
+        if rank == 0:
+            os.unlink(path)              # the mappings stay; nothing left behind
+        self._buf = (ctypes.c_char * size).from_buffer(self._mm)
+        self._addr = ctypes.addressof(self._buf)
+        self._round = 0
+        self._vals = np.zeros(self.MAX_VALS, dtype=np.int64)
+        self._out = np.zeros(world * self.MAX_VALS, dtype=np.int64)
+
+    def __call__(self, vals):
+        nv = len(vals)
+        self._vals[:nv] = vals
+        self._round += 1
+        rc = self.lib.hsz_hostcoll_allgather(self._addr, self.rank, self.world, self._round,
+                                             self._vals.ctypes.data, nv, self._out.ctypes.data,
+                                             self.timeout)
+        if rc != 0:
+            raise RuntimeError(f"host all-gather round {self._round} failed ({rc}): a peer "
+                               "did not publish in time")
+        return self._out[:self.world * nv].reshape(self.world, nv).tolist()
+
+
+def _f2i(v: float) -> int:
+    import struct
+
+    return struct.unpack("<q", struct.pack("<d", float(v)))[0]
+
+
+def _i2f(v: int) -> float:
+    import struct
+
+    return struct.unpack("<d", struct.pack("<q", int(v)))[0]
+
+
+class Collectives:
+    """The three collectives over a torch.distributed process group.
+
+    ``host_shm`` (default: on unless ``HSZ_HOSTCOLL=0``): the small host-scalar
+    exchanges (C1-C3, the byte counts of ``allreduce_streams``, timing maxima)
+    go through a node-local shared-memory all-gather when all ranks share
+    one host; bulk data always moves over the process group (NCCL)."""
+
+    def __init__(self, group=None, device=None, host_shm=None):
+        import os
+
         import torch
         import torch.distributed as dist
 
@@ -79,21 +156,45 @@ class Collectives:
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        backend = dist.get_backend(group)
+        self.backend = dist.get_backend(group)
         if device is None:
-            device = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" \
+            device = torch.device("cuda", torch.cuda.current_device()) if self.backend == "nccl" \
                 else torch.device("cpu")
         self.device = device
+        if host_shm is None:
+            host_shm = os.environ.get("HSZ_HOSTCOLL", "1") != "0"
+        self._hc = None
+        if host_shm:
+            try:
+                self._hc = HostAllGather(dist, group, self.rank, self.world)
+            except RuntimeError:
+                self._hc = None          # ranks on several hosts: process group only
+
+    @property
+    def host_shm(self) -> bool:
+        return self._hc is not None
 
     def global_range(self, lo: float, hi: float):
-        """C1: allreduce MIN over (lo, -hi) in float64 (exact)."""
+        """C1: MIN over (lo, -hi) in float64 (exact)."""
+        if self._hc is not None:
+            rows = self._hc([_f2i(lo), _f2i(-hi)])
+            return min(_i2f(r[0]) for r in rows), -min(_i2f(r[1]) for r in rows)
         t = self.torch.tensor([lo, -hi], dtype=self.torch.float64, device=self.device)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
         v = t.cpu().tolist()
         return float(v[0]), float(-v[1])
 
     def _allgather_i64(self, vals):
-        t = self.torch.tensor([int(v) for v in vals], dtype=self.torch.int64, device=self.device)
+        vals = [int(v) for v in vals]
+        if self._hc is not None and len(vals) <= HostAllGather.MAX_VALS:
+            return self._hc(vals)
+        t = self.torch.tensor(vals, dtype=self.torch.int64, device=self.device)
+        if self.backend == "nccl":
+            out = self.torch.empty(self.world * len(vals), dtype=self.torch.int64,
+                                   device=self.device)
+            self.dist.all_gather_into_tensor(out, t, group=self.group)
+            flat = out.cpu().tolist()
+            return [flat[i * len(vals):(i + 1) * len(vals)] for i in range(self.world)]
         out = [self.torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(out, t, group=self.group)
         return [[int(x) for x in o.cpu().tolist()] for o in out]
@@ -115,6 +216,37 @@ class Collectives:
             tot_s += s
             tot_q += q
         return tot_s, tot_q
+
+    def global_offsets_many(self, block0: int, sizes):
+        """C2 for several streams of this rank's shard in one exchange:
+        `sizes` = [(sign bytes, payload bytes), ...] -> [ShardLayout, ...]."""
+        sizes = [(int(a), int(b)) for a, b in sizes]
+        rows = self._allgather_i64([block0] + [v for sp in sizes for v in sp])
+        lays = []
+        for j in range(len(sizes)):
+            so, st = exclusive_scan(r[1 + 2 * j] for r in rows)
+            po, pt = exclusive_scan(r[2 + 2 * j] for r in rows)
+            lays.append(ShardLayout(self.rank, block0, so[self.rank], po[self.rank], st, pt))
+        return lays
+
+    def global_moments_offsets(self, S: int, Q: int, block0: int, sizes):
+        """C3 with C2 riding along: the exact (S, Q) totals and, for every
+        stream in `sizes` ((sign bytes, payload bytes) of this rank's shard),
+        its ShardLayout -- one exchange instead of one per collective, at a
+        point where the host has synchronised anyway (a moment result)."""
+        sizes = [(int(a), int(b)) for a, b in sizes]
+        rows = self._allgather_i64(_to_limbs(S, Q) + [block0] + [v for sp in sizes for v in sp])
+        tot_s = tot_q = 0
+        for r in rows:
+            s, q = _from_limbs(r[:5])
+            tot_s += s
+            tot_q += q
+        lays = []
+        for j in range(len(sizes)):
+            so, st = exclusive_scan(r[6 + 2 * j] for r in rows)
+            po, pt = exclusive_scan(r[7 + 2 * j] for r in rows)
+            lays.append(ShardLayout(self.rank, block0, so[self.rank], po[self.rank], st, pt))
+        return tot_s, tot_q, lays
 
     # -- reduce compressed streams (distsim.py:80-103 across ranks) ---------
     def gather_streams(self, stream):
@@ -304,6 +436,8 @@ class Collectives:
         self.dist.barrier(group=self.group)
 
     def max_over_ranks(self, value: float) -> float:
+        if self._hc is not None:
+            return max(_i2f(r[0]) for r in self._hc([_f2i(value)]))
         t = self.torch.tensor([value], dtype=self.torch.float64, device=self.device)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return float(t.item())

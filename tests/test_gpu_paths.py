@@ -203,3 +203,36 @@ def test_moments_monotone_wide_residuals(H, w):
     assert H.mean(s) == O.mean_from(S, n, 0.01)
     assert H.variance(s) == O.variance_from(S, Q, n, 0.01)
     assert np.array_equal(H.decode_to_quant(s).bins, bins)
+
+
+def test_prefetch_totals_matches_fetch(H):
+    """DeviceStream.prefetch_totals (side-stream copy into the pinned ring)
+    gives the same totals as the synchronous fetch, also when the ring wraps
+    around before the value is read."""
+    import torch
+
+    from paper_2408_11971_b200.device import DeviceStream
+
+    n = 4096 * 5 + 3
+    rng = np.random.default_rng(5)
+    x = torch.from_numpy(np.cumsum(rng.normal(0, 1, n)).astype(np.float32)).cuda()
+    p = H.QuantParams(0.01, (n,), 32, "f32")
+    streams = [H.compress(H.RawArray(x * (1 + i), (n,), "f32"), p) for i in range(3)]
+    want = []
+    for s in streams:
+        hs = s.to_host()
+        want.append((len(hs.sign_planes), len(hs.payload)))
+    fresh = [DeviceStream.from_host(s.to_host()) for s in streams]
+    for s in fresh:
+        s._totals = None
+        s.prefetch_totals()
+    assert [s.totals() for s in fresh] == want
+    # wrap the ring (64 slots) before reading the first prefetch: falls back
+    first = DeviceStream.from_host(streams[0].to_host())
+    first._totals = None
+    first.prefetch_totals()
+    for _ in range(70):
+        d = DeviceStream.from_host(streams[1].to_host())
+        d._totals = None
+        d.prefetch_totals()
+    assert first.totals() == want[0] and d.totals() == want[1]

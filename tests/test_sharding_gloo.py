@@ -29,7 +29,7 @@ def _field(n, seed=3):
     return (np.cumsum(rng.normal(0, 0.3, n)) + 280).astype(np.float32)
 
 
-def _worker(rank, world, port, n, rel, outdir):
+def _worker(rank, world, port, n, rel, outdir, host_shm=True):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import torch.distributed as dist
@@ -41,7 +41,8 @@ def _worker(rank, world, port, n, rel, outdir):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        coll = Collectives()
+        coll = Collectives(host_shm=host_shm)
+        assert coll.host_shm == host_shm
         x = _field(n)
         k = 32
         e0, e1 = element_range(n, k, rank, world)
@@ -52,6 +53,13 @@ def _worker(rank, world, port, n, rel, outdir):
         lay = coll.global_offsets(e0 // k, len(s["signs"]), len(s["payload"]))   # C2
         S, Q = O.moments(s)
         St, Qt = coll.global_moments(S, Q)                                # C3
+        assert coll.max_over_ranks(float(rank) + 0.5) == world - 0.5
+        S2, Q2, lays = coll.global_moments_offsets(S, Q, e0 // k,
+                                                   [(len(s["signs"]), len(s["payload"])), (3, 5)])
+        assert (S2, Q2) == (St, Qt) and lays[0] == lay
+        assert (lays[1].sign_offset, lays[1].payload_total) == (3 * rank, 5 * world)
+        assert coll.global_offsets_many(e0 // k, [(len(s["signs"]), len(s["payload"])),
+                                                  (3, 5)]) == lays
         parts = [None] * world
         dist.all_gather_object(parts, (lay.__dict__, s["widths"].tobytes(),
                                        np.asarray(s["outliers"], np.int64).tobytes(),
@@ -63,8 +71,10 @@ def _worker(rank, world, port, n, rel, outdir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_equals_single_process(tmp_path, world):
+@pytest.mark.parametrize("world,host_shm", [(2, True), (3, True), (2, False), (3, False)])
+def test_sharded_equals_single_process(tmp_path, world, host_shm):
+    """C1-C3 over the node-local shared-memory exchange and over the process
+    group give the single-process stream, eps and moments."""
     import torch.multiprocessing as mp
 
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -72,7 +82,8 @@ def test_sharded_equals_single_process(tmp_path, world):
     from paper_2408_11971_b200 import sharding
 
     n, rel = 32 * 997 + 13, 1e-4
-    mp.spawn(_worker, args=(world, _free_port(), n, rel, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), n, rel, str(tmp_path), host_shm), nprocs=world,
+             join=True)
     parts = list(np.load(tmp_path / "parts.npy", allow_pickle=True))
     x = _field(n)
     eps = O.resolve_eps(x, rel, "rel")
@@ -290,3 +301,38 @@ def test_write_sharded_equals_serialize(tmp_path, world):
     eps = 1e-4 * (float(x.max()) - float(x.min()))
     want = O.serialize(O.compress(x, eps, (n,), 32, "f32"))
     assert open(path, "rb").read() == want
+
+
+def _hc_worker(rank, world, port, outdir):
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from paper_2408_11971_b200.sharding import HostAllGather
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        hc = HostAllGather(dist, None, rank, world, timeout_s=60)
+        rows = []
+        for r in range(300):                       # many rounds: the double buffer is reused
+            nv = 1 + (r % HostAllGather.MAX_VALS)
+            vals = [rank * 1_000_003 + r * 7 + j - (1 << 62) for j in range(nv)]
+            got = hc(vals)
+            want = [[q * 1_000_003 + r * 7 + j - (1 << 62) for j in range(nv)]
+                    for q in range(world)]
+            rows.append(got == want)
+        with open(os.path.join(outdir, f"hc{rank}.txt"), "w") as f:
+            f.write("ok" if all(rows) else "mismatch")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_host_allgather_rounds(tmp_path, world):
+    """The shared-memory all-gather: 300 back-to-back rounds of 1..40 words,
+    every rank sees every rank's words of the same round."""
+    import torch.multiprocessing as mp
+
+    mp.spawn(_hc_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    assert all((tmp_path / f"hc{r}.txt").read_text() == "ok" for r in range(world))
