@@ -233,10 +233,19 @@ __device__ __forceinline__ void decode_block(const unsigned char* sgn, const uns
 // Register-light block sums for the moment kernels: the same field walk as
 // decode_block_t, but the prefix sums P_i are accumulated on the fly
 // (sum P_i, and sum P_i^2 for kSq) instead of being kept as 32 bins.
+#ifndef HSZ_SUM_V2
+#define HSZ_SUM_V2 1
+#endif
+
 template <bool kFull, int G, bool kSq>
 __device__ __forceinline__ void decode_sum_t(const unsigned char* sgn, const unsigned char* pay,
                                              uint32_t w, int len, int64_t* sp_out, uint64_t* sp2_out) {
   const uint32_t sw = bswap32(*reinterpret_cast<const uint32_t*>(sgn));
+#if HSZ_SUM_V2
+  uint32_t sh[8];   // sign of element i: PRMT sign replication (see decode_block_t)
+#pragma unroll
+  for (int k = 0; k < 8; ++k) sh[k] = sw << k;
+#endif
   const uint32_t* pw = reinterpret_cast<const uint32_t*>(pay);
   const uint32_t mask = (1u << w) - 1u;
   const int wg = G * static_cast<int>(w);
@@ -248,7 +257,9 @@ __device__ __forceinline__ void decode_sum_t(const unsigned char* sgn, const uns
   // w <= 16); the one-field-per-step path serves widths up to kFastW = 24
   using SumT = std::conditional_t<(G >= 2), int32_t, int64_t>;
   SumT sp = 0;
-  uint64_t sp2 = 0;   // sum P^2 < 32 * 2^58
+  // sum P^2 < 32 * 2^58; with w <= 8 (G = 4) sum_i (255 i)^2 < 6.8e8 fits 32 bits
+  using SqT = std::conditional_t<(HSZ_SUM_V2 && G >= 4), uint32_t, uint64_t>;
+  SqT sp2 = 0;
 #pragma unroll
   for (int c = 0; c < (K + G - 1) / G; ++c) {
     if (nb < wg) {
@@ -262,13 +273,28 @@ __device__ __forceinline__ void decode_sum_t(const unsigned char* sgn, const uns
       nb -= static_cast<int>(w);
       if (i == 0) continue;
       const int32_t mag = static_cast<int32_t>(static_cast<uint32_t>(win >> nb) & mask);
+#if HSZ_SUM_V2
+      const int32_t neg = static_cast<int32_t>(prmt_sign(sh[i & 7], 3 - (i >> 3)));
+#else
       const int32_t neg = static_cast<int32_t>(sw << i) >> 31;
+#endif
       int32_t d = (mag ^ neg) - neg;
       if (!kFull) d = (i < len) ? d : 0;
+      if (HSZ_SUM_V2 && kFull && !kSq) {
+        // sum_i P_i = sum_j (K - j) d_j: one multiply-add per element and no
+        // serial prefix chain (the same exact integer)
+        sp += static_cast<SumT>(K - i) * d;
+        continue;
+      }
       P += d;
       if (kFull || i < len) {
         sp += P;
-        if (kSq) sp2 += static_cast<uint64_t>(static_cast<int64_t>(P) * P);
+        if (kSq) {
+          if constexpr (sizeof(SqT) == 4)
+            sp2 += static_cast<uint32_t>(P * P);
+          else
+            sp2 += static_cast<uint64_t>(static_cast<int64_t>(P) * P);
+        }
       }
     }
   }
