@@ -333,6 +333,11 @@ __device__ __forceinline__ void decode_f32_t(const unsigned char* sgn, const uns
   // a constant block has no sign bytes: its offset may be unaligned (after
   // the stream's partial last block), so the word is read only when w > 0
   const uint32_t sw = w ? bswap32(*reinterpret_cast<const uint32_t*>(sgn)) : 0u;
+#if HSZ_SUM_V2
+  uint32_t sh[8];   // PRMT sign replication, as in decode_block_t
+#pragma unroll
+  for (int k = 0; k < 8; ++k) sh[k] = sw << k;
+#endif
   const uint32_t* pw = reinterpret_cast<const uint32_t*>(pay);
   const uint32_t mask = (1u << w) - 1u;
   const int wg = G * static_cast<int>(w);
@@ -355,7 +360,11 @@ __device__ __forceinline__ void decode_f32_t(const unsigned char* sgn, const uns
       nb -= static_cast<int>(w);
       if (i > 0 && w) {
         const int32_t mag = static_cast<int32_t>(static_cast<uint32_t>(win >> nb) & mask);
+#if HSZ_SUM_V2
+        const int32_t neg = static_cast<int32_t>(prmt_sign(sh[i & 7], 3 - (i >> 3)));
+#else
         const int32_t neg = static_cast<int32_t>(sw << i) >> 31;
+#endif
         int32_t d = (mag ^ neg) - neg;
         if (!kFull) d = (i < len) ? d : 0;
         P += d;

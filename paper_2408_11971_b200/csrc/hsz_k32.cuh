@@ -219,6 +219,9 @@ __device__ __forceinline__ void decode_row_fast(const TileIn& t, Emit&& emit) {
     return;
   }
   const uint32_t sw = bswap32(*reinterpret_cast<const uint32_t*>(t.sgn + t.soff));
+  uint32_t sh[8];   // PRMT sign replication: element i's sign from sh[i % 8]
+#pragma unroll
+  for (int k = 0; k < 8; ++k) sh[k] = sw << k;
   const uint32_t* pw = reinterpret_cast<const uint32_t*>(t.pay + t.poff);
   const uint32_t mask = (1u << w) - 1u;
   uint64_t acc = 0;
@@ -232,7 +235,8 @@ __device__ __forceinline__ void decode_row_fast(const TileIn& t, Emit&& emit) {
     }
     nb -= w;
     const int32_t mag = static_cast<int32_t>(static_cast<uint32_t>(acc >> nb) & mask);
-    if (i > 0 && i < t.len) P += ((sw >> (31 - i)) & 1u) ? -mag : mag;
+    const int32_t neg = static_cast<int32_t>(prmt_sign(sh[i & 7], 3 - (i >> 3)));
+    if (i > 0 && i < t.len) P += (mag ^ neg) - neg;
     emit(i, P);
   }
 }
