@@ -515,6 +515,7 @@ struct SmulParams {
   double d;      // 2 eps
   double rsd;    // (double) rs
   int small_rs;  // |rs| < 2^23: every register-path product is exact in float64
+  double negc;   // -(2^52 + 2^31) * rs, exact (45 significant bits)
 };
 
 // in-tile (sign, payload) byte offsets of this thread's block: one CTA scan
@@ -668,7 +669,11 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
         // then ops.py:199-208 verbatim
 #pragma unroll
         for (int i = 0; i < K; ++i) {
-          const double pd = __dmul_rn(i32_to_double(q[i]), sp.rsd);
+          // bin * rs in one FMA from the biased bin (2^52 + 2^31 + bin): the
+          // exact product-sum is bin * rs (< 2^53), so the one rounding is exact
+          const double pd = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(
+                                         static_cast<uint32_t>(q[i]) ^ 0x80000000u)),
+                                     sp.rsd, sp.negc);
           const double tt = __dmul_rn(sp.d, pd);
           // floor(RN(|t| + 1/2)): RN(|t| + 1/2) is exact here (|t| < 2^31), and
           // adding 2^52 rounding toward -inf leaves floor() in the low word
