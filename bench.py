@@ -643,7 +643,8 @@ def _cpu_baseline(x, cfg, budget_s=20.0):
             break
         sample = min(x.size, sample * 2)
     return {"value": round(len(OPS) * 4.0 * sample / dt / 1e9, 4), "unit": "GB/s",
-            "cores": procs, "kind": "port",
+            "cores": procs, "kind": "port", "os_cpu_count": os.cpu_count(),
+            "affinity": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None,
             "sample": f"first {sample} of {x.size} values of the bench field, whole op chain, "
                       f"{procs} processes over block ranges ({dt:.2f} s)"}
 
@@ -682,6 +683,9 @@ def run_reference(args):
         "config": {"workload": f"config {args.config}, op chain {'>'.join(OPS)}",
                    "sample_elements": sample},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": procs, "kind": "port",
+                         "os_cpu_count": os.cpu_count(),
+                         "affinity": len(os.sched_getaffinity(0))
+                         if hasattr(os, "sched_getaffinity") else None,
                          "sample": f"first {sample} values of the config-{args.config} field per "
                                    f"step, numpy oracle over {procs} processes"},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
