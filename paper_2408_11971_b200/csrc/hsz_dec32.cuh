@@ -154,7 +154,10 @@ __device__ __forceinline__ void put_bin(int32_t& qi, int32_t v) {
   else qi = static_cast<int32_t>(static_cast<uint32_t>(qi) - static_cast<uint32_t>(v));
 }
 
-template <bool kFull, int G, int kAcc = 0>
+// kResid: q[i] receives the signed residual d_i (q[0] the outlier) instead of
+// the bin -- the element-wise ops combine streams in the residual domain
+// (ops.py:171-176), so they need no prefix sums on the way in
+template <bool kFull, int G, int kAcc = 0, bool kResid = false>
 __device__ __forceinline__ void decode_block_t(const unsigned char* sgn, const unsigned char* pay,
                                                uint32_t w, int32_t o, int len, int32_t (&q)[K]) {
   const uint32_t sw = bswap32(*reinterpret_cast<const uint32_t*>(sgn));
@@ -201,32 +204,37 @@ __device__ __forceinline__ void decode_block_t(const unsigned char* sgn, const u
       const int32_t neg = static_cast<int32_t>(prmt_sign(sh[i & 7], 3 - (i >> 3)));
       int32_t d = (mag ^ neg) - neg;
       if (!kFull) d = (i < len) ? d : 0;
-      P += d;
-      put_bin<kAcc>(q[i], P);
+      if constexpr (kResid) {
+        put_bin<kAcc>(q[i], d);
+      } else {
+        P += d;
+        put_bin<kAcc>(q[i], P);
+      }
     }
   }
 }
 
 // all 32 lanes of the warp call this (the field grouping is warp-uniform)
-template <int kAcc = 0>
+template <int kAcc = 0, bool kResid = false>
 __device__ __forceinline__ void decode_block(const unsigned char* sgn, const unsigned char* pay,
                                              uint32_t w, int32_t o, int len, int32_t (&q)[K]) {
   const uint32_t wmax = __reduce_max_sync(kFull, w);
   if (w == 0) {
+    put_bin<kAcc>(q[0], o);
 #pragma unroll
-    for (int i = 0; i < K; ++i) put_bin<kAcc>(q[i], o);
+    for (int i = 1; i < K; ++i) put_bin<kAcc>(q[i], kResid ? 0 : o);
     return;
   }
   if (len != K) {
-    decode_block_t<false, 1, kAcc>(sgn, pay, w, o, len, q);
+    decode_block_t<false, 1, kAcc, kResid>(sgn, pay, w, o, len, q);
   } else if (wmax <= 8) {
-    decode_block_t<true, 4, kAcc>(sgn, pay, w, o, len, q);
+    decode_block_t<true, 4, kAcc, kResid>(sgn, pay, w, o, len, q);
   } else if (wmax <= 10) {
-    decode_block_t<true, 3, kAcc>(sgn, pay, w, o, len, q);
+    decode_block_t<true, 3, kAcc, kResid>(sgn, pay, w, o, len, q);
   } else if (wmax <= 16) {
-    decode_block_t<true, 2, kAcc>(sgn, pay, w, o, len, q);
+    decode_block_t<true, 2, kAcc, kResid>(sgn, pay, w, o, len, q);
   } else {
-    decode_block_t<true, 1, kAcc>(sgn, pay, w, o, len, q);
+    decode_block_t<true, 1, kAcc, kResid>(sgn, pay, w, o, len, q);
   }
 }
 
@@ -663,7 +671,7 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
     uint32_t qb[K];
     if (!exact) {
       int32_t q[K];
-      decode_block<0>(S.in.sgn + S.in.soff + ies, S.in.pay + S.in.poff + iep, w, o, len, q);
+      decode_block<0, kTwo>(S.in.sgn + S.in.soff + ies, S.in.pay + S.in.poff + iep, w, o, len, q);
       if constexpr (kOp == kOpSmul) {
         // rescale: |bin| < 2^30, |rs| < 2^23 -> bin * rs exact in float64;
         // then ops.py:199-208 verbatim
@@ -683,9 +691,9 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
           qb[i] = tt < 0.0 ? 0u - mi : mi;
         }
       } else {
-        // |bin_a|, |bin_b| < 2^30: the sum fits int32 and every residual
-        // sum fits 25 bits (the encoder's register path)
-        decode_block<kOp == kOpSub ? 2 : 1>(S.in2.sgn + S.in2.soff + ies2,
+        // residual domain (ops.py:171-176): outlier sums |o_a +- o_b| < 2^30
+        // and residual sums < 2^25 (the encoder's register path)
+        decode_block<kOp == kOpSub ? 2 : 1, true>(S.in2.sgn + S.in2.soff + ies2,
                                              S.in2.pay + S.in2.poff + iep2, w2, o2, len, q);
 #pragma unroll
         for (int i = 0; i < K; ++i) qb[i] = static_cast<uint32_t>(q[i]);
@@ -699,7 +707,10 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
     uint32_t ts = 0, tp = 0;
     if (!exact) {
       e32::BlockCode bc;
-      e32::block_code(qb, len, bc);
+      if constexpr (kTwo)
+        e32::block_code_resid(qb, bc);   // qb already holds the outlier and residuals
+      else
+        e32::block_code(qb, len, bc);
       const uint32_t wmax = __reduce_max_sync(kFull, bc.w);
       const uint32_t sb = (bc.w && active) ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
       const uint32_t pb = (static_cast<uint32_t>(len) * bc.w + 7u) >> 3;

@@ -220,6 +220,22 @@ __device__ __forceinline__ void block_code(uint32_t (&qb)[K], int len, BlockCode
   bc.w = 32u - __clz(mx);
 }
 
+// the same from signed residuals (qb[0] = the outlier, qb[i] = d_i; zero past
+// a tail block's length)
+__device__ __forceinline__ void block_code_resid(const uint32_t (&qb)[K], BlockCode& bc) {
+  uint32_t mx = 0, sg = 0;
+  bc.mg[0] = 0;
+#pragma unroll
+  for (int i = 1; i < K; ++i) {
+    const int32_t d = static_cast<int32_t>(qb[i]);
+    sg = __funnelshift_l(static_cast<uint32_t>(d), sg, 1);
+    bc.mg[i] = static_cast<uint32_t>(d < 0 ? -d : d);
+    mx |= bc.mg[i];
+  }
+  bc.sg = sg;
+  bc.w = 32u - __clz(mx);
+}
+
 #ifndef HSZ_PACK_G3
 #define HSZ_PACK_G3 0
 #endif
