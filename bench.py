@@ -1,35 +1,43 @@
 """Benchmark of the HoSZp hot path on B200 (one JSON line on rank 0).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2|4]
-    python bench.py --impl reference ...       # CPU oracle arm (rank 0 only)
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2|4|5]
+    python bench.py --impl reference ...       # CPU arm (rank 0 only)
 
-Workload (BASELINE.json configs[1] = config 2): a 100x500x500 float32 GRF
-field (P(k) ~ k^-11/3, mean 280, std 15; seeded synthetic -- SDRBench data is
-not available offline), relative error bound 1e-4, block_len 32.  One step is
-the whole op chain of the path on that field:
+Workload.  Every config is ONE field partitioned by contiguous block ranges
+across the ranks (north_star; rank r owns ``sharding.element_range(N, 32, r,
+world)``), so ``scaling`` is "strong" and ``value`` covers the whole field:
 
-    value range (K0) -> resolve rel eps -> compress (K1) -> negate (K4)
-    -> scalar_add 3.5 (K5) -> scalar_mul -1.25 (K6) -> mean (K7)
-    -> variance (K7) -> decompress (K3)
+* default at N = 1: **config 4** -- the 512^3 float32 lognormal field
+  (exp(1.5 G), G a Gaussian random field with P(k) ~ k^-2, seed 3), relative
+  error bound 1e-3, block_len 32: the largest BASELINE.json config pinned to
+  one GPU; 512 MiB of input, 4x the 126 MB L2.  The field is generated ONCE on
+  the host (numpy, ``workloads.config4``) and the same values feed both arms.
+* default at N > 1: **config 5** -- the 2048^3 field (2^33 values, 32 GiB),
+  generated per slab from (seed 4, slab) on each rank's GPU
+  (``workloads.config5_range``), so the field is identical for any N.  C1
+  (global value range -> the one relative eps), C2 (allgather of the shard
+  byte counts -> global section offsets) and C3 (allreduce of the exact
+  moment partial sums) run on NCCL.  The N = 1 line carries the same
+  config-5 chain on one GPU under ``config5_n1`` (the scaling baseline).
 
-``value`` = 7 ops x 4N uncompressed bytes / device step time (the chain
-aggregate of the per-op "uncompressed GB/s" metric; per-op numbers are in
-``ops``).  Inputs are resident in HBM; L2 (126 MB > the 100 MB field) is
-flushed with a 512 MB write between steps and excluded from the timing.  At
-N > 1 every rank owns one config-2-sized shard of a field partitioned by
-contiguous block ranges (weak scaling) and the step adds the collectives C1
-(global value range), C2 (global section offsets) and C3 (exact moments).
+One step is the whole op chain of the path on the field:
 
-``e2e`` runs the same chain through the public API starting from the field in
-pinned HOST memory (H2D inside the timed region) and ends with a D2H read of
-the resulting stream sections, the decompressed field and mean / variance.
+    value range (K0) -> C1 -> resolve rel eps -> compress (K1) -> negate (K4)
+    -> scalar_add (K5) -> scalar_mul (K6) -> mean (K7) + C3
+    -> variance (K7) + C3 -> decompress (K3) [+ C2]
+
+``value`` = 7 ops x 4N uncompressed bytes of the whole field / device step
+time (max over ranks).  Inputs are resident in HBM; L2 is flushed with a
+512 MB read between steps (excluded from the timing).  ``e2e`` runs the same
+chain through the public API from the field in pinned HOST memory (H2D
+inside the timed region) and ends with a D2H of the resulting stream
+sections and the decompressed field.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -42,14 +50,16 @@ sys.path.insert(0, ROOT)
 
 OPS = ("compress", "negate", "scalar_add", "scalar_mul", "mean", "variance", "decompress")
 METRIC = "uncompressed GB/s per op (compress/decompress/homomorphic) & % HBM roofline"
+L2_BYTES = 126 << 20
 
 
-def _traffic(op):
+def _traffic(config, op):
     """DRAM bytes per launch of `op`'s kernel (dram__bytes_read.sum +
-    dram__bytes_write.sum) from the committed ncu capture, if any."""
+    dram__bytes_write.sum) from the committed ncu --set full capture of this
+    config (profiles/traffic.json), if any."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            v = json.load(f)["config2"].get(op)
+            v = json.load(f).get(f"config{config}", {}).get(op)
         return int(v) if v is not None else None
     except Exception:
         return None
@@ -123,58 +133,65 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# the B200 arm
+# the workload: one field, a contiguous block range per rank
 
-def _dist_init():
-    import torch
-    import torch.distributed as dist
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    # HSZ_DIST_BACKEND=gloo: functional check of the N > 1 path with several
-    # ranks sharing one GPU (collectives on the host); the default is NCCL
-    backend = os.environ.get("HSZ_DIST_BACKEND", "nccl")
-    if backend != "nccl":
-        local = local % max(1, torch.cuda.device_count())
-    # HSZ_FORCE_COLL=1 (under torchrun): the collective path even at N = 1,
-    # so the NCCL code (device-resident collective buffers) runs on one GPU
-    if (world > 1 or os.environ.get("HSZ_FORCE_COLL")) and not dist.is_initialized():
-        torch.cuda.set_device(local)
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-    return world, rank, local
+def _default_config(world: int) -> int:
+    return 4 if world == 1 else 5
 
 
-def _field(config: int, rank: int, device):
+def _global_dims(config: int):
     from paper_2408_11971_b200 import workloads as W
 
-    if config == 2:
-        seed = 1 if rank == 0 else (1, rank)
-        if rank == 0:
-            import torch
+    return tuple(W.CONFIGS[config]["dims"])
 
-            return torch.from_numpy(W.config2()).to(device)
-        x = W.grf_device(W.CONFIGS[2]["dims"], 11.0 / 3.0, seed, device) * 15.0 + 280.0
-        return x.reshape(-1).float()
-    if config == 4:
-        return W.config4(seed=3 if rank == 0 else 3 + 1000 * rank, device=device)
+
+def _count(dims) -> int:
+    n = 1
+    for d in dims:
+        n *= int(d)
+    return n
+
+
+_HOST_FIELDS = {}
+
+
+def host_field(config: int):
+    """The host (numpy float32) field of configs 1-4 -- generated once per
+    process; both arms use exactly these values."""
+    from paper_2408_11971_b200 import workloads as W
+
+    if config not in _HOST_FIELDS:
+        _HOST_FIELDS[config] = W.field(config)
+    return _HOST_FIELDS[config]
+
+
+def shard_field(config: int, rank: int, world: int, device):
+    """(x on `device`, e0, e1): this rank's elements [e0, e1) of the field."""
+    import torch
+
+    from paper_2408_11971_b200 import workloads as W
+    from paper_2408_11971_b200.sharding import element_range
+
+    n = _count(_global_dims(config))
+    e0, e1 = element_range(n, 32, rank, world)
     if config == 5:
-        # 2048^3 field as 8 slabs of 2^30 values; rank r owns slab r (the
-        # 8-GPU partition); at N < 8 every rank still owns one slab (weak)
-        return W.config5_slab(rank % 8, device=device)
-    raise ValueError("bench supports --config 2, 4 or 5")
+        x = W.config5_range(e0, e1, device=device)
+    else:
+        x = torch.from_numpy(host_field(config)[e0:e1]).to(device)
+    return x.contiguous(), e0, e1
 
 
 class Chain:
-    """One step of the op chain through the public (device) API."""
+    """One step of the op chain on this rank's shard through the public
+    (device) API, with the collectives C1-C3 when the field is sharded."""
 
-    def __init__(self, H, cfg, coll):
+    def __init__(self, H, cfg, coll, dims_local, n_global, block0):
         self.H = H
         self.cfg = cfg
         self.coll = coll
+        self.dims = dims_local
+        self.n_global = n_global
+        self.block0 = block0
         self.layouts = None      # C2 of the last step (multi-rank)
 
     def run(self, x, events=None, host_out=False):
@@ -185,12 +202,12 @@ class Chain:
         mark = (lambda i: events[i].record() if i in events else None) if events is not None \
             else (lambda i: None)
         mark(0)
-        raw = H.RawArray(x, cfg["dims"], "f32")               # K0: range + finite check
+        raw = H.RawArray(x, self.dims, "f32")                  # K0: range + finite check
         lo, hi = raw.value_range()
         if self.coll is not None:
             lo, hi = self.coll.global_range(lo, hi)            # C1
         eps = float(cfg["rel_eps"]) * (hi - lo)
-        p = H.QuantParams(eps, cfg["dims"], 32, "f32")
+        p = H.QuantParams(eps, self.dims, 32, "f32")
         s = H.compress(raw, p)                                 # K1
         if self.coll is not None:
             s.prefetch_totals()        # C2 inputs: copied back asynchronously
@@ -203,16 +220,15 @@ class Chain:
         if self.coll is not None:
             z.prefetch_totals()
         mark(4)
-        mean = _global_mean(H, z, self.coll)                   # K7 (+ C3)
+        mean = global_mean(z, self.coll, self.n_global)        # K7 (+ C3)
         mark(5)
-        var = _global_var(H, z, self.coll)                     # K7 (+ squares)
+        var = global_variance(z, self.coll, self.n_global)     # K7 (+ C3)
         mark(6)
         out = H.decompress(z)                                  # K3
         if self.coll is not None:
             # C2 for the compressed field and the result while decompress runs
             # (their totals were prefetched; nothing in the step waits on it)
-            self.layouts = self.coll.global_offsets_many(
-                self.coll.rank * p.block_count, [s.totals(), z.totals()])
+            self.layouts = self.coll.global_offsets_many(self.block0, [s.totals(), z.totals()])
         mark(7)
         if host_out:
             from paper_2408_11971_b200.device import download
@@ -223,43 +239,45 @@ class Chain:
         return z, out, mean, var
 
 
-def _global_mean(H, z, coll):
+def global_mean(z, coll, n_global):
+    """ops.mean over the whole field: exact local S, C3, the reference's
+    float expression with the GLOBAL element count (ops.py:360-363)."""
     from paper_2408_11971_b200 import ops
 
     S, Q = ops.exact_moments(z, want_sq=False)
-    n = z.params.element_count
     if coll is not None:
         S, Q = coll.global_moments(S, 0)
-        n *= coll.world
-    return ops.mean_from(S, n, z.params.eps)
+    return ops.mean_from(S, n_global, z.params.eps)
 
 
-def _global_var(H, z, coll):
+def global_variance(z, coll, n_global):
+    """ops.variance over the whole field (ops.py:382-393)."""
     from paper_2408_11971_b200 import ops
 
     S, Q = ops.exact_moments(z, want_sq=True)
-    n = z.params.element_count
     if coll is not None:
         S, Q = coll.global_moments(S, Q)
-        n *= coll.world
-    return ops.variance_from(S, Q, n, z.params.eps)
+    return ops.variance_from(S, Q, n_global, z.params.eps)
 
 
-def _algorithmic_bytes(H, cfg, x):
-    """Per-op algorithmic bytes for this field."""
-    raw = H.RawArray(x, cfg["dims"], "f32")
+def _algorithmic_bytes(H, chain, x):
+    """Per-op algorithmic bytes of this rank's shard, from
+    device-side section totals (no host copy of the streams)."""
+    raw = H.RawArray(x, chain.dims, "f32")
     lo, hi = raw.value_range()
-    eps = float(cfg["rel_eps"]) * (hi - lo)
-    p = H.QuantParams(eps, cfg["dims"], 32, "f32")
+    if chain.coll is not None:
+        lo, hi = chain.coll.global_range(lo, hi)
+    eps = float(chain.cfg["rel_eps"]) * (hi - lo)
+    p = H.QuantParams(eps, chain.dims, 32, "f32")
     s = H.compress(raw, p)
-    z = H.scalar_mul(H.scalar_add(H.negate(s), cfg["sadd"]), cfg["smul"])
+    z = H.scalar_mul(H.scalar_add(H.negate(s), chain.cfg["sadd"]), chain.cfg["smul"])
     n = p.element_count
     B = p.block_count
-    hs = s.to_host()
-    hz = z.to_host()
-    C_in = B + 4 * B + len(hs.sign_planes) + len(hs.payload)
-    C_z = B + 4 * B + len(hz.sign_planes) + len(hz.payload)
-    nc = int((hs.widths > 0).sum())
+    ss, sp = s.totals()
+    zs, zp = z.totals()
+    C_in = B + 4 * B + ss + sp
+    C_z = B + 4 * B + zs + zp
+    nc = int((s.widths > 0).sum().item())
     return {
         "minmax": 4 * n,
         "compress": 4 * n + C_in,
@@ -269,144 +287,10 @@ def _algorithmic_bytes(H, cfg, x):
         "mean": C_z,
         "variance": C_z,
         "decompress": C_z + 4 * n,
-        "_C": C_in, "_C_chain": C_z, "_ratio": p.raw_nbytes / hs.serialized_size,
+        "_C": C_in, "_C_chain": C_z,
+        "_ratio": p.raw_nbytes / (C_in + 20 + 8 * len(chain.dims)),
         "_eps": eps,
     }
-
-
-def run_b200(args):
-    import torch
-
-    world, rank, local = _dist_init()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    import paper_2408_11971_b200 as H
-    from paper_2408_11971_b200 import workloads as W
-    from paper_2408_11971_b200.sharding import Collectives
-
-    coll = Collectives() if world > 1 or os.environ.get("HSZ_FORCE_COLL") else None
-    cfg = dict(W.CONFIGS[args.config])
-    if args.config == 5:
-        cfg["dims"] = (256, 2048, 2048)          # one 2^30-value slab per rank
-    x = _field(args.config, rank, dev).contiguous()
-    n = x.numel()
-    chain = Chain(H, cfg, coll)
-    abytes = _algorithmic_bytes(H, cfg, x)
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
-
-    sampler = ClockSampler(local)
-    sampler.start()                       # samples cover warm-up, timed steps and kernel timing
-    for _ in range(max(args.warmup, 3)):
-        chain.run(x)
-    torch.cuda.synchronize()
-
-    per_step = []
-    per_op = {op: [] for op in OPS}
-    if coll is not None:
-        coll.barrier()
-    torch.cuda.synchronize()
-    wall0 = time.perf_counter()
-    for _ in range(args.steps):
-        _flush(flush)                                   # evict L2 (excluded from timing)
-        evs = {0: torch.cuda.Event(enable_timing=True), 7: torch.cuda.Event(enable_timing=True)}
-        chain.run(x, evs)
-        torch.cuda.synchronize()
-        per_step.append(evs[0].elapsed_time(evs[7]))
-    torch.cuda.synchronize()
-    if coll is not None:
-        coll.barrier()
-    wall = time.perf_counter() - wall0
-    # per-op breakdown inside the chain: separate (untimed) steps with a mark
-    # between every op
-    for _ in range(min(args.steps, 5)):
-        _flush(flush)
-        evs = {i: torch.cuda.Event(enable_timing=True) for i in range(8)}
-        chain.run(x, evs)
-        torch.cuda.synchronize()
-        for i, op in enumerate(OPS):
-            per_op[op].append(evs[i].elapsed_time(evs[i + 1]))
-
-    step_ms = sum(per_step) / len(per_step)
-    if coll is not None:
-        step_ms = coll.max_over_ranks(step_ms)
-    # whole job: 7 ops over every rank's N elements
-    value = len(OPS) * 4.0 * n * world / (step_ms * 1e-3) / 1e9
-
-    # ---- per-kernel timing (each op alone, L2 flushed first) for the roofline
-    kern = _kernel_times(H, cfg, x, flush, reps=max(10, min(args.steps, 30)))
-    clocks = sampler.stop()
-    peak, peak_kind = _peaks()
-    ops_json = {}
-    for op in OPS:
-        t_ms = statistics.median(per_op[op])
-        ops_json[op] = {
-            "ms_in_chain": round(t_ms, 4),
-            "gbps_uncompressed_in_chain": round(4.0 * n / (t_ms * 1e-3) / 1e9, 2),
-            "kernel_ms": round(kern[op], 4),
-            "kernel_gbps_uncompressed": round(4.0 * n / (kern[op] * 1e-3) / 1e9, 2),
-            "algorithmic_bytes": int(abytes[op]),
-            "roofline_frac": round(abytes[op] / (kern[op] * 1e-3) / 1e9 / peak, 4),
-        }
-    ops_json["minmax"] = {"kernel_ms": round(kern["minmax"], 4),
-                          "algorithmic_bytes": int(abytes["minmax"]),
-                          "roofline_frac": round(abytes["minmax"] / (kern["minmax"] * 1e-3) / 1e9 / peak, 4)}
-    dom = max(OPS, key=lambda o: kern[o])
-    achieved = abytes[dom] / (kern[dom] * 1e-3) / 1e9
-
-    # ---- e2e through the public API from pinned host memory
-    if args.config == 5:
-        e2e = {"value": None, "unit": "GB/s", "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": None,
-               "skipped": "config 5 slab: the pinned host arenas would need ~25 GB; e2e is "
-                          "measured on the default config"}
-    else:
-        e2e = _e2e(H, chain, x, flush, steps=max(6, min(args.steps, 20)), coll=coll)
-
-    line = {
-        "metric": METRIC,
-        "value": round(value, 3),
-        "unit": "GB/s",
-        "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": round(step_ms, 4),
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "f64 quantize / int64 bins (f32 input)",
-        "data": "synthetic (seeded GRF stand-in for SDRBench; see DESIGN.md)",
-        "config": {
-            "workload": f"config {args.config}: {'x'.join(map(str, cfg['dims']))} f32, rel eps "
-                        f"{cfg['rel_eps']}, block_len 32, op chain {'>'.join(OPS)}",
-            "elements_per_gpu": n,
-            "global_elements": n * world,
-            "eps": abytes["_eps"],
-            "compression_ratio": round(abytes["_ratio"], 3),
-            "stream_bytes": int(abytes["_C"]),
-            "value_definition": "7 ops x 4N bytes (all ranks) / device step time",
-            "l2": "512 MB read between steps (field 100 MB < 126 MB L2), excluded from timing",
-            "parallelism": f"{world} rank(s), contiguous block ranges, NCCL C1/C2/C3" if world > 1
-            else "1 GPU",
-            "wall_s_timed_region": round(wall, 3),
-        },
-        "ops": ops_json,
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
-                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4),
-                     "traffic": _traffic(dom) if args.config == 2 else None,
-                     "algorithmic_bytes": int(abytes[dom])},
-        "e2e": e2e,
-        "gpu_launches": 8 * args.steps,
-        "clocks": clocks,
-    }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config != 5:
-        line["cpu_baseline"] = _cpu_baseline(x.cpu().numpy(), cfg, budget_s=args.cpu_budget)
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if coll is not None:
-        coll.barrier()
-        import torch.distributed as dist
-
-        dist.destroy_process_group()
 
 
 def _flush(flush):
@@ -415,26 +299,29 @@ def _flush(flush):
     flush.view(__import__("torch").int64).max()
 
 
-def _kernel_times(H, cfg, x, flush, reps=10):
-    """Mean device time (ms) of each op launched alone after an L2 flush.  A
-    ~0.2 ms spin kernel is queued first so the host enqueues the op while the
-    GPU is busy: the event interval holds device time only, not Python launch
-    latency.  (Events tick in 2.048 us steps on this driver; the mean over
-    `reps` launches resolves below that.)"""
+def _kernel_times(H, chain, x, flush, reps=10):
+    """Mean device time (ms) of each op launched alone after an L2 flush, on
+    the stream the op is launched on (torch's current stream: every op of
+    the package launches there).  A ~0.2 ms spin kernel is queued first so
+    the host enqueues the op while the GPU is busy: the event interval holds
+    device time only, not Python launch latency."""
     import torch
+    from paper_2408_11971_b200 import _native as N
     from paper_2408_11971_b200 import ops as O
+    from paper_2408_11971_b200.device import ptr
 
-    raw = H.RawArray(x, cfg["dims"], "f32")
+    cfg = chain.cfg
+    raw = H.RawArray(x, chain.dims, "f32")
     lo, hi = raw.value_range()
-    p = H.QuantParams(float(cfg["rel_eps"]) * (hi - lo), cfg["dims"], 32, "f32")
+    if chain.coll is not None:
+        lo, hi = chain.coll.global_range(lo, hi)
+    p = H.QuantParams(float(cfg["rel_eps"]) * (hi - lo), chain.dims, 32, "f32")
     s = H.compress(raw, p)
     z0 = H.scalar_add(H.negate(s), cfg["sadd"])
     z = H.scalar_mul(z0, cfg["smul"])
     ctx = s.ctx
     wsp, wsb = ctx.workspace(1, 1)
     mm = ctx.empty(2, torch.float64)
-    from paper_2408_11971_b200 import _native as N
-    from paper_2408_11971_b200.device import ptr
     fns = {
         "minmax": lambda: N.check(ctx.lib.hsz_minmax(ptr(x), N.HSZ_F32, x.numel(), ptr(mm), ctx.err_ptr,
                                                      wsp, wsb, ctx.handle), "hsz_minmax"),
@@ -454,16 +341,226 @@ def _kernel_times(H, cfg, x, flush, reps=10):
             torch.cuda._sleep(400_000)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            fn()
+            r = fn()
             b.record()
             torch.cuda.synchronize()
+            del r
             ts.append(a.elapsed_time(b))
         out[name] = sum(ts[2:]) / len(ts[2:])
     z.check()
     return out
 
 
-def _e2e(H, chain, x, flush, steps, coll):
+def _dist_init():
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # HSZ_DIST_BACKEND=gloo: functional check of the N > 1 path with several
+    # ranks sharing one GPU (collectives on the host); the default is NCCL
+    backend = os.environ.get("HSZ_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
+    # HSZ_FORCE_COLL=1 (under torchrun): the collective path even at N = 1
+    if (world > 1 or os.environ.get("HSZ_FORCE_COLL")) and not dist.is_initialized():
+        torch.cuda.set_device(local)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return world, rank, local
+
+
+def measure(args, config, world, rank, local, coll, light=False):
+    """Bench one config on this rank's shard; returns the JSON line (rank 0's
+    view, with maxima over ranks).  `light`: chain value and per-op in-chain
+    times only (the config-5 scaling baseline at N = 1)."""
+    import torch
+
+    import paper_2408_11971_b200 as H
+    from paper_2408_11971_b200 import workloads as W
+
+    dev = torch.device("cuda", local)
+    cfg = dict(W.CONFIGS[config])
+    gdims = _global_dims(config)
+    n_global = _count(gdims)
+    x, e0, e1 = shard_field(config, rank, world, dev)
+    n = x.numel()
+    dims_local = gdims if world == 1 else (n,)
+    chain = Chain(H, cfg, coll, dims_local, n_global, e0 // 32)
+    abytes = _algorithmic_bytes(H, chain, x)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    steps = args.steps if not light else max(3, min(args.steps, 5))
+    for _ in range(max(args.warmup, 3) if not light else 2):
+        chain.run(x)
+    torch.cuda.synchronize()
+
+    per_step = []
+    if coll is not None:
+        coll.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    for _ in range(steps):
+        _flush(flush)                                   # evict L2 (excluded from timing)
+        evs = {0: torch.cuda.Event(enable_timing=True), 7: torch.cuda.Event(enable_timing=True)}
+        chain.run(x, evs)
+        torch.cuda.synchronize()
+        per_step.append(evs[0].elapsed_time(evs[7]))
+    torch.cuda.synchronize()
+    if coll is not None:
+        coll.barrier()
+    wall = time.perf_counter() - wall0
+    # per-op breakdown inside the chain: separate (untimed) steps with a mark
+    # between every op
+    per_op = {op: [] for op in OPS}
+    for _ in range(min(steps, 5)):
+        _flush(flush)
+        evs = {i: torch.cuda.Event(enable_timing=True) for i in range(8)}
+        chain.run(x, evs)
+        torch.cuda.synchronize()
+        for i, op in enumerate(OPS):
+            per_op[op].append(evs[i].elapsed_time(evs[i + 1]))
+
+    step_ms = sum(per_step) / len(per_step)
+    if coll is not None:
+        step_ms = coll.max_over_ranks(step_ms)
+    # whole job: 7 ops over the whole field's N elements
+    value = len(OPS) * 4.0 * n_global / (step_ms * 1e-3) / 1e9
+    field_bytes = 4 * n
+    l2_note = (f"per-rank input {field_bytes / 1e6:.0f} MB "
+               f"{'>' if field_bytes > L2_BYTES else '<'} 126 MB L2; 512 MB read between "
+               f"steps, excluded from timing")
+    line = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(step_ms, 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64 quantize / int64 bins (f32 input)",
+        "data": "synthetic (seeded stand-in for SDRBench; see DESIGN.md)",
+        "config": {
+            "workload": f"config {config}: {'x'.join(map(str, gdims))} f32, rel eps "
+                        f"{cfg['rel_eps']}, block_len 32, op chain {'>'.join(OPS)}, "
+                        f"scalars sadd {cfg['sadd']} smul {cfg['smul']}",
+            "global_elements": n_global,
+            "elements_per_gpu": n,
+            "eps": abytes["_eps"],
+            "compression_ratio": round(abytes["_ratio"], 3),
+            "stream_bytes": int(abytes["_C"]),
+            "value_definition": "7 ops x 4N bytes of the whole field / device step time "
+                                "(max over ranks)",
+            "l2": l2_note,
+            "parallelism": (f"{world} ranks, one field by contiguous block ranges, "
+                            f"C1/C2/C3 on {coll.backend}"
+                            f"{' (host shm for the scalars)' if coll.host_shm else ''}")
+            if coll is not None else "1 GPU",
+            "wall_s_timed_region": round(wall, 3),
+        },
+        "ops_in_chain_ms": {op: round(statistics.median(per_op[op]), 4) for op in OPS},
+        "gpu_launches": 8 * steps,
+    }
+    if light:
+        del x, flush
+        return line
+
+    # ---- per-kernel timing (each op alone, L2 flushed first) for the roofline
+    kern = _kernel_times(H, chain, x, flush, reps=max(10, min(args.steps, 30)))
+    peak, peak_kind = _peaks()
+    ops_json = {}
+    for op in OPS:
+        t_ms = statistics.median(per_op[op])
+        ops_json[op] = {
+            "ms_in_chain": round(t_ms, 4),
+            "gbps_uncompressed_in_chain": round(4.0 * n / (t_ms * 1e-3) / 1e9, 2),
+            "kernel_ms": round(kern[op], 4),
+            "kernel_gbps_uncompressed": round(4.0 * n / (kern[op] * 1e-3) / 1e9, 2),
+            "algorithmic_bytes": int(abytes[op]),
+            "roofline_frac": round(abytes[op] / (kern[op] * 1e-3) / 1e9 / peak, 4),
+        }
+    ops_json["minmax"] = {"kernel_ms": round(kern["minmax"], 4),
+                          "algorithmic_bytes": int(abytes["minmax"]),
+                          "roofline_frac": round(abytes["minmax"] / (kern["minmax"] * 1e-3) / 1e9 / peak, 4)}
+    dom = max(OPS, key=lambda o: kern[o])
+    achieved = abytes[dom] / (kern[dom] * 1e-3) / 1e9
+    traffic = _traffic(config, dom)
+    line["ops"] = ops_json
+    line["roofline"] = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
+                        "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                        "frac": round(achieved / peak, 4),
+                        "traffic": traffic,
+                        "traffic_source": f"profiles/traffic.json config{config} (ncu --set full)"
+                        if traffic is not None else None,
+                        "algorithmic_bytes": int(abytes[dom])}
+    del abytes
+
+    # ---- e2e through the public API from pinned host memory
+    if config == 5:
+        win = min(n, 1 << 27)
+        e2e = _e2e(H, chain, x[:win], flush, steps=max(6, min(args.steps, 12)), coll=coll,
+                   dims=(win,), n_global=win * world)
+        e2e["window"] = (f"first {win} values of each rank's shard (a 2^27-value window per "
+                         f"rank: the whole 2^33-value field does not fit pinned host memory)")
+    else:
+        e2e = _e2e(H, chain, x, flush, steps=max(6, min(args.steps, 20)), coll=coll,
+                   dims=chain.dims, n_global=n_global)
+    line["e2e"] = e2e
+    del x, flush
+    return line
+
+
+def run_b200(args):
+    import torch
+
+    world, rank, local = _dist_init()
+    torch.cuda.set_device(local)
+    from paper_2408_11971_b200.sharding import Collectives
+
+    coll = Collectives() if world > 1 or os.environ.get("HSZ_FORCE_COLL") else None
+    config = args.config or _default_config(world)
+
+    sampler = ClockSampler(local)
+    sampler.start()                       # samples cover warm-up, timed steps and kernel timing
+    line = measure(args, config, world, rank, local, coll)
+    line["clocks"] = sampler.stop()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and config != 5:
+        line["cpu_baseline"] = _cpu_baseline(host_field(config), W_cfg(config),
+                                             budget_s=args.cpu_budget)
+    if world == 1 and config == 4 and not args.no_scale_baseline:
+        # the north_star scaling config on ONE GPU: the baseline of the N > 1 lines
+        import gc
+
+        gc.collect()
+        torch.cuda.empty_cache()
+        try:
+            sub = measure(args, 5, world, rank, local, coll, light=True)
+            line["config5_n1"] = {k: sub[k] for k in ("value", "unit", "ms_per_step", "steps",
+                                                      "config", "ops_in_chain_ms")}
+        except torch.cuda.OutOfMemoryError as e:      # report, never fail the headline line
+            line["config5_n1"] = {"skipped": f"out of memory: {str(e).splitlines()[0]}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if coll is not None:
+        coll.barrier()
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def W_cfg(config):
+    from paper_2408_11971_b200 import workloads as W
+
+    return dict(W.CONFIGS[config])
+
+
+def _e2e(H, chain, x, flush, steps, coll, dims, n_global):
     """The chain end to end from a pinned HOST field: every step copies the
     field host->device, runs the public API chain and copies the step's
     results (the final stream's four sections, the decompressed field) back
@@ -471,10 +568,11 @@ def _e2e(H, chain, x, flush, steps, coll):
     import torch
     from paper_2408_11971_b200.device import download_into
 
+    chain = Chain(H, chain.cfg, chain.coll, dims, n_global, chain.block0)
     host = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
     host.copy_(x.cpu())
     n = x.numel()
-    arena_bytes = 4 * n + 8 * n + (1 << 20)
+    arena_bytes = 4 * n + 3 * n + (1 << 20)      # values + the stream (< 3 B/value here)
     arena = torch.empty(arena_bytes, dtype=torch.uint8, pin_memory=True)
     # (1) serial latency: one field at a time, every copy on the critical path
     ts = []
@@ -490,6 +588,7 @@ def _e2e(H, chain, x, flush, steps, coll):
         got = download_into(secs, arena, z.ctx)
         ts.append(time.perf_counter() - t0)
         bo = sum(g.size for g in got) + 16
+        del z, out, xd, got
     t_serial = statistics.median(ts[1:])
 
     # (2) throughput: a three-stage pipeline over fields -- H2D of field k+1
@@ -562,20 +661,21 @@ def _e2e(H, chain, x, flush, steps, coll):
             ev.synchronize()
         torch.cuda.synchronize()
         passes.append((time.perf_counter() - t0) / steps)
+    keep[0] = keep[1] = None
     t = statistics.median(passes)
     if coll is not None:
         t = coll.max_over_ranks(t)
         t_serial = coll.max_over_ranks(t_serial)
-    world = coll.world if coll is not None else 1
-    return {"value": round(len(OPS) * 4.0 * n * world / t / 1e9, 3), "unit": "GB/s",
+    return {"value": round(len(OPS) * 4.0 * n_global / t / 1e9, 3), "unit": "GB/s",
             "ms_per_step": round(t * 1e3, 3), "h2d_bytes_per_step": 4 * n,
             "d2h_bytes_per_step": int(bo),
             "passes_ms_per_step": [round(v * 1e3, 3) for v in passes],
             "serial_ms_per_step": round(t_serial * 1e3, 3),
-            "serial_value": round(len(OPS) * 4.0 * n * world / t_serial / 1e9, 3),
+            "serial_value": round(len(OPS) * 4.0 * n_global / t_serial / 1e9, 3),
             "path": "pinned host field -> H2D -> public API chain -> D2H of the final stream "
-                    "sections + decompressed field into pinned host arenas; pipelined over fields on 3 CUDA streams (H2D of "
-                    "field k+1 | chain of field k | D2H of field k-1; serial_*: one field at a time)"}
+                    "sections + decompressed field into pinned host arenas; pipelined over fields "
+                    "on 3 CUDA streams (H2D of field k+1 | chain of field k | D2H of field k-1; "
+                    "serial_*: one field at a time); h2d/d2h bytes are per rank"}
 
 
 # ---------------------------------------------------------------------------
@@ -598,8 +698,9 @@ def _cpu_chain_slice(args):
     return len(s["payload"]), S, Q
 
 
-def _cpu_run(x, cfg, procs):
-    """One chain over `x` with `procs` worker processes (block-range slices)."""
+def _cpu_run(x, cfg, procs, eps=None):
+    """One chain over `x` with `procs` worker processes (block-range slices).
+    `eps` None: resolved from `x` (relative bound)."""
     import multiprocessing as mp
 
     global _POOL_X
@@ -608,7 +709,8 @@ def _cpu_run(x, cfg, procs):
 
     _POOL_X = x
     t0 = time.perf_counter()
-    eps = O.resolve_eps(x, cfg["rel_eps"], "rel")
+    if eps is None:
+        eps = O.resolve_eps(x, cfg["rel_eps"], "rel")
     nb = -(-x.size // 32)
     from paper_2408_11971_b200.sharding import block_range
 
@@ -645,8 +747,23 @@ def _cpu_baseline(x, cfg, budget_s=20.0):
     return {"value": round(len(OPS) * 4.0 * sample / dt / 1e9, 4), "unit": "GB/s",
             "cores": procs, "kind": "port", "os_cpu_count": os.cpu_count(),
             "affinity": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None,
-            "sample": f"first {sample} of {x.size} values of the bench field, whole op chain, "
-                      f"{procs} processes over block ranges ({dt:.2f} s)"}
+            "sample": f"first {sample} of {x.size} values of the bench field (the same host "
+                      f"array the B200 arm uploads), whole op chain, {procs} processes over "
+                      f"block ranges ({dt:.2f} s)"}
+
+
+def _reference_field(config):
+    """The reference arm's input: the same values the B200 arm uses."""
+    if config != 5:
+        return host_field(config), "the whole field (the host array the B200 arm uploads)"
+    import torch
+
+    from paper_2408_11971_b200 import workloads as W
+
+    # config 5 is generated on the GPU, slab by slab; the sample is a prefix of slab 0
+    x = W.config5_slab(0, device="cuda:0")[: 1 << 27].cpu().numpy()
+    torch.cuda.empty_cache()
+    return x, "a prefix of slab 0 of the 2048^3 field (generated on cuda:0 exactly as the B200 arm)"
 
 
 def run_reference(args):
@@ -654,40 +771,48 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2408_11971_b200 import workloads as W
-
-    cfg = dict(W.CONFIGS[args.config])
-    if args.config == 5:
-        cfg["dims"] = (256, 2048, 2048)          # one 2^30-value slab per rank
-    if args.config in (2, 5):
-        x = W.config2()          # config 5 = config 2's spectrum at 2048^3: a bounded sample of it
-    else:
-        x = W.config4()
+    config = args.config or _default_config(world)
+    cfg = W_cfg(config)
+    x, origin = _reference_field(config)
     procs = _cpu_cores()
-    sample = min(x.size, 1 << 25)       # the whole config-2 field (a bounded prefix of larger ones)
+    # size the per-step sample so the whole --steps/--warmup run stays within
+    # the budget: calibrate on a 2^22-value prefix, then scale
+    cal = min(x.size, 1 << 22)
+    dt, _ = _cpu_run(x[:cal], cfg, procs)
+    per_elem = dt / cal
+    budget_step = args.ref_budget / max(1, args.steps + args.warmup)
+    sample = int(min(x.size, budget_step / per_elem))
+    sample = max(32 * procs, (sample // (32 * procs)) * (32 * procs)) if sample < x.size else x.size
     xs = x[:sample]
+    import hoszp_oracle as O
+
+    eps = O.resolve_eps(x, cfg["rel_eps"], "rel")       # the field's eps, as in the B200 arm
     for _ in range(args.warmup):
-        _cpu_run(xs, cfg, procs)
+        _cpu_run(xs, cfg, procs, eps=None if sample == x.size else eps)
     times = []
     for _ in range(args.steps):
-        dt, _ = _cpu_run(xs, cfg, procs)
+        dt, _ = _cpu_run(xs, cfg, procs, eps=None if sample == x.size else eps)
         times.append(dt)
     t = sum(times) / len(times)
     value = len(OPS) * 4.0 * sample / t / 1e9
+    gdims = _global_dims(config)
+    what = (f"{sample} of {x.size} values: {origin}" if sample < x.size else origin)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64 quantize / int64 bins (f32 input)",
-        "data": "synthetic (seeded GRF stand-in for SDRBench)",
-        "config": {"workload": f"config {args.config}, op chain {'>'.join(OPS)}",
-                   "sample_elements": sample},
+        "data": "synthetic (seeded stand-in for SDRBench; see DESIGN.md)",
+        "config": {"workload": f"config {config}: {'x'.join(map(str, gdims))} f32, rel eps "
+                               f"{cfg['rel_eps']}, block_len 32, op chain {'>'.join(OPS)}, "
+                               f"scalars sadd {cfg['sadd']} smul {cfg['smul']}",
+                   "sample_elements": sample, "global_elements": _count(gdims)},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": procs, "kind": "port",
                          "os_cpu_count": os.cpu_count(),
                          "affinity": len(os.sched_getaffinity(0))
                          if hasattr(os, "sched_getaffinity") else None,
-                         "sample": f"first {sample} values of the config-{args.config} field per "
-                                   f"step, numpy oracle over {procs} processes"},
+                         "sample": f"per step {what}; numpy oracle (oracle/hoszp_oracle.py, the "
+                                   f"reference's algorithm restated) over {procs} processes"},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -699,10 +824,15 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2, choices=[2, 4, 5])
+    ap.add_argument("--config", type=int, default=None, choices=[2, 4, 5],
+                    help="default: 4 at N = 1, 5 at N > 1")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-scale-baseline", action="store_true",
+                    help="skip the config-5 chain on one GPU (config5_n1) at N = 1")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="seconds of CPU work for the whole --impl reference run")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

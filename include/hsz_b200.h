@@ -69,6 +69,9 @@ extern "C" {
 #define HSZ_ERR_CAPACITY (1u << 6)          /* output section buffer too small  */
 #define HSZ_ERR_OUTPUT_NONFINITE (1u << 7)  /* ValueError on decoded RawArray   */
 #define HSZ_ERR_BAD_WIDTH (1u << 8)         /* GeometryMismatch model.py:217    */
+#define HSZ_ERR_LOOKBACK_TIMEOUT (1u << 9)  /* encoder look-back watchdog fired:
+                                               offsets undefined (DeviceTimeout);
+                                               re-initialise the workspace      */
 
 /* ---- geometry / workspace ------------------------------------------------ */
 
@@ -244,6 +247,12 @@ int hsz_hostcoll_allgather(void* shm, int rank, int world, uint64_t round, const
 
 /* library identification (for the loader's sanity check) */
 const char* hsz_version(void);
+
+/* Look-back watchdog of the encoders: how many back-offs a warp waiting for
+ * a predecessor tile's offsets takes before it gives up and sets
+ * HSZ_ERR_LOOKBACK_TIMEOUT (0 = leave unchanged).  Returns the previous
+ * bound.  Default 2^23 (seconds of waiting; no legitimate wait comes close). */
+unsigned int hsz_set_lookback_watchdog(unsigned int max_sleeps);
 
 /* debug builds (-DHSZ_TRACE): copy out per-CTA phase timestamps; -1 otherwise */
 int hsz_trace_read(unsigned long long* host, int cap, int reset);

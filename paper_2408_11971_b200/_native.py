@@ -33,6 +33,7 @@ _dbl = C.c_double
 #: symbol -> (restype, argtypes); mirrors include/hsz_b200.h one-to-one
 SIGNATURES = {
     "hsz_version": (C.c_char_p, []),
+    "hsz_set_lookback_watchdog": (C.c_uint, [C.c_uint]),
     "hsz_trace_read": (_int, [_vp, _int, _int]),
     "hsz_trace_lookback": (_int, [_vp]),
     "hsz_tile_count": (_u64, [_u64, _u32]),

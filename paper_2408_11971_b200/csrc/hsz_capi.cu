@@ -669,7 +669,14 @@ __global__ void mailbox_post_kernel(Mailbox mb, const uint64_t* res, int nres, c
 
 extern "C" {
 
-const char* hsz_version(void) { return "hsz_b200 1.0 sm_100a"; }
+const char* hsz_version(void) { return "hsz_b200 1.1 sm_100a"; }
+
+unsigned int hsz_set_lookback_watchdog(unsigned int max_sleeps) {
+  unsigned int old = 0;
+  if (cudaMemcpyFromSymbol(&old, hsz::g_lb_max_sleeps, sizeof(old)) != cudaSuccess) return 0;
+  if (max_sleeps) cudaMemcpyToSymbol(hsz::g_lb_max_sleeps, &max_sleeps, sizeof(max_sleeps));
+  return old;
+}
 
 // debug: copy out phase-trace records (only in -DHSZ_TRACE builds; returns count)
 int hsz_trace_read(unsigned long long* host, int cap, int reset) {

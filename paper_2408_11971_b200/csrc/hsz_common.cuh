@@ -263,6 +263,17 @@ struct LookbackWs {
 
 constexpr uint64_t kStAgg = 1, kStInc = 2;
 
+// Look-back watchdog: a warp that has backed off this many times waiting for
+// a predecessor tile gives up, sets HSZ_ERR_LOOKBACK_TIMEOUT and publishes
+// what it has (the offsets of that tile and its successors are then wrong,
+// and flagged), so a protocol failure -- e.g. a workspace left inconsistent
+// by an aborted launch -- raises on the host instead of hanging the GPU.
+// Each back-off is >= 16-128 ns plus an L2 round trip: the default bound is
+// several seconds, far above any legitimate wait (tickets are drawn in
+// order, so every awaited predecessor is resident and progressing).
+// Settable through hsz_set_lookback_watchdog().
+__device__ unsigned int g_lb_max_sleeps = 1u << 23;
+
 // Called by thread 0: draw the launch epoch and a tile ticket (tickets are
 // handed out in order, so every predecessor of a tile is resident or done,
 // which makes the spin in lookback() deadlock-free).  The CTA drawing the
@@ -314,7 +325,7 @@ constexpr int kLbPerLane = HSZ_LB_PER_LANE;
 
 __device__ __forceinline__ void resolve_prefix(LookbackWs& w, uint64_t tile, uint64_t epoch,
                                                uint64_t agg_s, uint64_t agg_p, uint64_t* excl_s,
-                                               uint64_t* excl_p) {
+                                               uint64_t* excl_p, uint32_t* err) {
   const int lane = threadIdx.x & 31;
   if (tile == 0) {
     *excl_s = 0;
@@ -324,6 +335,8 @@ __device__ __forceinline__ void resolve_prefix(LookbackWs& w, uint64_t tile, uin
   uint64_t sum_s = 0, sum_p = 0;
   int64_t base = static_cast<int64_t>(tile) - 1;
   unsigned backoff = 32;
+  const unsigned max_sleeps = g_lb_max_sleeps;
+  unsigned sleeps = 0;
   while (true) {
     // relaxed flag loads (all in flight together), then one acquire fence
     uint32_t stj[kLbPerLane];
@@ -351,6 +364,10 @@ __device__ __forceinline__ void resolve_prefix(LookbackWs& w, uint64_t tile, uin
     const int first = inc ? (__ffs(inc) - 1) : 32;
     const bool bad = (lane < first && inv_all) || (lane == first && inv_pre);
     if (__any_sync(kFull, bad)) {        // a needed predecessor has not published yet
+      if (++sleeps > max_sleeps) {       // watchdog (warp-uniform)
+        if (lane == 0) atomicOr(err, HSZ_ERR_LOOKBACK_TIMEOUT);
+        break;
+      }
       __nanosleep(backoff);
       backoff = backoff < 256 ? backoff * 2 : 256;
       continue;
@@ -394,10 +411,10 @@ __device__ __forceinline__ void resolve_prefix(LookbackWs& w, uint64_t tile, uin
 // both steps back to back (callers with nothing to overlap)
 __device__ __forceinline__ void lookback(LookbackWs& w, uint64_t tile, uint64_t epoch,
                                          uint64_t agg_s, uint64_t agg_p, uint64_t* excl_s,
-                                         uint64_t* excl_p) {
+                                         uint64_t* excl_p, uint32_t* err) {
   if ((threadIdx.x & 31) == 0) publish_aggregate(w, tile, epoch, agg_s, agg_p);
   __syncwarp();
-  resolve_prefix(w, tile, epoch, agg_s, agg_p, excl_s, excl_p);
+  resolve_prefix(w, tile, epoch, agg_s, agg_p, excl_s, excl_p, err);
 }
 
 // ---------------------------------------------------------------------------
@@ -452,7 +469,7 @@ __device__ unsigned long long g_lb_cycles_round, g_lb_cycles_total;
 // publishes the tile's inclusive prefix.  Each round inspects 32 * L tiles.
 __device__ __forceinline__ void lb_resolve(uint64_t* words, uint64_t tile, uint64_t epoch,
                                            uint64_t agg_s, uint64_t agg_p, uint64_t* excl_s,
-                                           uint64_t* excl_p) {
+                                           uint64_t* excl_p, uint32_t* err) {
   constexpr int L = HSZ_LB2_PER_LANE;
   const int lane = threadIdx.x & 31;
   if (tile == 0) {
@@ -464,6 +481,8 @@ __device__ __forceinline__ void lb_resolve(uint64_t* words, uint64_t tile, uint6
   uint64_t sum_s = 0, sum_p = 0;
   int64_t base = static_cast<int64_t>(tile) - 1;
   unsigned backoff = 16;
+  const unsigned max_sleeps = g_lb_max_sleeps;
+  unsigned nsleep = 0;
 #ifdef HSZ_TRACE
   unsigned rounds = 0, sleeps = 0;
 #endif
@@ -507,6 +526,10 @@ __device__ __forceinline__ void lb_resolve(uint64_t* words, uint64_t tile, uint6
     // read only valid records before (or at) their inclusive one
     const bool bad = lane <= first && invalid;
     if (__any_sync(kFull, bad)) {
+      if (++nsleep > max_sleeps) {     // watchdog (warp-uniform): give up, flagged
+        if (lane == 0) atomicOr(err, HSZ_ERR_LOOKBACK_TIMEOUT);
+        break;
+      }
       __nanosleep(backoff);
       backoff = backoff < 128 ? backoff * 2 : 128;
 #ifdef HSZ_TRACE

@@ -503,7 +503,7 @@ __device__ __forceinline__ void smul_resolve(SM& S, const k32::EncodeOut& out, u
                                              uint32_t tp, int par) {
   const int lane = threadIdx.x & 31;
   uint64_t es, ep;
-  lb_resolve(lb_words(out.ws), tile, epoch, ts, tp, &es, &ep);
+  lb_resolve(lb_words(out.ws), tile, epoch, ts, tp, &es, &ep, out.err);
   if (lane == 0) {
     out.toff[2 * tile] = es;
     out.toff[2 * tile + 1] = ep;

@@ -324,7 +324,7 @@ __device__ __forceinline__ void resolve_tile(Smem& S, const k32::EncodeOut& out,
                                              uint32_t tp, int par) {
   const int lane = threadIdx.x & 31;
   uint64_t es, ep;
-  lb_resolve(lb_words(out.ws), tile, epoch, ts, tp, &es, &ep);
+  lb_resolve(lb_words(out.ws), tile, epoch, ts, tp, &es, &ep, out.err);
   if (lane == 0) {
     out.toff[2 * tile] = es;
     out.toff[2 * tile + 1] = ep;
@@ -419,7 +419,7 @@ __device__ __forceinline__ void resolve6(const k32::EncodeOut& out, uint64_t til
                                          uint64_t* ep_out) {
   const int lane = threadIdx.x & 31;
   uint64_t es, ep;
-  lb_resolve(lb_words(out.ws), tile, epoch, ts, tp, &es, &ep);
+  lb_resolve(lb_words(out.ws), tile, epoch, ts, tp, &es, &ep, out.err);
   const bool fits = es + ts <= out.sign_cap && ep + tp <= out.payload_cap;
   if (lane == 0) {
     out.toff[2 * tile] = es;

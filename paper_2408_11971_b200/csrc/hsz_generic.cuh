@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(kThreads) tile_offsets_kernel(const uint8_t* w
   cta_excl_scan2(sb, pb, &es, &ep, &ts, &tp);
   if (threadIdx.x < 32) {
     uint64_t xs, xp;
-    lookback(lw, tile, s_epoch, ts, tp, &xs, &xp);
+    lookback(lw, tile, s_epoch, ts, tp, &xs, &xp, err);
     if (threadIdx.x == 0) {
       toff[2 * tile] = xs;
       toff[2 * tile + 1] = xp;

@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(kEncThreads, Src::kMinBlocks) encode_kernel(Sr
       const uint32_t* packed = reinterpret_cast<const uint32_t*>(bufs + b * L::kBuf);
       const uint32_t* sgn = reinterpret_cast<const uint32_t*>(bufs + b * L::kBuf + L::kPackedCap);
       uint64_t es, ep;
-      resolve_prefix(lw, t, epoch, ts, tp, &es, &ep);
+      resolve_prefix(lw, t, epoch, ts, tp, &es, &ep, out.err);
       const bool fits = es + ts <= out.sign_cap && ep + tp <= out.payload_cap;
       if (lane == 0) {
         out.toff[2 * t] = es;
@@ -734,9 +734,9 @@ __global__ void __launch_bounds__(kEncThreads, Src::kMinBlocks) encode_kernel(Sr
     if (warp == 0) {
       uint64_t es, ep;
       if (published) {
-        resolve_prefix(lw, t, epoch, agg_s, agg_p, &es, &ep);
+        resolve_prefix(lw, t, epoch, agg_s, agg_p, &es, &ep, out.err);
       } else {
-        lookback(lw, t, epoch, agg_s, agg_p, &es, &ep);
+        lookback(lw, t, epoch, agg_s, agg_p, &es, &ep, out.err);
       }
       if (lane == 0) {
         s_excl_s = es;

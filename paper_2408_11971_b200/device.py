@@ -26,7 +26,7 @@ import threading
 import numpy as np
 
 from . import _native as N
-from .errors import CapacityExceeded, raise_for_flags
+from .errors import ERR_LOOKBACK_TIMEOUT, CapacityExceeded, raise_for_flags
 from .model import CompressedStream, QuantParams
 
 _torch = None
@@ -70,9 +70,13 @@ def ptr(t) -> int:
 
 DTYPE_CODE = {"f32": N.HSZ_F32, "f64": N.HSZ_F64}
 
-# payload capacity policy: the exact worst case (8 bytes/element) when it is
-# affordable, else 4 bytes/element with an exact-size retry on overflow
-_PAYLOAD_BOUND_LIMIT = 16 << 30
+# payload capacity policy: the exact worst case (8 bytes/element) up to 2 GiB
+# (fields up to 2^28 values, every single-GPU config), else 2 bytes/element
+# (16-bit mean width; the 2048^3 config-5 field needs ~1.1) with an
+# exact-size retry on overflow -- a whole-field config-5 chain on one GPU
+# then fits 180 GB of HBM, and so do shards of it sharing one GPU
+_PAYLOAD_BOUND_LIMIT = 2 << 30
+_PAYLOAD_BIG_BYTES_PER_ELEM = 2
 _WS_REINIT_USES = 1 << 22
 
 
@@ -134,6 +138,18 @@ class Context:
     def synchronize(self):
         self.stream.synchronize()
 
+    def raise_flags(self, flags: int, what: str = "") -> None:
+        """raise_for_flags, after re-initialising the workspace when an
+        encoder's look-back watchdog fired (its tickets / epoch may be left
+        inconsistent; the next launch must start from a clean slate)."""
+        if flags & ERR_LOOKBACK_TIMEOUT and self.ws is not None:
+            self.stream.synchronize()
+            N.check(self.lib.hsz_workspace_init(ptr(self.ws), self.ws_bytes, self.handle),
+                    "workspace init")
+            self.stream.synchronize()
+            self.ws_uses = 0
+        raise_for_flags(flags, what)
+
     def read_flags(self) -> int:
         """Synchronize, read and clear the sticky error word."""
         self.stream.synchronize()
@@ -144,7 +160,7 @@ class Context:
         return v
 
     def check(self, what: str = "") -> None:
-        raise_for_flags(self.read_flags(), what)
+        self.raise_flags(self.read_flags(), what)
 
     def next_seq(self) -> int:
         self.mailbox_seq += 1
@@ -166,7 +182,7 @@ class Context:
         if flags:
             self.err.zero_()
             self.stream.synchronize()
-            raise_for_flags(flags, what)
+            self.raise_flags(flags, what)
         return mb[1:1 + nwords].copy()
 
     def fetch_result(self, nbytes: int, what: str = ""):
@@ -180,7 +196,7 @@ class Context:
         if flags:
             self.err.zero_()
             self.stream.synchronize()
-            raise_for_flags(flags, what)
+            self.raise_flags(flags, what)
         return host[16:16 + nbytes].copy()
 
     def fetch_checked(self, tensors, what: str = ""):
@@ -210,7 +226,7 @@ class Context:
         if flags:
             self.err.zero_()
             self.stream.synchronize()
-            raise_for_flags(flags, what)
+            self.raise_flags(flags, what)
         return out[:-1]
 
     def empty(self, n, dtype):
@@ -275,7 +291,7 @@ def payload_capacity(lib, n: int, k: int) -> int:
     bound = int(lib.hsz_payload_bound(n, k))
     if bound <= _PAYLOAD_BOUND_LIMIT:
         return bound
-    return max(4 * n, 1 << 20)
+    return max(_PAYLOAD_BIG_BYTES_PER_ELEM * n, 1 << 20)
 
 
 class DeviceStream:
@@ -395,7 +411,7 @@ class DeviceStream:
             if flags:
                 ctx.err.zero_()
                 ctx.stream.synchronize()
-                raise_for_flags(flags, "totals")
+                ctx.raise_flags(flags, "totals")
             self._totals = (int(row[0]), int(row[1]))
         if self._totals is None:
             T = self.ntiles
@@ -567,8 +583,7 @@ def new_stream_buffers(ctx: Context, params: QuantParams, payload_cap: int = Non
     n, k = params.element_count, params.block_len
     B = params.block_count
     T, scap, pbound, _ = geometry(n, k)
-    pcap = (pbound if pbound <= _PAYLOAD_BOUND_LIMIT else max(4 * n, 1 << 20)) \
-        if payload_cap is None else int(payload_cap)
+    pcap = payload_capacity(ctx.lib, n, k) if payload_cap is None else int(payload_cap)
 
     def up(v):
         return (v + 255) & ~255
@@ -600,7 +615,7 @@ def run_encoder(ctx: Context, params: QuantParams, launch) -> DeviceStream:
         return ds                       # overflow impossible: stay asynchronous
     flags = ctx.read_flags()
     if flags & ~(1 << 6):
-        raise_for_flags(flags & ~(1 << 6))
+        ctx.raise_flags(flags & ~(1 << 6))
     if flags & (1 << 6):
         T = geometry(n, k)[0]
         need = int(ds.toff[2 * T + 1].item())
@@ -612,5 +627,5 @@ def run_encoder(ctx: Context, params: QuantParams, launch) -> DeviceStream:
         if flags:
             if flags & (1 << 6):
                 raise CapacityExceeded("payload capacity retry failed")
-            raise_for_flags(flags)
+            ctx.raise_flags(flags)
     return ds

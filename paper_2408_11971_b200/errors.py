@@ -52,6 +52,12 @@ class VerificationMismatch(HoszpError):
     """A homomorphic result disagrees with the traditional workflow."""
 
 
+class DeviceTimeout(HoszpError, RuntimeError):
+    """A device-side wait gave up (the encoders' look-back watchdog,
+    HSZ_ERR_LOOKBACK_TIMEOUT): the operation's output is undefined.  Not a
+    reference error class -- it replaces a GPU hang."""
+
+
 class CapacityExceeded(HoszpError):
     """Internal: an output section outgrew its preallocated device buffer.
 
@@ -69,6 +75,7 @@ ERR_OUTLIER_OVERFLOW = 1 << 5  # outlier outside int32            -> OutlierOver
 ERR_CAPACITY = 1 << 6         # output buffer too small (retry)
 ERR_OUTPUT_NONFINITE = 1 << 7  # decoded value overflowed the dtype -> ValueError
 ERR_BAD_WIDTH = 1 << 8        # width > 64 in a stream           -> GeometryMismatch
+ERR_LOOKBACK_TIMEOUT = 1 << 9  # encoder look-back watchdog fired   -> DeviceTimeout
 
 
 def raise_for_flags(flags: int, what: str = "") -> None:
@@ -82,6 +89,9 @@ def raise_for_flags(flags: int, what: str = "") -> None:
     if not flags:
         return
     tag = f" ({what})" if what else ""
+    if flags & ERR_LOOKBACK_TIMEOUT:
+        raise DeviceTimeout("an encoder's look-back wait timed out; the output is undefined "
+                            "and the workspace was re-initialised" + tag)
     if flags & ERR_NONFINITE:
         raise ValueError("raw data must be finite (no NaN/Inf)" + tag)
     if flags & ERR_BAD_WIDTH:

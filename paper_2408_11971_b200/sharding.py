@@ -95,17 +95,46 @@ class HostAllGather:
         root = "/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir()
         path = os.path.join(root, f"hsz_coll_{info[0][1]}")
         size = int(self.lib.hsz_hostcoll_bytes(world))
+        token = info[0][1].encode()            # rank 0 writes it, every rank must read it back
+        ok, err = True, ""
         if rank == 0:
-            fd = os.open(path, os.O_CREAT | os.O_EXCL | os.O_RDWR, 0o600)
-            os.ftruncate(fd, size)
-            os.close(fd)
+            try:
+                fd = os.open(path, os.O_CREAT | os.O_EXCL | os.O_RDWR, 0o600)
+                os.ftruncate(fd, size + 64)
+                os.pwrite(fd, token, size)
+                os.close(fd)
+            except OSError as e:
+                ok, err = False, repr(e)
         dist.barrier(group=group)
-        fd = os.open(path, os.O_RDWR)
-        self._mm = mmap.mmap(fd, size)
-        os.close(fd)
-        dist.barrier(group=group)
+        mm = None
+        if ok:
+            # a shared hostname does not prove a shared /dev/shm (private IPC
+            # namespaces, pods with equal hostnames): map the segment and
+            # check rank 0's token; every rank then agrees on the outcome
+            try:
+                fd = os.open(path, os.O_RDWR)
+                try:
+                    mm = mmap.mmap(fd, size + 64)
+                finally:
+                    os.close(fd)
+                ok = mm[size:size + len(token)] == token
+                if not ok:
+                    err = "token mismatch"
+            except OSError as e:
+                ok, err = False, repr(e)
+        votes = [None] * world
+        dist.all_gather_object(votes, (ok, err), group=group)
         if rank == 0:
-            os.unlink(path)              # the mappings stay; nothing left behind
+            try:
+                os.unlink(path)          # the mappings stay; nothing left behind
+            except OSError:
+                pass
+        bad = [(r, e) for r, (v, e) in enumerate(votes) if not v]
+        if bad:
+            if mm is not None:
+                mm.close()
+            raise RuntimeError(f"node-local shared memory unusable on rank {bad[0][0]}: {bad[0][1]}")
+        self._mm = mm
         self._buf = (ctypes.c_char * size).from_buffer(self._mm)
         self._addr = ctypes.addressof(self._buf)
         self._round = 0
@@ -140,10 +169,15 @@ def _i2f(v: int) -> float:
 class Collectives:
     """The three collectives over a torch.distributed process group.
 
-    ``host_shm`` (default: on unless ``HSZ_HOSTCOLL=0``): the small host-scalar
-    exchanges (C1-C3, the byte counts of ``allreduce_streams``, timing maxima)
-    go through a node-local shared-memory all-gather when all ranks share
-    one host; bulk data always moves over the process group (NCCL)."""
+    By default every exchange runs on the process group (NCCL on the GPU
+    path, as north_star names them: C1 an allreduce MIN, C2 an allgather of
+    the shard byte counts, C3 an allreduce SUM of int64 partial sums).
+    ``host_shm=True`` (or ``HSZ_HOSTCOLL=1``) moves the small host-scalar
+    exchanges to a node-local shared-memory all-gather (4-8 us instead of
+    44-57 us per NCCL round trip, profiles/r1e_coll_latency.json) when every
+    rank can map the same segment; setup failure on any rank makes every
+    rank fall back to the process group together.  Bulk data always moves
+    over the process group."""
 
     def __init__(self, group=None, device=None, host_shm=None):
         import os
@@ -162,13 +196,13 @@ class Collectives:
                 else torch.device("cpu")
         self.device = device
         if host_shm is None:
-            host_shm = os.environ.get("HSZ_HOSTCOLL", "1") != "0"
+            host_shm = os.environ.get("HSZ_HOSTCOLL", "0") == "1"
         self._hc = None
         if host_shm:
             try:
                 self._hc = HostAllGather(dist, group, self.rank, self.world)
             except RuntimeError:
-                self._hc = None          # ranks on several hosts: process group only
+                self._hc = None          # agreed on every rank: process group only
 
     @property
     def host_shm(self) -> bool:
@@ -207,15 +241,22 @@ class Collectives:
         return ShardLayout(self.rank, block0, so[self.rank], po[self.rank], st, pt)
 
     def global_moments(self, S: int, Q: int):
-        """C3: allgather of exact (S, Q) as 64-bit limbs, exact host sum."""
-        limbs = _to_limbs(S, Q)
-        rows = self._allgather_i64(limbs)
-        tot_s = tot_q = 0
-        for r in rows:
-            s, q = _from_limbs(r)
-            tot_s += s
-            tot_q += q
-        return tot_s, tot_q
+        """C3: exact global (S, Q).  On the process group: ONE allreduce SUM
+        of int64 partial sums -- S (int128) and Q (uint192) as ten 32-bit
+        chunks, so the sum cannot overflow for any world size below 2^31 and
+        the recombined totals are exact; on the shared-memory path an
+        allgather of 64-bit limbs and an exact host sum."""
+        if self._hc is not None:
+            rows = self._hc(_to_limbs(S, Q))
+            tot_s = tot_q = 0
+            for r in rows:
+                s, q = _from_limbs(r)
+                tot_s += s
+                tot_q += q
+            return tot_s, tot_q
+        t = self.torch.tensor(_to_chunks(S, Q), dtype=self.torch.int64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return _from_chunks(t.cpu().tolist())
 
     def global_offsets_many(self, block0: int, sizes):
         """C2 for several streams of this rank's shard in one exchange:
@@ -377,16 +418,14 @@ class Collectives:
     def _agreed(self, step, ctx):
         """Run one fold step and agree on its outcome across ranks: if any
         rank failed, every rank raises the error of highest precedence."""
-        from .errors import HoszpError, raise_for_flags
-
         err, res = None, None
         try:
             res = step()
             if ctx is not None:
                 flags = ctx.read_flags()
                 if flags:
-                    raise_for_flags(flags, "allreduce_streams")
-        except (HoszpError, ValueError) as e:
+                    ctx.raise_flags(flags, "allreduce_streams")
+        except Exception as e:        # any failure still takes part in the agreement
             err = e
         code = 0 if err is None else _precedence(err)
         codes = [r[0] for r in self._allgather_i64([code])]
@@ -441,6 +480,24 @@ class Collectives:
         t = self.torch.tensor([value], dtype=self.torch.float64, device=self.device)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return float(t.item())
+
+
+def _to_chunks(S: int, Q: int):
+    """S (signed, two's complement mod 2^128) and Q (unsigned, < 2^192) as ten
+    non-negative 32-bit chunks (int64 slots: summable over < 2^31 ranks)."""
+    s = S & ((1 << 128) - 1)
+    return [(s >> (32 * k)) & 0xFFFFFFFF for k in range(4)] + \
+        [(Q >> (32 * k)) & 0xFFFFFFFF for k in range(6)]
+
+
+def _from_chunks(chunks):
+    """Sum of chunk vectors -> exact (S, Q) (S wrapped back to signed 128-bit)."""
+    c = [int(v) for v in chunks]
+    s = sum(c[k] << (32 * k) for k in range(4)) & ((1 << 128) - 1)
+    if s >= 1 << 127:
+        s -= 1 << 128
+    q = sum(c[4 + k] << (32 * k) for k in range(6))
+    return s, q
 
 
 def _to_limbs(S: int, Q: int):
@@ -544,14 +601,18 @@ def _params_digest(p) -> int:
 
 
 def _precedence(err) -> int:
-    """errors.raise_for_flags order (1 = highest)."""
-    from .errors import CapacityExceeded, GeometryMismatch, OutlierOverflow, QuantOverflow
+    """errors.raise_for_flags order (1 = highest); 7 = a failure outside the
+    reference's error classes (CUDA RuntimeError, OverflowError, ...)."""
+    from .errors import (CapacityExceeded, GeometryMismatch, HoszpError, OutlierOverflow,
+                         QuantOverflow)
 
     for code, cls in ((2, GeometryMismatch), (3, QuantOverflow), (4, OutlierOverflow),
                       (5, CapacityExceeded)):
         if isinstance(err, cls):
             return code
-    return 1 if isinstance(err, ValueError) else 6
+    if isinstance(err, ValueError):
+        return 1
+    return 6 if isinstance(err, HoszpError) else 7
 
 
 def _exc_by_code():
@@ -559,7 +620,7 @@ def _exc_by_code():
                          QuantOverflow)
 
     return {1: ValueError, 2: GeometryMismatch, 3: QuantOverflow, 4: OutlierOverflow,
-            5: CapacityExceeded, 6: HoszpError}
+            5: CapacityExceeded, 6: HoszpError, 7: RuntimeError}
 
 
 class _LazyCodes(dict):

@@ -148,6 +148,34 @@ def config5_slab(slab: int, seed: int = 4, device="cuda"):
     return (grf_device(shape, 11.0 / 3.0, (seed, slab), device) * 15.0 + 280.0).reshape(-1).float()
 
 
+CONFIG5_SLAB = 1 << 30          # values per slab (256 x 2048 x 2048)
+CONFIG5_N = 8 * CONFIG5_SLAB    # the whole 2048^3 field
+
+
+def config5_range(e0: int, e1: int, seed: int = 4, device="cuda", out=None):
+    """Elements [e0, e1) of the ONE 2048^3 config-5 field (flat row-major),
+    assembled from the slabs they overlap -- identical for any partition, so
+    a rank owning a contiguous block range generates exactly its share of
+    the same field.  `out` (optional) receives the values in place."""
+    import torch
+
+    if not (0 <= e0 <= e1 <= CONFIG5_N):
+        raise ValueError(f"config 5 range [{e0}, {e1}) outside [0, 2^33)")
+    if out is None:
+        out = torch.empty(e1 - e0, dtype=torch.float32, device=device)
+    s0, s1 = e0 // CONFIG5_SLAB, -(-e1 // CONFIG5_SLAB)
+    for s in range(s0, s1):
+        a = max(e0, s * CONFIG5_SLAB)
+        b = min(e1, (s + 1) * CONFIG5_SLAB)
+        if a >= b:
+            continue
+        slab = config5_slab(s, seed=seed, device=device)
+        out[a - e0:b - e0].copy_(slab[a - s * CONFIG5_SLAB:b - s * CONFIG5_SLAB])
+        del slab
+        torch.cuda.empty_cache()
+    return out
+
+
 def field(config: int, device=None):
     if config == 1:
         return config1()

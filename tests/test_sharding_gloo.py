@@ -336,3 +336,68 @@ def test_host_allgather_rounds(tmp_path, world):
 
     mp.spawn(_hc_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
     assert all((tmp_path / f"hc{r}.txt").read_text() == "ok" for r in range(world))
+
+
+def test_chunk_packing_sums_exactly():
+    """C3 on the process group: ten 32-bit chunks per rank, one allreduce SUM,
+    exact recombination -- also when S is negative on some ranks and the
+    totals carry across chunks."""
+    from paper_2408_11971_b200.sharding import _from_chunks, _to_chunks
+
+    cases = [(0, 0), (-5, 7), (-(2 ** 120), 2 ** 191 - 1), (2 ** 126 - 1, 2 ** 64), (-1, 1)]
+    for S, Q in cases:
+        assert _from_chunks(_to_chunks(S, Q)) == (S, Q)
+    ranks = [(-(2 ** 100) + 3, 2 ** 150 + 9), (2 ** 99, 2 ** 150 - 1), (-7, 0), (5, 2 ** 40)]
+    summed = [sum(col) for col in zip(*(_to_chunks(S, Q) for S, Q in ranks))]
+    assert _from_chunks(summed) == (sum(S for S, _ in ranks), sum(Q for _, Q in ranks))
+
+
+def _shm_fail_worker(rank, world, port, outdir, fail_rank):
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from paper_2408_11971_b200 import sharding
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        if rank == fail_rank:
+            # this rank cannot see the segment (a private IPC namespace)
+            real_open = os.open
+
+            def no_shm(path, *a, **k):
+                if "hsz_coll_" in str(path):
+                    raise FileNotFoundError(path)
+                return real_open(path, *a, **k)
+
+            os.open = no_shm
+        coll = sharding.Collectives(host_shm=True)
+        lo, hi = coll.global_range(float(rank), float(rank) + 1.0)
+        S, Q = coll.global_moments(-rank - 1, 2 ** 70 + rank)
+        lay = coll.global_offsets(rank, 10 + rank, 100 + rank)
+        with open(os.path.join(outdir, f"shm{rank}.txt"), "w") as f:
+            f.write(repr((coll.host_shm, lo, hi, S, Q, lay.sign_offset, lay.payload_total)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,fail_rank", [(2, 1), (3, 0), (3, 2)])
+def test_host_shm_setup_failure_falls_back_on_every_rank(tmp_path, world, fail_rank):
+    """A rank that cannot map the shared-memory segment (same hostname, other
+    IPC namespace) makes EVERY rank fall back to the process group together
+    -- no rank blocks in a barrier while another crashes."""
+    import torch.multiprocessing as mp
+
+    mp.spawn(_shm_fail_worker, args=(world, _free_port(), str(tmp_path), fail_rank),
+             nprocs=world, join=True)
+    got = [eval((tmp_path / f"shm{r}.txt").read_text()) for r in range(world)]
+    S = sum(-r - 1 for r in range(world))
+    Q = sum(2 ** 70 + r for r in range(world))
+    tot_s = sum(10 + r for r in range(world))
+    tot_p = sum(100 + r for r in range(world))
+    for r, g in enumerate(got):
+        assert g[0] is False
+        assert g[1:5] == (0.0, float(world), S, Q)
+        assert g[5] == sum(10 + q for q in range(r)) and g[6] == tot_p
+    assert tot_s > 0
