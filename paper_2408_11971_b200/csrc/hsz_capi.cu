@@ -1050,10 +1050,7 @@ int hsz_elementwise(const uint8_t* wa, const int32_t* oa, const uint8_t* sa, con
       A, k32::SinkBins{bins}, err);
   gen::decode_kernel<ops::SinkCombineBins><<<static_cast<unsigned>(nt), gen::kThreads, 0, st>>>(
       B, ops::SinkCombineBins{bins, sub}, err);
-  if (k == 32) {
-    const k32::EncodeOut out{ow, oo, os, sign_cap, op, payload_cap, otoff, err, ws};
-    return launch_encode32(k32::SrcBins{bins, n}, out, n, st);
-  }
+  // (k == 32 returned above through the fused recode kernel)
   return launch_encode_generic(gen::GBins{bins}, n, k, ow, oo, os, sign_cap, op, payload_cap, otoff,
                                err, ws, st);
 }

@@ -140,8 +140,9 @@ __device__ __forceinline__ void stage_tile(const StreamIn& s, uint64_t t, uint64
 
 // Register decode of this thread's block (w <= kFastW, |o| < 2^29): bins as
 // int32 (|bin| < 2^30).  kFull: a full block (len == 32, no tail checks);
-// otherwise elements past `len` replicate the last live bin.  Fields are read
-// G at a time (G * w <= 32): one window refill check per G fields.
+// otherwise elements past `len` replicate the last live bin (kResid: their
+// residuals are 0).  Fields are read G at a time (G * w <= 32): one window
+// refill check per G fields.
 #ifndef HSZ_REFILL_AHEAD
 #define HSZ_REFILL_AHEAD 1
 #endif

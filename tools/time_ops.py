@@ -59,7 +59,7 @@ def main():
     ap.add_argument("--ops", default="")
     a = ap.parse_args()
     cfg = W.CONFIGS[a.config]
-    x = W.field(a.config, device="cuda")
+    x = W.field(a.config)
     if not torch.is_tensor(x):
         x = torch.from_numpy(x)
     x = x.cuda().contiguous().reshape(-1)
