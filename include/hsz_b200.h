@@ -58,6 +58,7 @@ extern "C" {
 #define HSZ_OK 0
 #define HSZ_EINVAL (-1)
 #define HSZ_ECUDA (-2)
+#define HSZ_ETIMEDOUT (-3) /* a host-side wait on the stream exceeded its bound */
 
 /* device error-word bits */
 #define HSZ_ERR_NONFINITE (1u << 0)         /* ValueError      codec.py:52-53   */
@@ -244,6 +245,12 @@ int hsz_mailbox_wait(const uint64_t* mailbox, uint64_t seq, void* stream);
 uint64_t hsz_hostcoll_bytes(int world);
 int hsz_hostcoll_allgather(void* shm, int rank, int world, uint64_t round, const int64_t* vals,
                            int nvals, int64_t* out, double timeout_s);
+
+/* Bound (seconds, default 600) of every host-side wait of this library
+ * (hsz_stream_sync, hsz_fetch, hsz_mailbox_wait): past it they return
+ * HSZ_ETIMEDOUT instead of blocking forever on a hung kernel.  seconds <= 0
+ * leaves it unchanged; returns the previous bound. */
+double hsz_set_host_wait_timeout(double seconds);
 
 /* library identification (for the loader's sanity check) */
 const char* hsz_version(void);

@@ -16,6 +16,7 @@ from . import build as _build
 HSZ_OK = 0
 HSZ_EINVAL = -1
 HSZ_ECUDA = -2
+HSZ_ETIMEDOUT = -3
 HSZ_F32, HSZ_F64 = 0, 1
 HSZ_OUT_F32, HSZ_OUT_F64, HSZ_OUT_BINS = 0, 1, 2
 HSZ_OUT_BINS_ADD, HSZ_OUT_BINS_SUB = 3, 4
@@ -34,6 +35,7 @@ _dbl = C.c_double
 SIGNATURES = {
     "hsz_version": (C.c_char_p, []),
     "hsz_set_lookback_watchdog": (C.c_uint, [C.c_uint]),
+    "hsz_set_host_wait_timeout": (C.c_double, [C.c_double]),
     "hsz_trace_read": (_int, [_vp, _int, _int]),
     "hsz_trace_lookback": (_int, [_vp]),
     "hsz_tile_count": (_u64, [_u64, _u32]),
@@ -107,5 +109,10 @@ def load(build_if_missing: bool = True):
 
 
 def check(rc: int, what: str) -> None:
+    if rc == HSZ_ETIMEDOUT:
+        from .errors import DeviceTimeout
+
+        raise DeviceTimeout(f"{what}: the CUDA stream did not drain within the host wait bound "
+                            "(a kernel hung; hsz_set_host_wait_timeout)")
     if rc != HSZ_OK:
         raise RuntimeError(f"{what} failed with status {rc} (invalid argument or CUDA launch error)")

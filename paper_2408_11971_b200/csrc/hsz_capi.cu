@@ -230,49 +230,75 @@ __global__ void __launch_bounds__(kMmThreads) minmax_f32_kernel(const float* __r
 
 // ---- K4 for block_len 32: every stored sign byte flips (full blocks have 4
 // sign bytes, all bits live); only the partial tail block's last byte keeps
-// its zero padding.  Sign chunks and outlier chunks share one index space;
-// each thread issues up to 4 independent 16-byte loads.
-__global__ void __launch_bounds__(kThreads) negate32_kernel(
+// its zero padding (ops.py:88-109).  One wave of CTAs (SMs x 8); per round a
+// thread issues ALL its loads -- kStreamU 16-byte outlier chunks and
+// kStreamU 16-byte sign chunks -- before it computes or stores anything, so
+// a round costs one DRAM round trip (the arrays are 10s of MB: latency, not
+// bandwidth, is what a naive grid-stride loop pays).
+constexpr int kStreamU = 4;
+constexpr int kStreamThreads = 256;
+
+__device__ __forceinline__ int4 neg4(int4 v, uint32_t& flags) {
+  flags |= (v.x == INT32_MIN) | (v.y == INT32_MIN) | (v.z == INT32_MIN) | (v.w == INT32_MIN)
+               ? HSZ_ERR_OUTLIER_OVERFLOW : 0u;
+  return make_int4(-v.x, -v.y, -v.z, -v.w);
+}
+
+__global__ void __launch_bounds__(kStreamThreads) negate32_kernel(
     const uint8_t* __restrict__ widths, const int32_t* __restrict__ oin, int32_t* __restrict__ oout,
     const uint8_t* __restrict__ sin, uint8_t* __restrict__ sout, const uint64_t* __restrict__ toff,
     uint64_t ntiles, uint64_t n, uint64_t nblocks, uint64_t sign_chunks_max, uint32_t* err) {
-  const uint64_t S = __ldg(toff + 2 * ntiles);
-  const uint64_t nsc = (S + 15) / 16;                  // sign chunks in use
+  const uint64_t S = __ldg(toff + 2 * ntiles);          // issued first: the sign bound
   const uint64_t noc = nblocks / 4;                    // full outlier chunks
   const uint32_t r = static_cast<uint32_t>(n % 32);
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int4* oin4 = reinterpret_cast<const int4*>(oin);
+  int4* oout4 = reinterpret_cast<int4*>(oout);
+  const uint4* sin4 = reinterpret_cast<const uint4*>(sin);
+  uint4* sout4 = reinterpret_cast<uint4*>(sout);
   uint32_t flags = 0;
-  // outliers first (independent of S)
-  for (uint64_t c = tid; c < noc; c += stride) {
-    int4 v = reinterpret_cast<const int4*>(oin)[c];
-    flags |= (v.x == INT32_MIN) | (v.y == INT32_MIN) | (v.z == INT32_MIN) | (v.w == INT32_MIN)
-                 ? HSZ_ERR_OUTLIER_OVERFLOW : 0u;
-    v.x = -v.x;
-    v.y = -v.y;
-    v.z = -v.z;
-    v.w = -v.w;
-    reinterpret_cast<int4*>(oout)[c] = v;
+  (void)sign_chunks_max;
+  for (uint64_t c0 = tid;; c0 += kStreamU * stride) {
+    const uint64_t nsc = (S + 15) / 16;                // sign chunks in use
+    if (c0 >= noc && c0 >= nsc) break;
+    int4 ov[kStreamU];
+    uint4 sv[kStreamU];
+#pragma unroll
+    for (int u = 0; u < kStreamU; ++u) {
+      const uint64_t c = c0 + u * stride;
+      if (c < noc) ov[u] = __ldcs(oin4 + c);
+    }
+#pragma unroll
+    for (int u = 0; u < kStreamU; ++u) {
+      const uint64_t c = c0 + u * stride;
+      if (c < nsc) sv[u] = __ldcs(sin4 + c);
+    }
+#pragma unroll
+    for (int u = 0; u < kStreamU; ++u) {
+      const uint64_t c = c0 + u * stride;
+      if (c < noc) oout4[c] = neg4(ov[u], flags);
+    }
+#pragma unroll
+    for (int u = 0; u < kStreamU; ++u) {
+      const uint64_t c = c0 + u * stride;
+      if (c < nsc) {
+        uint4 v = make_uint4(~sv[u].x, ~sv[u].y, ~sv[u].z, ~sv[u].w);
+        if (c == nsc - 1 && (r & 7u) != 0 && widths[nblocks - 1] > 0) {
+          // the tail block's last sign byte: its padding bits stay zero
+          const uint32_t j = static_cast<uint32_t>((S - 1) & 15u);
+          const uint32_t tmask = (0xFFu << (8 - (r & 7u))) & 0xFFu;
+          reinterpret_cast<uint32_t*>(&v)[j >> 2] ^= (0xFFu ^ tmask) << (8 * (j & 3u));
+        }
+        sout4[c] = v;
+      }
+    }
   }
-  for (uint64_t b = noc * 4 + tid; b < nblocks; b += stride) {
+
+  for (uint64_t b = noc * 4 + tid; b < nblocks; b += stride) {   // the last < 4 outliers
     const int32_t v = oin[b];
     if (v == INT32_MIN) flags |= HSZ_ERR_OUTLIER_OVERFLOW;
     oout[b] = -v;
-  }
-  (void)sign_chunks_max;
-  for (uint64_t c = tid; c < nsc; c += stride) {
-    uint4 v = reinterpret_cast<const uint4*>(sin)[c];
-    v.x = ~v.x;
-    v.y = ~v.y;
-    v.z = ~v.z;
-    v.w = ~v.w;
-    if (c == nsc - 1 && (r & 7u) != 0 && widths[nblocks - 1] > 0) {
-      // the tail block's last sign byte: its padding bits stay zero
-      const uint32_t j = static_cast<uint32_t>((S - 1) & 15u);
-      const uint32_t tmask = (0xFFu << (8 - (r & 7u))) & 0xFFu;
-      reinterpret_cast<uint32_t*>(&v)[j >> 2] ^= (0xFFu ^ tmask) << (8 * (j & 3u));
-    }
-    reinterpret_cast<uint4*>(sout)[c] = v;
   }
   if (flags) atomicOr(err, flags);
 }
@@ -339,27 +365,31 @@ __device__ __forceinline__ int32_t sadd1(int32_t o, int64_t rs, uint32_t& flags)
   return static_cast<int32_t>(static_cast<int64_t>(v));
 }
 
-__global__ void __launch_bounds__(kThreads) sadd_kernel(const int32_t* oin, int32_t* oout,
-                                                        uint64_t nblocks, int64_t rs,
-                                                        uint32_t* err) {
+__global__ void __launch_bounds__(kStreamThreads) sadd_kernel(const int32_t* oin, int32_t* oout,
+                                                              uint64_t nblocks, int64_t rs,
+                                                              uint32_t* err) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   uint32_t flags = 0;
   const bool vec = ((reinterpret_cast<uintptr_t>(oin) | reinterpret_cast<uintptr_t>(oout)) & 15u) == 0;
   const uint64_t nv = vec ? nblocks / 4 : 0;
-  uint64_t i = tid;
-  for (; i + stride < nv; i += 2 * stride) {   // two independent 16-byte loads in flight
-    int4 a = reinterpret_cast<const int4*>(oin)[i];
-    int4 b = reinterpret_cast<const int4*>(oin)[i + stride];
-    a = make_int4(sadd1(a.x, rs, flags), sadd1(a.y, rs, flags), sadd1(a.z, rs, flags), sadd1(a.w, rs, flags));
-    b = make_int4(sadd1(b.x, rs, flags), sadd1(b.y, rs, flags), sadd1(b.z, rs, flags), sadd1(b.w, rs, flags));
-    reinterpret_cast<int4*>(oout)[i] = a;
-    reinterpret_cast<int4*>(oout)[i + stride] = b;
-  }
-  for (; i < nv; i += stride) {
-    int4 a = reinterpret_cast<const int4*>(oin)[i];
-    a = make_int4(sadd1(a.x, rs, flags), sadd1(a.y, rs, flags), sadd1(a.z, rs, flags), sadd1(a.w, rs, flags));
-    reinterpret_cast<int4*>(oout)[i] = a;
+  const int4* in4 = reinterpret_cast<const int4*>(oin);
+  int4* out4 = reinterpret_cast<int4*>(oout);
+  // one DRAM round trip per round: all kStreamU loads issued before any store
+  for (uint64_t c0 = tid; c0 < nv; c0 += kStreamU * stride) {
+    int4 v[kStreamU];
+#pragma unroll
+    for (int u = 0; u < kStreamU; ++u) {
+      const uint64_t c = c0 + u * stride;
+      if (c < nv) v[u] = __ldcs(in4 + c);
+    }
+#pragma unroll
+    for (int u = 0; u < kStreamU; ++u) {
+      const uint64_t c = c0 + u * stride;
+      if (c < nv)
+        out4[c] = make_int4(sadd1(v[u].x, rs, flags), sadd1(v[u].y, rs, flags),
+                            sadd1(v[u].z, rs, flags), sadd1(v[u].w, rs, flags));
+    }
   }
   for (uint64_t j = nv * 4 + tid; j < nblocks; j += stride) oout[j] = sadd1(oin[j], rs, flags);
   if (flags) atomicOr(err, flags);
@@ -396,6 +426,18 @@ static inline uint64_t grid_for(uint64_t items, uint64_t per_thread, int threads
   uint64_t g = ceil_div(ceil_div(items, per_thread), threads);
   if (g < 1) g = 1;
   return g < cap ? g : cap;
+}
+
+// one resident wave of 256-thread streaming CTAs: SMs x 8
+static inline uint64_t stream_wave() {
+  static int sms = 0, dev_cached = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev_cached != dev) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    dev_cached = dev;
+  }
+  return static_cast<uint64_t>(sms > 0 ? sms : 148) * 8;
 }
 
 static inline uint32_t tail_len_of(uint64_t n, uint32_t k) {
@@ -738,15 +780,45 @@ int hsz_copy_d2h(void* host, const void* dev, uint64_t bytes, void* stream) {
              : HSZ_ECUDA;
 }
 
+// Host-side waits are bounded: a kernel that never finishes (a GPU-side hang)
+// turns into HSZ_ETIMEDOUT after g_host_wait_s seconds instead of blocking the
+// calling thread forever (which no Python-level timeout could interrupt).
+static double g_host_wait_s = 600.0;
+
+static inline double wall_s() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return static_cast<double>(ts.tv_sec) + 1e-9 * static_cast<double>(ts.tv_nsec);
+}
+
+static int bounded_sync(cudaStream_t st) {
+  cudaError_t e = cudaStreamQuery(st);
+  if (e == cudaSuccess) return HSZ_OK;
+  const double t0 = wall_s();
+  for (uint64_t it = 1;; ++it) {
+    if (e == cudaSuccess) return HSZ_OK;
+    if (e != cudaErrorNotReady) return HSZ_ECUDA;
+    if ((it & 1023u) == 0 && wall_s() - t0 > g_host_wait_s) return HSZ_ETIMEDOUT;
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+    e = cudaStreamQuery(st);
+  }
+}
+
+double hsz_set_host_wait_timeout(double seconds) {
+  const double old = g_host_wait_s;
+  if (seconds > 0) g_host_wait_s = seconds;
+  return old;
+}
+
 int hsz_fetch(void* host, const void* dev, uint64_t bytes, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess) return HSZ_ECUDA;
-  return cudaStreamSynchronize(st) == cudaSuccess ? HSZ_OK : HSZ_ECUDA;
+  return bounded_sync(st);
 }
 
-int hsz_stream_sync(void* stream) {
-  return cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) == cudaSuccess ? HSZ_OK : HSZ_ECUDA;
-}
+int hsz_stream_sync(void* stream) { return bounded_sync(static_cast<cudaStream_t>(stream)); }
 
 uint64_t hsz_tile_count(uint64_t n, uint32_t k) {
   if (k == 0) return 0;
@@ -960,9 +1032,10 @@ int hsz_negate(const uint8_t* widths, const int32_t* oin, int32_t* oout, const u
   const bool aligned = ((reinterpret_cast<uintptr_t>(oin) | reinterpret_cast<uintptr_t>(oout) |
                          reinterpret_cast<uintptr_t>(sin) | reinterpret_cast<uintptr_t>(sout)) & 15u) == 0;
   if (k == 32 && aligned) {
-    const uint64_t items = nb / 4 + sign_bound / 16;
-    const unsigned g = static_cast<unsigned>(grid_for(items, 2, ops::kThreads, 148 * 32));
-    ops::negate32_kernel<<<g, ops::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+    const uint64_t items = nb / 4 > sign_bound / 16 ? nb / 4 : sign_bound / 16;
+    const unsigned g = static_cast<unsigned>(
+        grid_for(items, ops::kStreamU, ops::kStreamThreads, stream_wave()));
+    ops::negate32_kernel<<<g, ops::kStreamThreads, 0, static_cast<cudaStream_t>(stream)>>>(
         widths, oin, oout, sin, sout, toff, nt, n, nb, sign_bound / 16, err);
     return launch_status();
   }
@@ -976,8 +1049,9 @@ int hsz_negate(const uint8_t* widths, const int32_t* oin, int32_t* oout, const u
 int hsz_scalar_add(const int32_t* oin, int32_t* oout, uint64_t nblocks, int64_t rs, uint32_t* err,
                    void* stream) {
   if (!oin || !oout || !err || nblocks == 0) return HSZ_EINVAL;
-  const unsigned g = static_cast<unsigned>(grid_for(nblocks, 8, ops::kThreads, 148 * 16));
-  ops::sadd_kernel<<<g, ops::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(oin, oout, nblocks, rs, err);
+  const unsigned g = static_cast<unsigned>(
+      grid_for(nblocks, 4 * ops::kStreamU, ops::kStreamThreads, stream_wave()));
+  ops::sadd_kernel<<<g, ops::kStreamThreads, 0, static_cast<cudaStream_t>(stream)>>>(oin, oout, nblocks, rs, err);
   return launch_status();
 }
 
@@ -1154,12 +1228,16 @@ int hsz_mailbox_wait(const uint64_t* mailbox, uint64_t seq, void* stream) {
   // stream died (error) or drained without posting (caller falls back)
   const volatile uint64_t* w = mailbox;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double t0 = -1.0;
   for (uint64_t it = 1;; ++it) {
     if (*w == seq) {
       __atomic_thread_fence(__ATOMIC_ACQUIRE);
       return HSZ_OK;
     }
     if ((it & 4095u) == 0) {
+      const double now = wall_s();
+      if (t0 < 0) t0 = now;
+      else if (now - t0 > g_host_wait_s) return HSZ_ETIMEDOUT;
       const cudaError_t e = cudaStreamQuery(st);
       if (e == cudaSuccess) {
         if (*w == seq) {

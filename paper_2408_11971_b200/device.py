@@ -136,27 +136,29 @@ class Context:
         return ptr(self.ws), self.ws_bytes
 
     def synchronize(self):
-        self.stream.synchronize()
+        """Wait for the stream, bounded (hsz_stream_sync: a hung kernel raises
+        DeviceTimeout instead of blocking forever)."""
+        N.check(self.lib.hsz_stream_sync(self.handle), "stream sync")
 
     def raise_flags(self, flags: int, what: str = "") -> None:
         """raise_for_flags, after re-initialising the workspace when an
         encoder's look-back watchdog fired (its tickets / epoch may be left
         inconsistent; the next launch must start from a clean slate)."""
         if flags & ERR_LOOKBACK_TIMEOUT and self.ws is not None:
-            self.stream.synchronize()
+            self.synchronize()
             N.check(self.lib.hsz_workspace_init(ptr(self.ws), self.ws_bytes, self.handle),
                     "workspace init")
-            self.stream.synchronize()
+            self.synchronize()
             self.ws_uses = 0
         raise_for_flags(flags, what)
 
     def read_flags(self) -> int:
         """Synchronize, read and clear the sticky error word."""
-        self.stream.synchronize()
+        self.synchronize()
         v = int(self.err[0].item())
         if v:
             self.err.zero_()
-            self.stream.synchronize()
+            self.synchronize()
         return v
 
     def check(self, what: str = "") -> None:
@@ -175,13 +177,14 @@ class Context:
         if rc != N.HSZ_OK:
             if rc == N.HSZ_EINVAL:
                 return self.fetch_result(8 * nwords, what).view(np.uint64)
-            self.stream.synchronize()            # surfaces the CUDA error
+            N.check(rc, f"{what}: mailbox wait")      # DeviceTimeout on a hung kernel
+            self.synchronize()                        # surfaces the CUDA error
             raise RuntimeError(f"{what}: stream failed while waiting for the result")
         mb = self._mailbox_np
         flags = int(mb[1 + nwords]) & 0xFFFFFFFF
         if flags:
             self.err.zero_()
-            self.stream.synchronize()
+            self.synchronize()
             self.raise_flags(flags, what)
         return mb[1:1 + nwords].copy()
 
@@ -195,7 +198,7 @@ class Context:
         flags = int(host[:4].view(np.int32)[0])
         if flags:
             self.err.zero_()
-            self.stream.synchronize()
+            self.synchronize()
             self.raise_flags(flags, what)
         return host[16:16 + nbytes].copy()
 

@@ -61,7 +61,12 @@ def _worker(rank, world, port, outdir, case):
     torch.cuda.set_device(0)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import datetime
+    import faulthandler
+
+    faulthandler.dump_traceback_later(300, exit=True)       # a hung rank shows where it hangs
+    dist.init_process_group("gloo", rank=rank, world_size=world,
+                            timeout=datetime.timedelta(seconds=240))
     try:
         coll = Collectives()
         n, eps = CASES[case]

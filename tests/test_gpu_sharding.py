@@ -132,7 +132,9 @@ def _rank_worker(rank, world, port, refs, want, outdir, host_shm):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import datetime
+    import faulthandler
 
+    faulthandler.dump_traceback_later(900, exit=True)       # a hung rank shows where it hangs
     dist.init_process_group("gloo", rank=rank, world_size=world,
                             timeout=datetime.timedelta(seconds=300))
     msgs = []

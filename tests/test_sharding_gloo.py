@@ -16,6 +16,11 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+import datetime  # noqa: E402
+
+_PG_TIMEOUT = datetime.timedelta(seconds=180)   # a stuck peer fails the test, not the suite
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -39,7 +44,7 @@ def _worker(rank, world, port, n, rel, outdir, host_shm=True):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=_PG_TIMEOUT)
     try:
         coll = Collectives(host_shm=host_shm)
         assert coll.host_shm == host_shm
@@ -164,7 +169,7 @@ def _stream_worker(rank, world, port, outdir, case):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=_PG_TIMEOUT)
     try:
         coll = Collectives()
         n, seed, eps = STREAM_CASES[case]
@@ -214,7 +219,7 @@ def _err_worker(rank, world, port, outdir):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=_PG_TIMEOUT)
     try:
         coll = Collectives()
         n = 32 * 128 * 3
@@ -269,7 +274,7 @@ def _write_worker(rank, world, port, path):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=_PG_TIMEOUT)
     try:
         coll = Collectives()
         n, k = 32 * 700 + 9, 32
@@ -311,7 +316,7 @@ def _hc_worker(rank, world, port, outdir):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=_PG_TIMEOUT)
     try:
         hc = HostAllGather(dist, None, rank, world, timeout_s=60)
         rows = []
@@ -360,7 +365,7 @@ def _shm_fail_worker(rank, world, port, outdir, fail_rank):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=_PG_TIMEOUT)
     try:
         if rank == fail_rank:
             # this rank cannot see the segment (a private IPC namespace)

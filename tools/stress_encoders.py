@@ -81,7 +81,8 @@ def run(iters=2000, seed=0, oracle_every=50, verbose=True):
                 ("esub", lambda: H.elementwise_sub(a, b)),
                 ("hadamard", lambda: H.hadamard(a, b)),
                 ("encode_from_quant", lambda: H.encode_from_quant(H.decode_to_quant(a))),
-                ("from_sections", lambda: H.DeviceStream.from_sections(p, *_bytes(a))),
+                ("from_sections", lambda: H.DeviceStream.from_sections(
+                    p, a.widths, a.outliers.view(torch.uint8), *_bytes(a)[2:])),
             ]
             order = rng.permutation(len(ops))
             first, second = {}, {}
