@@ -95,6 +95,9 @@ def load(build_if_missing: bool = True):
     if _LIB is not None:
         return _LIB
     path = lib_path()
+    # HSZ_NO_BUILD=1: load exactly the given library (A/B runs of prebuilt variants)
+    if os.environ.get("HSZ_NO_BUILD") == "1":
+        build_if_missing = False
     if not os.path.exists(path) or (build_if_missing and _build.needs_build()):
         if not build_if_missing:
             raise NativeLibraryMissing(f"{path} not built; run python -m paper_2408_11971_b200.build")

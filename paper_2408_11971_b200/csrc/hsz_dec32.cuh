@@ -431,7 +431,11 @@ struct RecodeSmem {
   uint32_t agg_ts[2], agg_tp[2];
   uint64_t tile_of[2];
   uint64_t epoch;
-  uint32_t scan[4];
+  // three scan buffers: the two operands' in-tile offset scans run back to
+  // back with no barrier between the first one's reads and the second one's
+  // writes, so they must not share one (a shared buffer let a fast warp
+  // overwrite a total a slow warp had not read yet: wrong offsets)
+  uint32_t scan[4], scan_in[4], scan_in2[4];
   uint32_t wsb[4], wpb[4];
 };
 using SmulSmem = RecodeSmem<kOpSmul>;
@@ -647,7 +651,7 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
       w = 0;
     }
     uint32_t ies, iep;
-    block_offsets(w, len, S.scan, &ies, &iep);
+    block_offsets(w, len, S.scan_in, &ies, &iep);
     S.bes[tid] = ies;
     S.bep[tid] = iep;
     bool fast_in = S.in.staged && w <= static_cast<uint32_t>(kFastW) && o > -(1 << 29) && o < (1 << 29);
@@ -660,7 +664,7 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
         flags |= HSZ_ERR_BAD_WIDTH;
         w2 = 0;
       }
-      block_offsets(w2, len, S.scan, &ies2, &iep2);
+      block_offsets(w2, len, S.scan_in2, &ies2, &iep2);
       S.bes2[tid] = ies2;
       S.bep2[tid] = iep2;
       fast_in = fast_in && S.in2.staged && w2 <= static_cast<uint32_t>(kFastW) && o2 > -(1 << 29) &&
@@ -785,6 +789,320 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
 template <int kOp>
 constexpr uint32_t recode_smem_bytes() { return sizeof(RecodeSmem<kOp>) + 1024; }
 constexpr uint32_t kSmulSmemBytes = recode_smem_bytes<kOpSmul>();
+
+// ---------------------------------------------------------------------------
+// scalar_mul v3 (ops.py:199-225): 4 compute warps + 1 placement warp, 160
+// threads, 5 CTAs per SM (the stager warp of recode_kernel is gone: compute
+// warp 1 issues the bulk copies of the tile two ahead as soon as the CTA is
+// done reading a buffer).  Per tile only TWO CTA barriers, each carrying an
+// OR-reduction: (A) the in-tile offsets scan + "a block cannot take the
+// register path", (B) the output sizes scan + "a rescaled bin left the
+// register range".  Input tiles are double-buffered (the copies of tile k+2
+// land while tiles k, k+1 compute); packed payloads go through the 16 KB
+// staging ring of the compressor (hsz_enc32.cuh) to the placement warp.
+
+#ifndef HSZ_R3_PAYCAP
+#define HSZ_R3_PAYCAP 8192
+#endif
+#ifndef HSZ_R3_CTAS
+#define HSZ_R3_CTAS 5
+#endif
+constexpr uint32_t kR3PayCap = HSZ_R3_PAYCAP;
+using R3Tile = InTileT<kR3PayCap>;
+
+struct R3Smem {
+  R3Tile in[2];                                 // double-buffered input tiles
+  unsigned char ring[e32::kRingBytes];          // staged output payloads
+  alignas(16) uint32_t sgn[e32::kSlots][TB];    // staged output sign words
+  uint64_t full[2];
+  uint64_t st_full[e32::kSlots], st_empty[e32::kSlots];
+  e32::RingRec rec[e32::kSlots];
+  volatile uint64_t ring_tail;
+  uint64_t epoch;
+  uint64_t excl_s[e32::kSlots], excl_p[e32::kSlots];
+  uint32_t scan_a[4], scan_b[4];
+  uint32_t wsb[4], wpb[4];
+  uint32_t bes[TB], bep[TB];                    // in-tile input offsets (exact path)
+  uint32_t xscratch[4][64];                     // exact path: one block's packed words per warp
+};
+constexpr uint32_t kR3SmemBytes = sizeof(R3Smem) + 1024;
+
+// exclusive scan of one u32 over the 128 compute threads, fused with an OR
+// reduction of `p` in the same barrier (bar.red.or); *total = sum
+__device__ __forceinline__ uint32_t cta_scan_or(uint32_t v, uint32_t* s_scan, uint32_t* total,
+                                                bool p, bool* any) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t inc = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t o = __shfl_up_sync(kFull, inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (lane == 31) s_scan[warp] = inc;
+  *any = e32::bar_or_compute(p);
+  const uint32_t a0 = s_scan[0], a1 = s_scan[1], a2 = s_scan[2], a3 = s_scan[3];
+  const uint32_t pre = (warp > 0 ? a0 : 0u) + (warp > 1 ? a1 : 0u) + (warp > 2 ? a2 : 0u);
+  *total = a0 + a1 + a2 + a3;
+  return pre + inc - v;
+}
+
+// the exact warp-per-block source of v3 (input block decoded from global memory)
+struct SrcSmul3 {
+  StreamIn in;
+  const R3Tile* it;
+  const uint32_t* bes;
+  const uint32_t* bep;
+  int64_t rs;
+  double d;
+  __device__ __forceinline__ int64_t lane_bin(int lb, int lane, int len, uint32_t* flags) {
+    uint32_t f = 0;
+    const int64_t q = k32::decode_lane(in.signs, in.payload, it->w[lb], it->o[lb], it->gs0 + bes[lb],
+                                       it->gp0 + bep[lb], len, lane, &f);
+    *flags |= f;
+    if (f || lane >= len) return 0;
+    return rescale1(product_rn(q, rs), d, flags);
+  }
+};
+
+__global__ void __launch_bounds__(e32::kThreadsC, HSZ_R3_CTAS)
+    smul3_kernel(StreamIn in, SmulParams sp, k32::EncodeOut out) {
+  extern __shared__ unsigned char smraw[];
+  const uint32_t a0 = smem_u32(smraw);
+  R3Smem& S = *reinterpret_cast<R3Smem*>(smraw + (((a0 + 1023u) & ~1023u) - a0));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint64_t ntiles = in.ntiles, nblocks = in.nblocks;
+  LookbackWs lw = LookbackWs::bind(out.ws, ntiles);
+  const uint64_t last_draw = ntiles + gridDim.x - 1;   // every CTA draws once past the end
+  constexpr int kSlots = e32::kSlots;
+  constexpr uint32_t kRing = e32::kRingBytes;
+  if (tid == 0) {
+    mbar_init(&S.full[0], 1);
+    mbar_init(&S.full[1], 1);
+    for (int i = 0; i < kSlots; ++i) {
+      mbar_init(&S.st_full[i], kCompute / 32);
+      mbar_init(&S.st_empty[i], 1);
+    }
+    S.ring_tail = 0;
+    fence_mbar_init();
+    S.epoch = ld_acquire(lw.epoch);
+  }
+  __syncthreads();
+  const uint64_t epoch = S.epoch;
+
+  if (warp == kCompute / 32) {
+    // =========================== placement warp ===========================
+    for (uint32_t kk = 0;; ++kk) {
+      const int slot = kk % kSlots;
+      mbar_wait_parity_sleep(&S.st_full[slot], (kk / kSlots) & 1u);
+      const e32::RingRec r = S.rec[slot];
+      if (r.ts == e32::kDone) break;
+      if (r.ts != e32::kSelfPlaced) {
+        uint64_t es, ep;
+        e32::resolve6(out, r.tile, epoch, ntiles, r.ts, r.tp, &es, &ep);
+        if (es != ~0ull) e32::copy_ring(S.sgn[slot], S.ring, out, r, es, ep);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();   // the ring reads complete before the space is reused
+        S.ring_tail = r.end;
+        mbar_arrive(&S.st_empty[slot]);
+      }
+    }
+    return;
+  }
+
+  // =========================== compute warps ===========================
+  // warp 1 stages input tiles (lane 0 draws the tickets, in order, one
+  // staged tile ahead of the buffer it fills)
+  auto draw = [&]() -> uint64_t {
+    const uint64_t t = atom_add_relaxed(lw.ticket, 1);
+    if (t == last_draw) {
+      st_relaxed(lw.ticket, 0);
+      st_release(lw.epoch, epoch + 1);
+    }
+    return t;
+  };
+  uint64_t nxt = ~0ull, tv = 0;   // warp 1: the drawn, not yet staged ticket (+ its offsets)
+  if (warp == 1) {
+    uint64_t t0 = 0, t1 = ~0ull;
+    if (lane == 0) {
+      t0 = draw();
+      if (t0 < ntiles) t1 = draw();
+    }
+    t0 = __shfl_sync(kFull, t0, 0);
+    t1 = __shfl_sync(kFull, t1, 0);
+    stage_tile(in, t0, prefetch_toff(in, t0), S.in[0], &S.full[0]);
+    if (t0 < ntiles) {
+      stage_tile(in, t1, prefetch_toff(in, t1), S.in[1], &S.full[1]);
+      if (t1 < ntiles) {
+        uint64_t t2 = 0;
+        if (lane == 0) t2 = draw();
+        nxt = __shfl_sync(kFull, t2, 0);
+        tv = prefetch_toff(in, nxt);
+      }
+    }
+  }
+  // buffer b is free again: stage the next drawn ticket into it (warp 1)
+  auto restage = [&](int b) {
+    if (warp != 1 || nxt == ~0ull) return;
+    stage_tile(in, nxt, tv, S.in[b], &S.full[b]);
+    if (nxt < ntiles) {
+      uint64_t t = 0;
+      if (lane == 0) t = draw();
+      nxt = __shfl_sync(kFull, t, 0);
+      tv = prefetch_toff(in, nxt);
+    } else {
+      nxt = ~0ull;                 // the terminal ticket is staged: no more draws
+    }
+  };
+
+  uint32_t flags = 0;
+  uint64_t head = 0;   // ring bytes allocated (identical in every compute thread)
+  for (uint32_t k = 0;; ++k) {
+    const int b = k & 1;
+    const int slot = k % kSlots;
+    mbar_wait_parity(&S.full[b], (k >> 1) & 1u);
+    const R3Tile& it = S.in[b];
+    const uint64_t cur = it.tile;
+    if (cur >= ntiles) {
+      if (k >= kSlots) mbar_wait_parity(&S.st_empty[slot], ((k / kSlots) - 1) & 1u);
+      if (tid == 0) {
+        S.rec[slot].ts = e32::kDone;
+        S.rec[slot].end = head;
+      }
+      mbar_arrive_warp(&S.st_full[slot]);
+      break;
+    }
+    // ---- (A) this thread's block: in-tile offsets, register-path test ------
+    const uint64_t gb = cur * TB + tid;
+    const bool active = gb < nblocks;
+    const int len = !active ? 0 : (gb == nblocks - 1 ? static_cast<int>(in.tail_len) : K);
+    uint32_t w = it.w[tid];
+    const int32_t o = it.o[tid];
+    if (w > 64) {
+      flags |= HSZ_ERR_BAD_WIDTH;
+      w = 0;
+    }
+    const uint32_t isb = w ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
+    const uint32_t ipb = (static_cast<uint32_t>(len) * w + 7u) >> 3;
+    const bool slow_in = !(it.staged && w <= static_cast<uint32_t>(kFastW) && o > -(1 << 29) &&
+                           o < (1 << 29));
+    uint32_t itot;
+    bool slow;
+    const uint32_t iex = cta_scan_or(isb | (ipb << 10), S.scan_a, &itot, slow_in, &slow);
+    const uint32_t ies = iex & 1023u, iep = iex >> 10;
+    S.bes[tid] = ies;
+    S.bep[tid] = iep;
+    bool exact = slow || !sp.small_rs;            // CTA-uniform
+    uint32_t ts = 0, tp = 0;
+    if (!exact) {
+      // ---- decode, exact rescale (ops.py:199-208), code ---------------------
+      uint32_t qb[K];
+      bool ovf = false;
+      {
+        int32_t q[K];
+        decode_block<0, false>(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, o, len, q);
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          // bin * rs in one FMA from the biased bin (2^52 + 2^31 + bin): the
+          // exact product-sum is bin * rs (< 2^53), so the rounding is exact
+          const double pd = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(
+                                         static_cast<uint32_t>(q[i]) ^ 0x80000000u)),
+                                     sp.rsd, sp.negc);
+          const double tt = __dmul_rn(sp.d, pd);
+          // floor(RN(|t| + 1/2)) by one DADD rounding toward -inf against 2^52
+          const uint32_t mi = static_cast<uint32_t>(
+              __double2loint(__dadd_rd(__dadd_rn(fabs(tt), 0.5), 4503599627370496.0)));
+          ovf |= mi >= 1073741823u;
+          qb[i] = tt < 0.0 ? 0u - mi : mi;
+        }
+      }
+      e32::BlockCode bc;
+      e32::block_code(qb, len, bc);
+      const uint32_t wmax = __reduce_max_sync(kFull, bc.w);
+      const uint32_t sb = (bc.w && active) ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
+      const uint32_t pb = (static_cast<uint32_t>(len) * bc.w + 7u) >> 3;
+      uint32_t tot;
+      // ---- (B) output sizes scan + overflow test; every read of S.in[b] done
+      const uint32_t ex = cta_scan_or(sb | (pb << 10), S.scan_b, &tot, ovf, &exact);
+      if (!exact) {
+        restage(b);                                 // tile k+2's copies fly during the pack
+        const uint32_t es = ex & 1023u, ep = ex >> 10;
+        ts = tot & 1023u;
+        tp = tot >> 10;
+        if (tid == 0) lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
+        if (active) {
+          out.widths[gb] = static_cast<uint8_t>(bc.w);
+          out.outliers[gb] = static_cast<int32_t>(qb[0]);
+        }
+        if (k >= kSlots) mbar_wait_parity(&S.st_empty[slot], ((k / kSlots) - 1) & 1u);
+        const uint32_t need = (tp + 127u) & ~127u;
+        uint32_t pos = static_cast<uint32_t>(head % kRing);
+        if (pos + need > kRing) {   // no wrap inside a tile: skip to the ring start
+          head += kRing - pos;
+          pos = 0;
+        }
+        if (head + need - S.ring_tail > kRing) {
+          unsigned ns = 32;
+          while (head + need - S.ring_tail > kRing) {
+            __nanosleep(ns);
+            ns = ns < 256 ? ns * 2 : 256;
+          }
+        }
+        head += need;
+        if (tid == 0) {
+          S.rec[slot].tile = cur;
+          S.rec[slot].end = head;
+          S.rec[slot].ts = ts;
+          S.rec[slot].tp = tp;
+          S.rec[slot].off = pos;
+        }
+        if (sb) S.sgn[slot][es >> 2] = bswap32(bc.sg);
+        e32::pack_block(bc, wmax, ep >> 2, reinterpret_cast<uint32_t*>(S.ring + pos));
+        mbar_arrive_warp(&S.st_full[slot]);
+        continue;
+      }
+    }
+    // ---- exact warp-per-block path: decodes from global memory, places itself
+    {
+      SrcSmul3 src{in, &it, S.bes, S.bep, sp.rs, sp.d};
+      e32::bar_sync_n(1, kCompute);                // S.bes / S.bep of every block visible
+      flags |= k32::fallback_sizes(src, out, cur, nblocks, in.tail_len, S.wsb, S.wpb);
+      e32::bar_sync_n(1, kCompute);
+      ts = S.wsb[0] + S.wsb[1] + S.wsb[2] + S.wsb[3];
+      tp = S.wpb[0] + S.wpb[1] + S.wpb[2] + S.wpb[3];
+      if (tid == 0) lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
+      if (k >= kSlots) mbar_wait_parity(&S.st_empty[slot], ((k / kSlots) - 1) & 1u);
+      if (tid == 0) {
+        S.rec[slot].tile = cur;
+        S.rec[slot].end = head;
+        S.rec[slot].ts = e32::kSelfPlaced;
+      }
+      mbar_arrive_warp(&S.st_full[slot]);
+      if (warp == 0) {
+        uint64_t es, ep;
+        e32::resolve6(out, cur, epoch, ntiles, ts, tp, &es, &ep);
+        if (lane == 0) {
+          S.excl_s[slot] = es;
+          S.excl_p[slot] = ep;
+        }
+      }
+      e32::bar_sync_n(1, kCompute);
+      if (S.excl_s[slot] != ~0ull) {
+        uint64_t gs = S.excl_s[slot], gp = S.excl_p[slot];
+        for (int i = 0; i < warp; ++i) {
+          gs += S.wsb[i];
+          gp += S.wpb[i];
+        }
+        k32::fallback_pack(src, out, cur, nblocks, in.tail_len, gs, gp, S.xscratch[warp]);
+      }
+      e32::bar_sync_n(1, kCompute);                // every read of S.in[b] done
+      restage(b);
+    }
+  }
+  flags = __reduce_or_sync(kFull, flags);
+  if (lane == 0 && flags) atomicOr(out.err, flags);
+}
 
 // ---------------------------------------------------------------------------
 // Decode pipeline (moments, decompress to float32): persistent CTAs of 4
