@@ -893,7 +893,7 @@ __global__ void __launch_bounds__(e32::kThreadsC, HSZ_R3_CTAS)
     // =========================== placement warp ===========================
     for (uint32_t kk = 0;; ++kk) {
       const int slot = kk % kSlots;
-      mbar_wait_parity_sleep(&S.st_full[slot], (kk / kSlots) & 1u);
+      e32::slot_wait(&S.st_full[slot], slot, (kk / kSlots) & 1u);
       const e32::RingRec r = S.rec[slot];
       if (r.ts == e32::kDone) break;
       if (r.ts != e32::kSelfPlaced) {
@@ -922,22 +922,26 @@ __global__ void __launch_bounds__(e32::kThreadsC, HSZ_R3_CTAS)
     }
     return t;
   };
-  uint64_t nxt = ~0ull, tv = 0;   // warp 1: the drawn, not yet staged ticket (+ its offsets)
+  // warp 1: `nxt` = the next ticket to stage (its tile offsets prefetched in
+  // `tv`), `ahead` (lane 0) = the ticket after it, drawn one restage early so
+  // the atomic's latency never stalls the warp
+  uint64_t nxt = ~0ull, tv = 0, ahead = ~0ull;
   if (warp == 1) {
-    uint64_t t0 = 0, t1 = ~0ull;
+    uint64_t t0 = 0, t1 = ~0ull, t2 = ~0ull;
     if (lane == 0) {
       t0 = draw();
       if (t0 < ntiles) t1 = draw();
+      if (t1 < ntiles) t2 = draw();
+      if (t2 < ntiles) ahead = draw();
     }
     t0 = __shfl_sync(kFull, t0, 0);
     t1 = __shfl_sync(kFull, t1, 0);
+    t2 = __shfl_sync(kFull, t2, 0);
     stage_tile(in, t0, prefetch_toff(in, t0), S.in[0], &S.full[0]);
     if (t0 < ntiles) {
       stage_tile(in, t1, prefetch_toff(in, t1), S.in[1], &S.full[1]);
       if (t1 < ntiles) {
-        uint64_t t2 = 0;
-        if (lane == 0) t2 = draw();
-        nxt = __shfl_sync(kFull, t2, 0);
+        nxt = t2;
         tv = prefetch_toff(in, nxt);
       }
     }
@@ -947,10 +951,9 @@ __global__ void __launch_bounds__(e32::kThreadsC, HSZ_R3_CTAS)
     if (warp != 1 || nxt == ~0ull) return;
     stage_tile(in, nxt, tv, S.in[b], &S.full[b]);
     if (nxt < ntiles) {
-      uint64_t t = 0;
-      if (lane == 0) t = draw();
-      nxt = __shfl_sync(kFull, t, 0);
+      nxt = __shfl_sync(kFull, ahead, 0);        // drawn one restage ago
       tv = prefetch_toff(in, nxt);
+      if (lane == 0 && nxt < ntiles) ahead = draw();
     } else {
       nxt = ~0ull;                 // the terminal ticket is staged: no more draws
     }
@@ -970,7 +973,7 @@ __global__ void __launch_bounds__(e32::kThreadsC, HSZ_R3_CTAS)
         S.rec[slot].ts = e32::kDone;
         S.rec[slot].end = head;
       }
-      mbar_arrive_warp(&S.st_full[slot]);
+      e32::slot_staged(&S.st_full[slot], slot);
       break;
     }
     // ---- (A) this thread's block: in-tile offsets, register-path test ------
@@ -1059,7 +1062,7 @@ __global__ void __launch_bounds__(e32::kThreadsC, HSZ_R3_CTAS)
         }
         if (sb) S.sgn[slot][es >> 2] = bswap32(bc.sg);
         e32::pack_block(bc, wmax, ep >> 2, reinterpret_cast<uint32_t*>(S.ring + pos));
-        mbar_arrive_warp(&S.st_full[slot]);
+        e32::slot_staged(&S.st_full[slot], slot);
         continue;
       }
     }
@@ -1078,7 +1081,7 @@ __global__ void __launch_bounds__(e32::kThreadsC, HSZ_R3_CTAS)
         S.rec[slot].end = head;
         S.rec[slot].ts = e32::kSelfPlaced;
       }
-      mbar_arrive_warp(&S.st_full[slot]);
+      e32::slot_staged(&S.st_full[slot], slot);
       if (warp == 0) {
         uint64_t es, ep;
         e32::resolve6(out, cur, epoch, ntiles, ts, tp, &es, &ep);
@@ -1136,6 +1139,55 @@ struct DecSmem {
 template <int kMode>
 constexpr uint32_t dec_smem_bytes() { return sizeof(DecSmem<kMode>) + 1024; }
 constexpr int kDecThreads = kCompute + 32;
+
+// Hand-offs between the TMA warp and the compute warps (HSZ_DEC_NAMED): the
+// TMA warp alone waits for a tile's bytes (mbarrier complete_tx), then
+// releases the compute warps through a NAMED barrier -- they block in
+// hardware instead of polling an mbarrier (the polls were ~12% of the
+// moment kernels' issued instructions).  Both hand-offs strictly alternate
+// per buffer (a buffer is restaged only after its release), which is what a
+// named barrier needs.  Barrier ids: 1 = the compute group, 2-3 full[b],
+// 4-5 empty[b].
+#ifndef HSZ_DEC_NAMED
+#define HSZ_DEC_NAMED 1
+#endif
+constexpr int kBarFull = 2, kBarEmpty = 4;
+
+// named barrier ops with IMMEDIATE ids (a register id makes ptxas reserve all
+// 16 barriers of the CTA)
+template <int kId>
+__device__ __forceinline__ void nbar_sync() {
+  asm volatile("bar.sync %0, %1;" ::"n"(kId), "n"(kDecThreads) : "memory");
+}
+template <int kId>
+__device__ __forceinline__ void nbar_arrive() {
+  asm volatile("bar.arrive %0, %1;" ::"n"(kId), "n"(kDecThreads) : "memory");
+}
+__device__ __forceinline__ void nbar_sync2(int base, int b) {   // base + b, b in {0, 1}
+  if (base == kBarFull) {
+    if (b) nbar_sync<kBarFull + 1>(); else nbar_sync<kBarFull>();
+  } else {
+    if (b) nbar_sync<kBarEmpty + 1>(); else nbar_sync<kBarEmpty>();
+  }
+}
+__device__ __forceinline__ void nbar_arrive2(int base, int b) {
+  if (base == kBarFull) {
+    if (b) nbar_arrive<kBarFull + 1>(); else nbar_arrive<kBarFull>();
+  } else {
+    if (b) nbar_arrive<kBarEmpty + 1>(); else nbar_arrive<kBarEmpty>();
+  }
+}
+
+__device__ __forceinline__ void dec_release(uint64_t* empty_bar, int b) {
+#if HSZ_DEC_NAMED
+  (void)empty_bar;
+  __syncwarp();
+  nbar_arrive2(kBarEmpty, b);
+#else
+  (void)b;
+  mbar_arrive_warp(empty_bar);
+#endif
+}
 
 // the 32-lane exact decode of one tile's blocks (any width up to 64, any
 // outlier), reading the sections in place; calls f(local block, lane, bin,
@@ -1256,9 +1308,22 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
     for (uint64_t t = blockIdx.x;; t += gridDim.x, ++i) {
       const int b = i & 1;
       const uint64_t tvn = prefetch_toff(in, t + gridDim.x);   // consumed next iteration
+#if HSZ_DEC_NAMED
+      if (i >= 2) nbar_sync2(kBarEmpty, b);                    // compute done with tile i-2
+      stage_tile(in, t, tv, S.in[b], &S.full[b]);
+      mbar_wait_parity(&S.full[b], (i >> 1) & 1u);             // the bytes landed
+      nbar_arrive2(kBarFull, b);
+      if (t >= ntiles) {
+        // consume the compute warps' release of the last real tile, so no
+        // named barrier is left with pending arrivals
+        if (i >= 1) nbar_sync2(kBarEmpty, b ^ 1);
+        break;
+      }
+#else
       if (i >= 2) mbar_wait_parity_sleep(&S.empty[b], ((i >> 1) - 1) & 1u);
       stage_tile(in, t, tv, S.in[b], &S.full[b]);
       if (t >= ntiles) break;
+#endif
       tv = tvn;
     }
     return;
@@ -1272,7 +1337,11 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
   uint32_t i = 0;
   for (;; ++i) {
     const int b = i & 1;
+#if HSZ_DEC_NAMED
+    nbar_sync2(kBarFull, b);                      // blocks without issuing (no polling)
+#else
     mbar_wait_parity(&S.full[b], (i >> 1) & 1u);
+#endif
     const auto& it = S.in[b];
     const uint64_t cur = it.tile;
     if (cur >= ntiles) break;
@@ -1301,7 +1370,7 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
       int64_t sp;
       uint64_t sp2;
       decode_sum<kMode == 1>(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, len, &sp, &sp2);
-      mbar_arrive_warp(&S.empty[b]);          // staged bytes consumed
+      dec_release(&S.empty[b], b);          // staged bytes consumed
       if (len > 0) {
         const __int128 oo = o;
         acc.s += oo * len + sp;
@@ -1315,11 +1384,11 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
     } else if (fast && HSZ_F32_STREAM) {
       decode_f32(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, o, len, fs.d, S.out + tid * 128,
                  static_cast<uint32_t>(tid & 7), fs.may_overflow, &flags);
-      mbar_arrive_warp(&S.empty[b]);          // staged bytes consumed
+      dec_release(&S.empty[b], b);          // staged bytes consumed
     } else if (fast) {
       int32_t q[K];
       decode_block(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, o, len, q);
-      mbar_arrive_warp(&S.empty[b]);          // staged bytes consumed
+      dec_release(&S.empty[b], b);          // staged bytes consumed
       if (kMode == 2) {
         // f32 values = RN32(RN64(2eps * bin)) (codec.py:107-115), into the
         // swizzled 128-byte row of this block
@@ -1381,7 +1450,7 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
           if (live) acc.add(q, kMode == 1);
         });
       }
-      mbar_arrive_warp(&S.empty[b]);
+      dec_release(&S.empty[b], b);
     }
     if (kMode == 2) {
       // one TMA tensor store of the whole tile (the stream's partial last
