@@ -260,6 +260,67 @@ def global_variance(z, coll, n_global):
     return ops.variance_from(S, Q, n_global, z.params.eps)
 
 
+_MIX_A, _MIX_B, _MIX_C = -7046029254386353131, 6364136223846793005, 1442695040888963407
+
+
+def _digest(t, off0):
+    """Position-weighted checksum of a device tensor's BYTES whose first byte
+    sits at global byte offset `off0` of its section: sum_i byte_i * c(off0 + i)
+    mod 2^64, c a 64-bit mix of the position.  Shards' digests of the same
+    section ADD UP to the whole stream's digest, so the C2-assembled stream
+    of N ranks can be compared with the single-GPU stream without gathering
+    it (bench.py --digest; tests/test_gpu_bench_sharded.py)."""
+    import torch
+
+    u = t.reshape(-1).view(torch.uint8)
+    total = torch.zeros((), dtype=torch.int64, device=u.device)
+    step = 1 << 26
+    for a in range(0, u.numel(), step):
+        v = u[a:a + step].to(torch.int64)
+        i = torch.arange(off0 + a, off0 + a + v.numel(), dtype=torch.int64, device=u.device)
+        c = (i * _MIX_A) ^ (i >> 17)
+        c = c * _MIX_B + _MIX_C
+        total += (v * c).sum()
+        del v, i, c
+    return int(total.item()) & ((1 << 64) - 1)
+
+
+def stream_digests(ds, lay, block0):
+    """Digests of the four sections of this rank's shard of a stream at its
+    global offsets (C2 layout `lay`; None at N = 1)."""
+    sb, pb = ds.totals()
+    so = lay.sign_offset if lay is not None else 0
+    po = lay.payload_offset if lay is not None else 0
+    return [_digest(ds.widths, block0), _digest(ds.outliers, 4 * block0),
+            _digest(ds.signs[:sb], so), _digest(ds.payload[:pb], po)]
+
+
+def chain_digests(H, chain, x, coll):
+    """One untimed chain step, then digests of the compressed stream, the
+    chained stream and the decompressed values over the WHOLE field (summed
+    over ranks), with eps and mean / variance as float hex -- identical for
+    any rank count when the sharded path is right."""
+    z, out, mean, var = chain.run(x)
+    raw = H.RawArray(x, chain.dims, "f32")
+    lo, hi = raw.value_range()
+    if coll is not None:
+        lo, hi = coll.global_range(lo, hi)
+    eps = float(chain.cfg["rel_eps"]) * (hi - lo)
+    s = H.compress(raw, H.QuantParams(eps, chain.dims, 32, "f32"))
+    b0 = chain.block0
+    ls = lz = None
+    if coll is not None:
+        ls, lz = coll.global_offsets_many(b0, [s.totals(), z.totals()])
+    vals = [_digest(out.values, 4 * 32 * b0)] + stream_digests(s, ls, b0) + stream_digests(z, lz, b0)
+    if coll is not None:
+        rows = coll._allgather_i64([v - (1 << 64) if v >= (1 << 63) else v for v in vals])
+        vals = [sum(int(r[j]) & ((1 << 64) - 1) for r in rows) & ((1 << 64) - 1)
+                for j in range(len(vals))]
+    hx = [f"{v:016x}" for v in vals]
+    return {"eps": float(eps).hex(), "mean": float(mean).hex(), "variance": float(var).hex(),
+            "decompress": hx[0], "compress": hx[1:5], "chain": hx[5:9]}
+
+
 def _algorithmic_bytes(H, chain, x):
     """Per-op algorithmic bytes of this rank's shard, from
     device-side section totals (no host copy of the streams)."""
@@ -394,7 +455,7 @@ def measure(args, config, world, rank, local, coll, light=False):
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
     steps = args.steps if not light else max(3, min(args.steps, 5))
-    for _ in range(max(args.warmup, 3) if not light else 2):
+    for _ in range(max(args.warmup, 3) if not (light or args.quick) else max(1, min(args.warmup, 2))):
         chain.run(x)
     torch.cuda.synchronize()
 
@@ -467,7 +528,9 @@ def measure(args, config, world, rank, local, coll, light=False):
         "ops_in_chain_ms": {op: round(statistics.median(per_op[op]), 4) for op in OPS},
         "gpu_launches": 8 * steps,
     }
-    if light:
+    if args.digest or args.quick:
+        line["digests"] = chain_digests(H, chain, x, coll)
+    if light or args.quick:
         del x, flush
         return line
 
@@ -530,10 +593,10 @@ def run_b200(args):
     sampler.start()                       # samples cover warm-up, timed steps and kernel timing
     line = measure(args, config, world, rank, local, coll)
     line["clocks"] = sampler.stop()
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and config != 5:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and config != 5 and not args.quick:
         line["cpu_baseline"] = _cpu_baseline(host_field(config), W_cfg(config),
                                              budget_s=args.cpu_budget)
-    if world == 1 and config == 4 and not args.no_scale_baseline:
+    if world == 1 and config == 4 and not args.no_scale_baseline and not args.quick:
         # the north_star scaling config on ONE GPU: the baseline of the N > 1 lines
         import gc
 
@@ -830,6 +893,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-scale-baseline", action="store_true",
                     help="skip the config-5 chain on one GPU (config5_n1) at N = 1")
+    ap.add_argument("--quick", action="store_true",
+                    help="functional run: chain timing + digests only (no kernel timing, e2e, "
+                         "CPU baseline or config-5 scaling baseline)")
+    ap.add_argument("--digest", action="store_true",
+                    help="add digests of the whole-field streams / values (sharding check)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=150.0,
                     help="seconds of CPU work for the whole --impl reference run")

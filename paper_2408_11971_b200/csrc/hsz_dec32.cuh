@@ -791,65 +791,57 @@ constexpr uint32_t recode_smem_bytes() { return sizeof(RecodeSmem<kOp>) + 1024; 
 constexpr uint32_t kSmulSmemBytes = recode_smem_bytes<kOpSmul>();
 
 // ---------------------------------------------------------------------------
-// scalar_mul v3 (ops.py:199-225): 4 compute warps + 1 placement warp, 160
-// threads, 5 CTAs per SM (the stager warp of recode_kernel is gone: compute
-// warp 1 issues the bulk copies of the tile two ahead as soon as the CTA is
-// done reading a buffer).  Per tile only TWO CTA barriers, each carrying an
-// OR-reduction: (A) the in-tile offsets scan + "a block cannot take the
-// register path", (B) the output sizes scan + "a rescaled bin left the
-// register range".  Input tiles are double-buffered (the copies of tile k+2
-// land while tiles k, k+1 compute); packed payloads go through the 16 KB
-// staging ring of the compressor (hsz_enc32.cuh) to the placement warp.
+// scalar_mul v4 (ops.py:199-225): barrier-free compute warps.
+//
+// recode_kernel keeps the 4 compute warps of a CTA in lockstep (four CTA
+// barriers per tile) and single-buffers the input; ncu on config 4 shows the
+// compute warps spending about half their time waiting there (barrier stalls
+// and the loop-top wait for the next tile).  Here every compute warp owns
+// blocks [32q, 32q + 32) of each tile and never waits for another warp:
+//   * in-tile input offsets: a warp scan plus the sizes of the preceding
+//     warps' blocks, recomputed from their widths (no CTA scan);
+//   * the register-path / exact decision is per warp;
+//   * output: the warp packs its segment into its own staging region of the
+//     tile's slot; the LAST warp to report its segment sizes (one 64-bit
+//     shared atomic) publishes the tile aggregate for the look-back;
+//   * input tiles are double-buffered; the stager restages a buffer once all
+//     four warps released it, so warps drift apart by up to a tile.
+// The placement warp resolves each tile (decoupled look-back over whole
+// 128-block tiles, so the tile-offset cache is unchanged) and copies the four
+// segments out.  A warp that needs the exact (64/128-bit) path reports its
+// segment sizes, waits for the tile's resolution and writes its blocks to
+// global memory itself.
 
-#ifndef HSZ_R3_PAYCAP
-#define HSZ_R3_PAYCAP 8192
+#ifndef HSZ_S4_PAYCAP
+#define HSZ_S4_PAYCAP 8192
 #endif
-#ifndef HSZ_R3_CTAS
-#define HSZ_R3_CTAS 5
-#endif
-constexpr uint32_t kR3PayCap = HSZ_R3_PAYCAP;
-using R3Tile = InTileT<kR3PayCap>;
+constexpr uint32_t kS4PayCap = HSZ_S4_PAYCAP;
+using S4Tile = InTileT<kS4PayCap>;
+constexpr uint32_t kSegCap = 4096;              // a warp's packed payload: 32 blocks, w <= 31
+constexpr uint64_t kAggCnt = 1ull << 56;        // aggregate word: count | sign bytes << 28 | payload
 
-struct R3Smem {
-  R3Tile in[2];                                 // double-buffered input tiles
-  unsigned char ring[e32::kRingBytes];          // staged output payloads
-  alignas(16) uint32_t sgn[e32::kSlots][TB];    // staged output sign words
-  uint64_t full[2];
-  uint64_t st_full[e32::kSlots], st_empty[e32::kSlots];
-  e32::RingRec rec[e32::kSlots];
-  volatile uint64_t ring_tail;
+struct S4Smem {
+  S4Tile in[2];                                 // double-buffered input tiles
+  alignas(16) unsigned char pay[2][4][kSegCap];  // per slot, per warp: packed payload
+  alignas(16) uint32_t sgn[2][4][32];           // per slot, per warp: sign words
+  uint32_t seg_s[2][4], seg_p[2][4];            // per slot, per warp: segment sizes
+  uint32_t seg_x[2];                            // bit q: warp q places itself (exact path)
+  unsigned long long agg[2];                    // per slot: reported segments (count, sums)
+  uint64_t tile_of[2];
+  uint64_t xs[2][4], xp[2][4];                  // resolved offsets of self-placing warps
+  volatile uint64_t res_tile[2];                // the tile whose xs/xp are valid
+  uint64_t full[2], in_empty[2], st_full[2], st_empty[2];
   uint64_t epoch;
-  uint64_t excl_s[e32::kSlots], excl_p[e32::kSlots];
-  uint32_t scan_a[4], scan_b[4];
-  uint32_t wsb[4], wpb[4];
   uint32_t bes[TB], bep[TB];                    // in-tile input offsets (exact path)
   uint32_t xscratch[4][64];                     // exact path: one block's packed words per warp
 };
-constexpr uint32_t kR3SmemBytes = sizeof(R3Smem) + 1024;
+constexpr uint32_t kS4SmemBytes = sizeof(S4Smem) + 1024;
+constexpr int kS4Threads = kCompute + 64;       // 4 compute warps + stager + placement
 
-// exclusive scan of one u32 over the 128 compute threads, fused with an OR
-// reduction of `p` in the same barrier (bar.red.or); *total = sum
-__device__ __forceinline__ uint32_t cta_scan_or(uint32_t v, uint32_t* s_scan, uint32_t* total,
-                                                bool p, bool* any) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t inc = v;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t o = __shfl_up_sync(kFull, inc, d);
-    if (lane >= d) inc += o;
-  }
-  if (lane == 31) s_scan[warp] = inc;
-  *any = e32::bar_or_compute(p);
-  const uint32_t a0 = s_scan[0], a1 = s_scan[1], a2 = s_scan[2], a3 = s_scan[3];
-  const uint32_t pre = (warp > 0 ? a0 : 0u) + (warp > 1 ? a1 : 0u) + (warp > 2 ? a2 : 0u);
-  *total = a0 + a1 + a2 + a3;
-  return pre + inc - v;
-}
-
-// the exact warp-per-block source of v3 (input block decoded from global memory)
-struct SrcSmul3 {
+// the exact warp-per-block source of v4 (input block decoded from global memory)
+struct SrcSmul4 {
   StreamIn in;
-  const R3Tile* it;
+  const S4Tile* it;
   const uint32_t* bes;
   const uint32_t* bep;
   int64_t rs;
@@ -864,25 +856,49 @@ struct SrcSmul3 {
   }
 };
 
-__global__ void __launch_bounds__(e32::kThreadsC, HSZ_R3_CTAS)
-    smul3_kernel(StreamIn in, SmulParams sp, k32::EncodeOut out) {
+// placement warp: copy one warp segment (sign words + payload) to its offsets
+__device__ __forceinline__ void copy_segment(const uint32_t* sgn, const unsigned char* pay,
+                                             const k32::EncodeOut& out, uint32_t ts, uint32_t tp,
+                                             uint64_t es, uint64_t ep) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t* dsg = reinterpret_cast<uint32_t*>(out.signs + es);
+  if (lane < ((ts + 3u) >> 2)) dsg[lane] = sgn[lane];
+  const uint32_t* pbuf = reinterpret_cast<const uint32_t*>(pay);
+  uint32_t* dst = reinterpret_cast<uint32_t*>(out.payload + ep);
+  const uint32_t nw = (tp + 3u) >> 2;
+  uint32_t head = static_cast<uint32_t>(((16u - (ep & 15u)) & 15u) >> 2);
+  head = head < nw ? head : nw;
+  if (lane < head) dst[lane] = pbuf[e32::swz_word(lane)];
+  const uint32_t nv = (nw - head) >> 2;
+  uint4* dv = reinterpret_cast<uint4*>(dst + head);
+  for (uint32_t i = lane; i < nv; i += 32) {
+    const uint32_t k = head + 4u * i;
+    dv[i] = make_uint4(pbuf[e32::swz_word(k)], pbuf[e32::swz_word(k + 1)],
+                       pbuf[e32::swz_word(k + 2)], pbuf[e32::swz_word(k + 3)]);
+  }
+  const uint32_t rest = head + 4u * nv + lane;
+  if (rest < nw) dst[rest] = pbuf[e32::swz_word(rest)];
+}
+
+__global__ void __launch_bounds__(kS4Threads, HSZ_ENC_CTAS)
+    smul4_kernel(StreamIn in, SmulParams sp, k32::EncodeOut out) {
   extern __shared__ unsigned char smraw[];
   const uint32_t a0 = smem_u32(smraw);
-  R3Smem& S = *reinterpret_cast<R3Smem*>(smraw + (((a0 + 1023u) & ~1023u) - a0));
+  S4Smem& S = *reinterpret_cast<S4Smem*>(smraw + (((a0 + 1023u) & ~1023u) - a0));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t ntiles = in.ntiles, nblocks = in.nblocks;
   LookbackWs lw = LookbackWs::bind(out.ws, ntiles);
   const uint64_t last_draw = ntiles + gridDim.x - 1;   // every CTA draws once past the end
-  constexpr int kSlots = e32::kSlots;
-  constexpr uint32_t kRing = e32::kRingBytes;
   if (tid == 0) {
-    mbar_init(&S.full[0], 1);
-    mbar_init(&S.full[1], 1);
-    for (int i = 0; i < kSlots; ++i) {
-      mbar_init(&S.st_full[i], kCompute / 32);
-      mbar_init(&S.st_empty[i], 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&S.full[b], 1);
+      mbar_init(&S.in_empty[b], kCompute / 32);
+      mbar_init(&S.st_full[b], kCompute / 32);
+      mbar_init(&S.st_empty[b], 1);
+      S.agg[b] = 0;
+      S.seg_x[b] = 0;
+      S.res_tile[b] = ~0ull;
     }
-    S.ring_tail = 0;
     fence_mbar_init();
     S.epoch = ld_acquire(lw.epoch);
   }
@@ -890,218 +906,228 @@ __global__ void __launch_bounds__(e32::kThreadsC, HSZ_R3_CTAS)
   const uint64_t epoch = S.epoch;
 
   if (warp == kCompute / 32) {
+    // ============================ stager warp ==============================
+    auto draw = [&]() -> uint64_t {
+      const uint64_t t = atom_add_relaxed(lw.ticket, 1);
+      if (t == last_draw) {
+        st_relaxed(lw.ticket, 0);
+        st_release(lw.epoch, epoch + 1);
+      }
+      return t;
+    };
+    uint64_t t = 0, ahead = ~0ull;
+    if (lane == 0) {
+      t = draw();
+      if (t < ntiles) ahead = draw();
+    }
+    t = __shfl_sync(kFull, t, 0);
+    uint64_t tv = prefetch_toff(in, t);
+    for (uint32_t i = 0;; ++i) {
+      const int b = i & 1;
+      if (i >= 2) mbar_wait_parity_sleep(&S.in_empty[b], ((i >> 1) - 1) & 1u);
+      stage_tile(in, t, tv, S.in[b], &S.full[b]);
+      if (t >= ntiles) break;
+      t = __shfl_sync(kFull, ahead, 0);            // drawn one tile ago
+      tv = prefetch_toff(in, t);
+      if (lane == 0 && t < ntiles) ahead = draw();
+    }
+    return;
+  }
+
+  if (warp == kCompute / 32 + 1) {
     // =========================== placement warp ===========================
     for (uint32_t kk = 0;; ++kk) {
-      const int slot = kk % kSlots;
-      e32::slot_wait(&S.st_full[slot], slot, (kk / kSlots) & 1u);
-      const e32::RingRec r = S.rec[slot];
-      if (r.ts == e32::kDone) break;
-      if (r.ts != e32::kSelfPlaced) {
-        uint64_t es, ep;
-        e32::resolve6(out, r.tile, epoch, ntiles, r.ts, r.tp, &es, &ep);
-        if (es != ~0ull) e32::copy_ring(S.sgn[slot], S.ring, out, r, es, ep);
+      const int p = kk & 1;
+      mbar_wait_parity_sleep(&S.st_full[p], (kk >> 1) & 1u);
+      const uint64_t cur = S.tile_of[p];
+      if (cur >= ntiles) break;
+      uint32_t ss[4], pp[4];
+      uint32_t ts = 0, tp = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        ss[q] = S.seg_s[p][q];
+        pp[q] = S.seg_p[p][q];
+        ts += ss[q];
+        tp += pp[q];
+      }
+      uint64_t es, ep;
+      lb_resolve(lb_words(out.ws), cur, epoch, ts, tp, &es, &ep, out.err);
+      const bool fits = es + ts <= out.sign_cap && ep + tp <= out.payload_cap;
+      if (lane == 0) {
+        out.toff[2 * cur] = es;
+        out.toff[2 * cur + 1] = ep;
+        if (cur == ntiles - 1) {
+          out.toff[2 * ntiles] = es + ts;
+          out.toff[2 * ntiles + 1] = ep + tp;
+        }
+        if (!fits) atomicOr(out.err, HSZ_ERR_CAPACITY);
+      }
+      const uint32_t xmask = S.seg_x[p];
+      uint64_t os = es, op = ep;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if ((xmask >> q) & 1u) {
+          if (lane == 0) {
+            S.xs[p][q] = fits ? os : ~0ull;
+            S.xp[p][q] = op;
+          }
+        } else if (fits) {
+          copy_segment(S.sgn[p][q], S.pay[p][q], out, ss[q], pp[q], os, op);
+        }
+        os += ss[q];
+        op += pp[q];
       }
       __syncwarp();
       if (lane == 0) {
-        __threadfence_block();   // the ring reads complete before the space is reused
-        S.ring_tail = r.end;
-        mbar_arrive(&S.st_empty[slot]);
+        if (xmask) {
+          __threadfence_block();
+          S.res_tile[p] = cur;              // self-placing warps may write now
+        }
+        S.seg_x[p] = 0;
+        __threadfence_block();              // the slot's reads complete before it is reused
+        mbar_arrive(&S.st_empty[p]);
       }
     }
     return;
   }
 
   // =========================== compute warps ===========================
-  // warp 1 stages input tiles (lane 0 draws the tickets, in order, one
-  // staged tile ahead of the buffer it fills)
-  auto draw = [&]() -> uint64_t {
-    const uint64_t t = atom_add_relaxed(lw.ticket, 1);
-    if (t == last_draw) {
-      st_relaxed(lw.ticket, 0);
-      st_release(lw.epoch, epoch + 1);
-    }
-    return t;
-  };
-  // warp 1: `nxt` = the next ticket to stage (its tile offsets prefetched in
-  // `tv`), `ahead` (lane 0) = the ticket after it, drawn one restage early so
-  // the atomic's latency never stalls the warp
-  uint64_t nxt = ~0ull, tv = 0, ahead = ~0ull;
-  if (warp == 1) {
-    uint64_t t0 = 0, t1 = ~0ull, t2 = ~0ull;
-    if (lane == 0) {
-      t0 = draw();
-      if (t0 < ntiles) t1 = draw();
-      if (t1 < ntiles) t2 = draw();
-      if (t2 < ntiles) ahead = draw();
-    }
-    t0 = __shfl_sync(kFull, t0, 0);
-    t1 = __shfl_sync(kFull, t1, 0);
-    t2 = __shfl_sync(kFull, t2, 0);
-    stage_tile(in, t0, prefetch_toff(in, t0), S.in[0], &S.full[0]);
-    if (t0 < ntiles) {
-      stage_tile(in, t1, prefetch_toff(in, t1), S.in[1], &S.full[1]);
-      if (t1 < ntiles) {
-        nxt = t2;
-        tv = prefetch_toff(in, nxt);
-      }
-    }
-  }
-  // buffer b is free again: stage the next drawn ticket into it (warp 1)
-  auto restage = [&](int b) {
-    if (warp != 1 || nxt == ~0ull) return;
-    stage_tile(in, nxt, tv, S.in[b], &S.full[b]);
-    if (nxt < ntiles) {
-      nxt = __shfl_sync(kFull, ahead, 0);        // drawn one restage ago
-      tv = prefetch_toff(in, nxt);
-      if (lane == 0 && nxt < ntiles) ahead = draw();
-    } else {
-      nxt = ~0ull;                 // the terminal ticket is staged: no more draws
-    }
-  };
-
   uint32_t flags = 0;
-  uint64_t head = 0;   // ring bytes allocated (identical in every compute thread)
   for (uint32_t k = 0;; ++k) {
-    const int b = k & 1;
-    const int slot = k % kSlots;
+    const int b = k & 1;      // input buffer
+    const int p = k & 1;      // output slot
     mbar_wait_parity(&S.full[b], (k >> 1) & 1u);
-    const R3Tile& it = S.in[b];
+    const S4Tile& it = S.in[b];
     const uint64_t cur = it.tile;
     if (cur >= ntiles) {
-      if (k >= kSlots) mbar_wait_parity(&S.st_empty[slot], ((k / kSlots) - 1) & 1u);
-      if (tid == 0) {
-        S.rec[slot].ts = e32::kDone;
-        S.rec[slot].end = head;
-      }
-      e32::slot_staged(&S.st_full[slot], slot);
+      if (k >= 2) mbar_wait_parity(&S.st_empty[p], ((k >> 1) - 1) & 1u);
+      if (tid == 0) S.tile_of[p] = cur;
+      mbar_arrive_warp(&S.st_full[p]);
       break;
     }
-    // ---- (A) this thread's block: in-tile offsets, register-path test ------
-    const uint64_t gb = cur * TB + tid;
+    // ---- this lane's block: in-tile input offsets without a CTA scan ---------
+    const int lb = warp * 32 + lane;
+    const uint64_t gb = cur * TB + lb;
     const bool active = gb < nblocks;
     const int len = !active ? 0 : (gb == nblocks - 1 ? static_cast<int>(in.tail_len) : K);
-    uint32_t w = it.w[tid];
-    const int32_t o = it.o[tid];
+    uint32_t w = it.w[lb];
+    const int32_t o = it.o[lb];
     if (w > 64) {
       flags |= HSZ_ERR_BAD_WIDTH;
       w = 0;
     }
     const uint32_t isb = w ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
     const uint32_t ipb = (static_cast<uint32_t>(len) * w + 7u) >> 3;
-    const bool slow_in = !(it.staged && w <= static_cast<uint32_t>(kFastW) && o > -(1 << 29) &&
-                           o < (1 << 29));
-    uint32_t itot;
-    bool slow;
-    const uint32_t iex = cta_scan_or(isb | (ipb << 10), S.scan_a, &itot, slow_in, &slow);
-    const uint32_t ies = iex & 1023u, iep = iex >> 10;
-    S.bes[tid] = ies;
-    S.bep[tid] = iep;
-    bool exact = slow || !sp.small_rs;            // CTA-uniform
-    uint32_t ts = 0, tp = 0;
-    if (!exact) {
-      // ---- decode, exact rescale (ops.py:199-208), code ---------------------
-      uint32_t qb[K];
-      bool ovf = false;
-      {
-        int32_t q[K];
-        decode_block<0, false>(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, o, len, q);
+    uint32_t base = 0;        // (sign | payload << 10) bytes of the preceding warps' blocks
+    for (int j = 0; j < warp; ++j) {   // blocks 32j + lane are full blocks (before ours)
+      const uint32_t wj = it.w[32 * j + lane];
+      base += (wj ? 4u : 0u) | ((4u * (wj > 64 ? 0u : wj)) << 10);
+    }
+    base = __reduce_add_sync(kFull, base);
+    uint32_t inc = isb | (ipb << 10);
 #pragma unroll
-        for (int i = 0; i < K; ++i) {
-          // bin * rs in one FMA from the biased bin (2^52 + 2^31 + bin): the
-          // exact product-sum is bin * rs (< 2^53), so the rounding is exact
-          const double pd = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(
-                                         static_cast<uint32_t>(q[i]) ^ 0x80000000u)),
-                                     sp.rsd, sp.negc);
-          const double tt = __dmul_rn(sp.d, pd);
-          // floor(RN(|t| + 1/2)) by one DADD rounding toward -inf against 2^52
-          const uint32_t mi = static_cast<uint32_t>(
-              __double2loint(__dadd_rd(__dadd_rn(fabs(tt), 0.5), 4503599627370496.0)));
-          ovf |= mi >= 1073741823u;
-          qb[i] = tt < 0.0 ? 0u - mi : mi;
-        }
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFull, inc, d);
+      if (lane >= d) inc += v;
+    }
+    const uint32_t iex = base + inc - (isb | (ipb << 10));
+    const uint32_t ies = iex & 1023u, iep = iex >> 10;
+    S.bes[lb] = ies;
+    S.bep[lb] = iep;
+    const bool fast_in = it.staged && w <= static_cast<uint32_t>(kFastW) && o > -(1 << 29) &&
+                         o < (1 << 29);
+    bool exact = __any_sync(kFull, !fast_in) || !sp.small_rs;      // warp-uniform
+    uint32_t qb[K];
+    if (!exact) {
+      bool ovf = false;
+      int32_t q[K];
+      decode_block<0, false>(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, o, len, q);
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        // bin * rs in one FMA from the biased bin (2^52 + 2^31 + bin): the
+        // exact product-sum is bin * rs (< 2^53), so the rounding is exact
+        const double pd = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(
+                                       static_cast<uint32_t>(q[i]) ^ 0x80000000u)),
+                                   sp.rsd, sp.negc);
+        const double tt = __dmul_rn(sp.d, pd);
+        // floor(RN(|t| + 1/2)) by one DADD rounding toward -inf against 2^52
+        const uint32_t mi = static_cast<uint32_t>(
+            __double2loint(__dadd_rd(__dadd_rn(fabs(tt), 0.5), 4503599627370496.0)));
+        ovf |= mi >= 1073741823u;
+        qb[i] = tt < 0.0 ? 0u - mi : mi;
       }
+      exact = __any_sync(kFull, ovf);
+    }
+    if (!exact) {
+      mbar_arrive_warp(&S.in_empty[b]);               // every read of S.in[b] done
       e32::BlockCode bc;
       e32::block_code(qb, len, bc);
       const uint32_t wmax = __reduce_max_sync(kFull, bc.w);
       const uint32_t sb = (bc.w && active) ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
       const uint32_t pb = (static_cast<uint32_t>(len) * bc.w + 7u) >> 3;
-      uint32_t tot;
-      // ---- (B) output sizes scan + overflow test; every read of S.in[b] done
-      const uint32_t ex = cta_scan_or(sb | (pb << 10), S.scan_b, &tot, ovf, &exact);
-      if (!exact) {
-        restage(b);                                 // tile k+2's copies fly during the pack
-        const uint32_t es = ex & 1023u, ep = ex >> 10;
-        ts = tot & 1023u;
-        tp = tot >> 10;
-        if (tid == 0) lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
-        if (active) {
-          out.widths[gb] = static_cast<uint8_t>(bc.w);
-          out.outliers[gb] = static_cast<int32_t>(qb[0]);
+      uint32_t oinc = sb | (pb << 10);
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(kFull, oinc, d);
+        if (lane >= d) oinc += v;
+      }
+      const uint32_t tot = __shfl_sync(kFull, oinc, 31);
+      const uint32_t ex = oinc - (sb | (pb << 10));
+      const uint32_t es = ex & 1023u, ep = ex >> 10;
+      if (active) {
+        out.widths[gb] = static_cast<uint8_t>(bc.w);
+        out.outliers[gb] = static_cast<int32_t>(qb[0]);
+      }
+      if (k >= 2) mbar_wait_parity(&S.st_empty[p], ((k >> 1) - 1) & 1u);
+      if (lane == 0) {
+        const uint32_t ts = tot & 1023u, tp = tot >> 10;
+        S.seg_s[p][warp] = ts;
+        S.seg_p[p][warp] = tp;
+        if (warp == 0) S.tile_of[p] = cur;
+        const unsigned long long mine = kAggCnt | (static_cast<unsigned long long>(ts) << 28) | tp;
+        const unsigned long long now = atomicAdd(&S.agg[p], mine) + mine;
+        if ((now >> 56) == 4) {               // the tile's last segment: publish its aggregate
+          S.agg[p] = 0;
+          lb_publish(lb_words(out.ws), cur, epoch, (now >> 28) & 0xFFFFFFFull, now & 0xFFFFFFFull);
         }
-        if (k >= kSlots) mbar_wait_parity(&S.st_empty[slot], ((k / kSlots) - 1) & 1u);
-        const uint32_t need = (tp + 127u) & ~127u;
-        uint32_t pos = static_cast<uint32_t>(head % kRing);
-        if (pos + need > kRing) {   // no wrap inside a tile: skip to the ring start
-          head += kRing - pos;
-          pos = 0;
-        }
-        if (head + need - S.ring_tail > kRing) {
-          unsigned ns = 32;
-          while (head + need - S.ring_tail > kRing) {
-            __nanosleep(ns);
-            ns = ns < 256 ? ns * 2 : 256;
-          }
-        }
-        head += need;
-        if (tid == 0) {
-          S.rec[slot].tile = cur;
-          S.rec[slot].end = head;
-          S.rec[slot].ts = ts;
-          S.rec[slot].tp = tp;
-          S.rec[slot].off = pos;
-        }
-        if (sb) S.sgn[slot][es >> 2] = bswap32(bc.sg);
-        e32::pack_block(bc, wmax, ep >> 2, reinterpret_cast<uint32_t*>(S.ring + pos));
-        e32::slot_staged(&S.st_full[slot], slot);
-        continue;
+      }
+      if (sb) S.sgn[p][warp][es >> 2] = bswap32(bc.sg);
+      e32::pack_block(bc, wmax, ep >> 2, reinterpret_cast<uint32_t*>(S.pay[p][warp]));
+      mbar_arrive_warp(&S.st_full[p]);
+      continue;
+    }
+    // ---- exact warp-per-block path for this warp's 32 blocks ----------------
+    __syncwarp();                                     // S.bes / S.bep of the warp visible
+    SrcSmul4 src{in, &it, S.bes, S.bep, sp.rs, sp.d};
+    if (k >= 2) mbar_wait_parity(&S.st_empty[p], ((k >> 1) - 1) & 1u);
+    flags |= k32::fallback_sizes(src, out, cur, nblocks, in.tail_len, S.seg_s[p], S.seg_p[p]);
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t ts = S.seg_s[p][warp], tp = S.seg_p[p][warp];
+      if (warp == 0) S.tile_of[p] = cur;
+      atomicOr(&S.seg_x[p], 1u << warp);
+      const unsigned long long mine = kAggCnt | (static_cast<unsigned long long>(ts) << 28) | tp;
+      const unsigned long long now = atomicAdd(&S.agg[p], mine) + mine;
+      if ((now >> 56) == 4) {
+        S.agg[p] = 0;
+        lb_publish(lb_words(out.ws), cur, epoch, (now >> 28) & 0xFFFFFFFull, now & 0xFFFFFFFull);
       }
     }
-    // ---- exact warp-per-block path: decodes from global memory, places itself
-    {
-      SrcSmul3 src{in, &it, S.bes, S.bep, sp.rs, sp.d};
-      e32::bar_sync_n(1, kCompute);                // S.bes / S.bep of every block visible
-      flags |= k32::fallback_sizes(src, out, cur, nblocks, in.tail_len, S.wsb, S.wpb);
-      e32::bar_sync_n(1, kCompute);
-      ts = S.wsb[0] + S.wsb[1] + S.wsb[2] + S.wsb[3];
-      tp = S.wpb[0] + S.wpb[1] + S.wpb[2] + S.wpb[3];
-      if (tid == 0) lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
-      if (k >= kSlots) mbar_wait_parity(&S.st_empty[slot], ((k / kSlots) - 1) & 1u);
-      if (tid == 0) {
-        S.rec[slot].tile = cur;
-        S.rec[slot].end = head;
-        S.rec[slot].ts = e32::kSelfPlaced;
+    mbar_arrive_warp(&S.st_full[p]);
+    // wait for the placement warp's resolution of this tile, then write
+    if (lane == 0) {
+      unsigned ns = 32;
+      while (S.res_tile[p] != cur) {
+        __nanosleep(ns);
+        ns = ns < 256 ? ns * 2 : 256;
       }
-      e32::slot_staged(&S.st_full[slot], slot);
-      if (warp == 0) {
-        uint64_t es, ep;
-        e32::resolve6(out, cur, epoch, ntiles, ts, tp, &es, &ep);
-        if (lane == 0) {
-          S.excl_s[slot] = es;
-          S.excl_p[slot] = ep;
-        }
-      }
-      e32::bar_sync_n(1, kCompute);
-      if (S.excl_s[slot] != ~0ull) {
-        uint64_t gs = S.excl_s[slot], gp = S.excl_p[slot];
-        for (int i = 0; i < warp; ++i) {
-          gs += S.wsb[i];
-          gp += S.wpb[i];
-        }
-        k32::fallback_pack(src, out, cur, nblocks, in.tail_len, gs, gp, S.xscratch[warp]);
-      }
-      e32::bar_sync_n(1, kCompute);                // every read of S.in[b] done
-      restage(b);
     }
+    __syncwarp();
+    __threadfence_block();
+    const uint64_t gs = S.xs[p][warp], gp = S.xp[p][warp];
+    if (gs != ~0ull)
+      k32::fallback_pack(src, out, cur, nblocks, in.tail_len, gs, gp, S.xscratch[warp]);
+    mbar_arrive_warp(&S.in_empty[b]);
   }
   flags = __reduce_or_sync(kFull, flags);
   if (lane == 0 && flags) atomicOr(out.err, flags);
@@ -1149,7 +1175,7 @@ constexpr int kDecThreads = kCompute + 32;
 // named barrier needs.  Barrier ids: 1 = the compute group, 2-3 full[b],
 // 4-5 empty[b].
 #ifndef HSZ_DEC_NAMED
-#define HSZ_DEC_NAMED 1
+#define HSZ_DEC_NAMED 0
 #endif
 constexpr int kBarFull = 2, kBarEmpty = 4;
 

@@ -449,7 +449,7 @@ constexpr int kThreadsC = kCompute + 32;
 // hand-off alternates strictly (slot s is refilled only after the placement
 // warp released it on st_empty[s]).
 #ifndef HSZ_PLACE_NAMED
-#define HSZ_PLACE_NAMED 1
+#define HSZ_PLACE_NAMED 0
 #endif
 constexpr int kBarSlot = 2;
 
