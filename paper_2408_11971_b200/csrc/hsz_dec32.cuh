@@ -806,11 +806,14 @@ constexpr uint32_t kSmulSmemBytes = recode_smem_bytes<kOpSmul>();
 //     shared atomic) publishes the tile aggregate for the look-back;
 //   * input tiles are double-buffered; the stager restages a buffer once all
 //     four warps released it, so warps drift apart by up to a tile.
-// The placement warp resolves each tile (decoupled look-back over whole
-// 128-block tiles, so the tile-offset cache is unchanged) and copies the four
-// segments out.  A warp that needs the exact (64/128-bit) path reports its
-// segment sizes, waits for the tile's resolution and writes its blocks to
-// global memory itself.
+// The placement warp only resolves each tile (decoupled look-back over whole
+// 128-block tiles, so the tile-offset cache is unchanged) and posts each
+// warp's global offsets; every compute warp copies its OWN staged segment out
+// one tile later (its two slot regions alternate, so no warp ever waits for
+// another warp's copy, and the copy-out work is spread over four warps
+// instead of serialising behind the look-back).  A warp that needs the exact
+// (64/128-bit) path reports its segment sizes, waits for the tile's
+// resolution and writes its blocks to global memory itself.
 
 #ifndef HSZ_S4_PAYCAP
 #define HSZ_S4_PAYCAP 8192
@@ -825,12 +828,11 @@ struct S4Smem {
   alignas(16) unsigned char pay[2][4][kSegCap];  // per slot, per warp: packed payload
   alignas(16) uint32_t sgn[2][4][32];           // per slot, per warp: sign words
   uint32_t seg_s[2][4], seg_p[2][4];            // per slot, per warp: segment sizes
-  uint32_t seg_x[2];                            // bit q: warp q places itself (exact path)
   unsigned long long agg[2];                    // per slot: reported segments (count, sums)
   uint64_t tile_of[2];
   uint64_t xs[2][4], xp[2][4];                  // resolved offsets of self-placing warps
   volatile uint64_t res_tile[2];                // the tile whose xs/xp are valid
-  uint64_t full[2], in_empty[2], st_full[2], st_empty[2];
+  uint64_t full[2], in_empty[2], st_full[2];
   uint64_t epoch;
   uint32_t bes[TB], bep[TB];                    // in-tile input offsets (exact path)
   uint32_t xscratch[4][64];                     // exact path: one block's packed words per warp
@@ -894,9 +896,7 @@ __global__ void __launch_bounds__(kS4Threads, HSZ_ENC_CTAS)
       mbar_init(&S.full[b], 1);
       mbar_init(&S.in_empty[b], kCompute / 32);
       mbar_init(&S.st_full[b], kCompute / 32);
-      mbar_init(&S.st_empty[b], 1);
       S.agg[b] = 0;
-      S.seg_x[b] = 0;
       S.res_tile[b] = ~0ull;
     }
     fence_mbar_init();
@@ -935,7 +935,8 @@ __global__ void __launch_bounds__(kS4Threads, HSZ_ENC_CTAS)
   }
 
   if (warp == kCompute / 32 + 1) {
-    // =========================== placement warp ===========================
+    // ==================== placement warp: look-back only ====================
+    // (the compute warps copy their own segments out, one tile later)
     for (uint32_t kk = 0;; ++kk) {
       const int p = kk & 1;
       mbar_wait_parity_sleep(&S.st_full[p], (kk >> 1) & 1u);
@@ -952,8 +953,8 @@ __global__ void __launch_bounds__(kS4Threads, HSZ_ENC_CTAS)
       }
       uint64_t es, ep;
       lb_resolve(lb_words(out.ws), cur, epoch, ts, tp, &es, &ep, out.err);
-      const bool fits = es + ts <= out.sign_cap && ep + tp <= out.payload_cap;
       if (lane == 0) {
+        const bool fits = es + ts <= out.sign_cap && ep + tp <= out.payload_cap;
         out.toff[2 * cur] = es;
         out.toff[2 * cur + 1] = ep;
         if (cur == ntiles - 1) {
@@ -961,31 +962,16 @@ __global__ void __launch_bounds__(kS4Threads, HSZ_ENC_CTAS)
           out.toff[2 * ntiles + 1] = ep + tp;
         }
         if (!fits) atomicOr(out.err, HSZ_ERR_CAPACITY);
-      }
-      const uint32_t xmask = S.seg_x[p];
-      uint64_t os = es, op = ep;
+        uint64_t os = es, op = ep;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if ((xmask >> q) & 1u) {
-          if (lane == 0) {
-            S.xs[p][q] = fits ? os : ~0ull;
-            S.xp[p][q] = op;
-          }
-        } else if (fits) {
-          copy_segment(S.sgn[p][q], S.pay[p][q], out, ss[q], pp[q], os, op);
+        for (int q = 0; q < 4; ++q) {
+          S.xs[p][q] = fits ? os : ~0ull;
+          S.xp[p][q] = op;
+          os += ss[q];
+          op += pp[q];
         }
-        os += ss[q];
-        op += pp[q];
-      }
-      __syncwarp();
-      if (lane == 0) {
-        if (xmask) {
-          __threadfence_block();
-          S.res_tile[p] = cur;              // self-placing warps may write now
-        }
-        S.seg_x[p] = 0;
-        __threadfence_block();              // the slot's reads complete before it is reused
-        mbar_arrive(&S.st_empty[p]);
+        __threadfence_block();
+        S.res_tile[p] = cur;                  // the tile's segments may be written now
       }
     }
     return;
@@ -993,6 +979,32 @@ __global__ void __launch_bounds__(kS4Threads, HSZ_ENC_CTAS)
 
   // =========================== compute warps ===========================
   uint32_t flags = 0;
+  // the warp's staged segment of the previous tile, copied out once the
+  // placement warp resolved it (a tile later: the wait is almost never felt)
+  bool pend = false;
+  int pend_p = 0;
+  uint64_t pend_tile = 0;
+  uint32_t pend_ts = 0, pend_tp = 0;
+  auto wait_resolved = [&](int p, uint64_t tile) {
+    if (lane == 0) {
+      unsigned ns = 32;
+      while (S.res_tile[p] != tile) {
+        __nanosleep(ns);
+        ns = ns < 256 ? ns * 2 : 256;
+      }
+    }
+    __syncwarp();
+    __threadfence_block();
+  };
+  auto flush_pending = [&]() {
+    if (!pend) return;
+    wait_resolved(pend_p, pend_tile);
+    const uint64_t gs = S.xs[pend_p][warp], gp = S.xp[pend_p][warp];
+    if (gs != ~0ull)
+      copy_segment(S.sgn[pend_p][warp], S.pay[pend_p][warp], out, pend_ts, pend_tp, gs, gp);
+    __syncwarp();
+    pend = false;
+  };
   for (uint32_t k = 0;; ++k) {
     const int b = k & 1;      // input buffer
     const int p = k & 1;      // output slot
@@ -1000,7 +1012,7 @@ __global__ void __launch_bounds__(kS4Threads, HSZ_ENC_CTAS)
     const S4Tile& it = S.in[b];
     const uint64_t cur = it.tile;
     if (cur >= ntiles) {
-      if (k >= 2) mbar_wait_parity(&S.st_empty[p], ((k >> 1) - 1) & 1u);
+      flush_pending();
       if (tid == 0) S.tile_of[p] = cur;
       mbar_arrive_warp(&S.st_full[p]);
       break;
@@ -1074,13 +1086,12 @@ __global__ void __launch_bounds__(kS4Threads, HSZ_ENC_CTAS)
       const uint32_t tot = __shfl_sync(kFull, oinc, 31);
       const uint32_t ex = oinc - (sb | (pb << 10));
       const uint32_t es = ex & 1023u, ep = ex >> 10;
+      const uint32_t ts = tot & 1023u, tp = tot >> 10;
       if (active) {
         out.widths[gb] = static_cast<uint8_t>(bc.w);
         out.outliers[gb] = static_cast<int32_t>(qb[0]);
       }
-      if (k >= 2) mbar_wait_parity(&S.st_empty[p], ((k >> 1) - 1) & 1u);
       if (lane == 0) {
-        const uint32_t ts = tot & 1023u, tp = tot >> 10;
         S.seg_s[p][warp] = ts;
         S.seg_p[p][warp] = tp;
         if (warp == 0) S.tile_of[p] = cur;
@@ -1091,21 +1102,27 @@ __global__ void __launch_bounds__(kS4Threads, HSZ_ENC_CTAS)
           lb_publish(lb_words(out.ws), cur, epoch, (now >> 28) & 0xFFFFFFFull, now & 0xFFFFFFFull);
         }
       }
+      // this warp's own staging region of slot p held tile k-2: copied out already
       if (sb) S.sgn[p][warp][es >> 2] = bswap32(bc.sg);
       e32::pack_block(bc, wmax, ep >> 2, reinterpret_cast<uint32_t*>(S.pay[p][warp]));
       mbar_arrive_warp(&S.st_full[p]);
+      flush_pending();                                // tile k-1's segment (slot p ^ 1)
+      pend = true;
+      pend_p = p;
+      pend_tile = cur;
+      pend_ts = ts;
+      pend_tp = tp;
       continue;
     }
     // ---- exact warp-per-block path for this warp's 32 blocks ----------------
+    flush_pending();
     __syncwarp();                                     // S.bes / S.bep of the warp visible
     SrcSmul4 src{in, &it, S.bes, S.bep, sp.rs, sp.d};
-    if (k >= 2) mbar_wait_parity(&S.st_empty[p], ((k >> 1) - 1) & 1u);
     flags |= k32::fallback_sizes(src, out, cur, nblocks, in.tail_len, S.seg_s[p], S.seg_p[p]);
     __syncwarp();
     if (lane == 0) {
       const uint32_t ts = S.seg_s[p][warp], tp = S.seg_p[p][warp];
       if (warp == 0) S.tile_of[p] = cur;
-      atomicOr(&S.seg_x[p], 1u << warp);
       const unsigned long long mine = kAggCnt | (static_cast<unsigned long long>(ts) << 28) | tp;
       const unsigned long long now = atomicAdd(&S.agg[p], mine) + mine;
       if ((now >> 56) == 4) {
@@ -1114,16 +1131,7 @@ __global__ void __launch_bounds__(kS4Threads, HSZ_ENC_CTAS)
       }
     }
     mbar_arrive_warp(&S.st_full[p]);
-    // wait for the placement warp's resolution of this tile, then write
-    if (lane == 0) {
-      unsigned ns = 32;
-      while (S.res_tile[p] != cur) {
-        __nanosleep(ns);
-        ns = ns < 256 ? ns * 2 : 256;
-      }
-    }
-    __syncwarp();
-    __threadfence_block();
+    wait_resolved(p, cur);                            // then write the blocks in place
     const uint64_t gs = S.xs[p][warp], gp = S.xp[p][warp];
     if (gs != ~0ull)
       k32::fallback_pack(src, out, cur, nblocks, in.tail_len, gs, gp, S.xscratch[warp]);
