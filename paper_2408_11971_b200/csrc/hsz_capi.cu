@@ -698,33 +698,6 @@ static int launch_recode(const d32::StreamIn& a, const d32::StreamIn& b, const d
   return launch_status();
 }
 
-#ifndef HSZ_SMUL_V4
-#define HSZ_SMUL_V4 1
-#endif
-
-// scalar_mul v4 (d32::smul4_kernel): persistent, every CTA resident
-static int launch_smul4(const d32::StreamIn& a, const d32::SmulParams& sp, const k32::EncodeOut& out,
-                        uint64_t nt, cudaStream_t st) {
-  constexpr int smem = static_cast<int>(d32::kS4SmemBytes);
-  auto kern = d32::smul4_kernel;
-  static int resident = 0, resident_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (resident_dev != dev) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
-    int per_sm = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, d32::kS4Threads, smem);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    resident = (per_sm > 0 ? per_sm : 1) * sms;
-    resident_dev = dev;
-  }
-  const uint64_t grid = nt < static_cast<uint64_t>(resident) ? nt : static_cast<uint64_t>(resident);
-  kern<<<static_cast<unsigned>(grid), d32::kS4Threads, smem, st>>>(a, sp, out);
-  return launch_status();
-}
-
 namespace hsz {
 namespace ops {
 // mailbox post for reduction paths that do not post in-kernel
@@ -1104,11 +1077,7 @@ int hsz_scalar_mul(const uint8_t* widths, const int32_t* outliers, const uint8_t
     sp.small_rs = (rs > -(1ll << 23) && rs < (1ll << 23)) ? 1 : 0;
     sp.negc = -4503601774854144.0 * sp.rsd;   // exact when small_rs (register path only)
     const k32::EncodeOut out{ow, oo, os, sign_cap, op, payload_cap, otoff, err, ws};
-#if HSZ_SMUL_V4
-    return launch_smul4(in, sp, out, nt, st);
-#else
     return launch_recode<d32::kOpSmul>(in, in, sp, out, nt, st);
-#endif
   }
   if (!scratch) return HSZ_EINVAL;
   int64_t* bins = static_cast<int64_t*>(scratch);

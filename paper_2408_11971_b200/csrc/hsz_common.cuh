@@ -172,38 +172,6 @@ __device__ __forceinline__ bool grp_and(bool p) {
   return r != 0;
 }
 
-// Named-barrier hand-offs with IMMEDIATE ids (a register id makes ptxas
-// reserve all 16 barriers of the CTA): kN threads take part (producer +
-// consumer threads); bar.sync blocks in hardware without issuing, unlike a
-// polled mbarrier.  Only for hand-offs that strictly alternate.
-template <int kId, int kN>
-__device__ __forceinline__ void nbar_sync_i() {
-  asm volatile("bar.sync %0, %1;" ::"n"(kId), "n"(kN) : "memory");
-}
-template <int kId, int kN>
-__device__ __forceinline__ void nbar_arrive_i() {
-  asm volatile("bar.arrive %0, %1;" ::"n"(kId), "n"(kN) : "memory");
-}
-// barrier kBase + i, i in [0, 4)
-template <int kBase, int kN>
-__device__ __forceinline__ void nbar_sync4(int i) {
-  switch (i) {
-    case 0: nbar_sync_i<kBase, kN>(); break;
-    case 1: nbar_sync_i<kBase + 1, kN>(); break;
-    case 2: nbar_sync_i<kBase + 2, kN>(); break;
-    default: nbar_sync_i<kBase + 3, kN>(); break;
-  }
-}
-template <int kBase, int kN>
-__device__ __forceinline__ void nbar_arrive4(int i) {
-  switch (i) {
-    case 0: nbar_arrive_i<kBase, kN>(); break;
-    case 1: nbar_arrive_i<kBase + 1, kN>(); break;
-    case 2: nbar_arrive_i<kBase + 2, kN>(); break;
-    default: nbar_arrive_i<kBase + 3, kN>(); break;
-  }
-}
-
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

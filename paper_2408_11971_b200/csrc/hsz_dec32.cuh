@@ -791,357 +791,6 @@ constexpr uint32_t recode_smem_bytes() { return sizeof(RecodeSmem<kOp>) + 1024; 
 constexpr uint32_t kSmulSmemBytes = recode_smem_bytes<kOpSmul>();
 
 // ---------------------------------------------------------------------------
-// scalar_mul v4 (ops.py:199-225): barrier-free compute warps.
-//
-// recode_kernel keeps the 4 compute warps of a CTA in lockstep (four CTA
-// barriers per tile) and single-buffers the input; ncu on config 4 shows the
-// compute warps spending about half their time waiting there (barrier stalls
-// and the loop-top wait for the next tile).  Here every compute warp owns
-// blocks [32q, 32q + 32) of each tile and never waits for another warp:
-//   * in-tile input offsets: a warp scan plus the sizes of the preceding
-//     warps' blocks, recomputed from their widths (no CTA scan);
-//   * the register-path / exact decision is per warp;
-//   * output: the warp packs its segment into its own staging region of the
-//     tile's slot; the LAST warp to report its segment sizes (one 64-bit
-//     shared atomic) publishes the tile aggregate for the look-back;
-//   * input tiles are double-buffered; the stager restages a buffer once all
-//     four warps released it, so warps drift apart by up to a tile.
-// The placement warp only resolves each tile (decoupled look-back over whole
-// 128-block tiles, so the tile-offset cache is unchanged) and posts each
-// warp's global offsets; every compute warp copies its OWN staged segment out
-// one tile later (its two slot regions alternate, so no warp ever waits for
-// another warp's copy, and the copy-out work is spread over four warps
-// instead of serialising behind the look-back).  A warp that needs the exact
-// (64/128-bit) path reports its segment sizes, waits for the tile's
-// resolution and writes its blocks to global memory itself.
-
-#ifndef HSZ_S4_PAYCAP
-#define HSZ_S4_PAYCAP 8192
-#endif
-constexpr uint32_t kS4PayCap = HSZ_S4_PAYCAP;
-using S4Tile = InTileT<kS4PayCap>;
-constexpr uint32_t kSegCap = 4096;              // a warp's packed payload: 32 blocks, w <= 31
-constexpr uint64_t kAggCnt = 1ull << 56;        // aggregate word: count | sign bytes << 28 | payload
-
-struct S4Smem {
-  S4Tile in[2];                                 // double-buffered input tiles
-  alignas(16) unsigned char pay[2][4][kSegCap];  // per slot, per warp: packed payload
-  alignas(16) uint32_t sgn[2][4][32];           // per slot, per warp: sign words
-  uint32_t seg_s[2][4], seg_p[2][4];            // per slot, per warp: segment sizes
-  unsigned long long agg[2];                    // per slot: reported segments (count, sums)
-  uint64_t tile_of[2];
-  uint64_t xs[2][4], xp[2][4];                  // resolved offsets of self-placing warps
-  volatile uint64_t res_tile[2];                // the tile whose xs/xp are valid
-  uint64_t full[2], in_empty[2], st_full[2];
-  uint64_t epoch;
-  uint32_t bes[TB], bep[TB];                    // in-tile input offsets (exact path)
-  uint32_t xscratch[4][64];                     // exact path: one block's packed words per warp
-};
-constexpr uint32_t kS4SmemBytes = sizeof(S4Smem) + 1024;
-constexpr int kS4Threads = kCompute + 64;       // 4 compute warps + stager + placement
-
-// the exact warp-per-block source of v4 (input block decoded from global memory)
-struct SrcSmul4 {
-  StreamIn in;
-  const S4Tile* it;
-  const uint32_t* bes;
-  const uint32_t* bep;
-  int64_t rs;
-  double d;
-  __device__ __forceinline__ int64_t lane_bin(int lb, int lane, int len, uint32_t* flags) {
-    uint32_t f = 0;
-    const int64_t q = k32::decode_lane(in.signs, in.payload, it->w[lb], it->o[lb], it->gs0 + bes[lb],
-                                       it->gp0 + bep[lb], len, lane, &f);
-    *flags |= f;
-    if (f || lane >= len) return 0;
-    return rescale1(product_rn(q, rs), d, flags);
-  }
-};
-
-// placement warp: copy one warp segment (sign words + payload) to its offsets
-__device__ __forceinline__ void copy_segment(const uint32_t* sgn, const unsigned char* pay,
-                                             const k32::EncodeOut& out, uint32_t ts, uint32_t tp,
-                                             uint64_t es, uint64_t ep) {
-  const uint32_t lane = threadIdx.x & 31;
-  uint32_t* dsg = reinterpret_cast<uint32_t*>(out.signs + es);
-  if (lane < ((ts + 3u) >> 2)) dsg[lane] = sgn[lane];
-  const uint32_t* pbuf = reinterpret_cast<const uint32_t*>(pay);
-  uint32_t* dst = reinterpret_cast<uint32_t*>(out.payload + ep);
-  const uint32_t nw = (tp + 3u) >> 2;
-  uint32_t head = static_cast<uint32_t>(((16u - (ep & 15u)) & 15u) >> 2);
-  head = head < nw ? head : nw;
-  if (lane < head) dst[lane] = pbuf[e32::swz_word(lane)];
-  const uint32_t nv = (nw - head) >> 2;
-  uint4* dv = reinterpret_cast<uint4*>(dst + head);
-  for (uint32_t i = lane; i < nv; i += 32) {
-    const uint32_t k = head + 4u * i;
-    dv[i] = make_uint4(pbuf[e32::swz_word(k)], pbuf[e32::swz_word(k + 1)],
-                       pbuf[e32::swz_word(k + 2)], pbuf[e32::swz_word(k + 3)]);
-  }
-  const uint32_t rest = head + 4u * nv + lane;
-  if (rest < nw) dst[rest] = pbuf[e32::swz_word(rest)];
-}
-
-__global__ void __launch_bounds__(kS4Threads, HSZ_ENC_CTAS)
-    smul4_kernel(StreamIn in, SmulParams sp, k32::EncodeOut out) {
-  extern __shared__ unsigned char smraw[];
-  const uint32_t a0 = smem_u32(smraw);
-  S4Smem& S = *reinterpret_cast<S4Smem*>(smraw + (((a0 + 1023u) & ~1023u) - a0));
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint64_t ntiles = in.ntiles, nblocks = in.nblocks;
-  LookbackWs lw = LookbackWs::bind(out.ws, ntiles);
-  const uint64_t last_draw = ntiles + gridDim.x - 1;   // every CTA draws once past the end
-  if (tid == 0) {
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&S.full[b], 1);
-      mbar_init(&S.in_empty[b], kCompute / 32);
-      mbar_init(&S.st_full[b], kCompute / 32);
-      S.agg[b] = 0;
-      S.res_tile[b] = ~0ull;
-    }
-    fence_mbar_init();
-    S.epoch = ld_acquire(lw.epoch);
-  }
-  __syncthreads();
-  const uint64_t epoch = S.epoch;
-
-  if (warp == kCompute / 32) {
-    // ============================ stager warp ==============================
-    auto draw = [&]() -> uint64_t {
-      const uint64_t t = atom_add_relaxed(lw.ticket, 1);
-      if (t == last_draw) {
-        st_relaxed(lw.ticket, 0);
-        st_release(lw.epoch, epoch + 1);
-      }
-      return t;
-    };
-    uint64_t t = 0, ahead = ~0ull;
-    if (lane == 0) {
-      t = draw();
-      if (t < ntiles) ahead = draw();
-    }
-    t = __shfl_sync(kFull, t, 0);
-    uint64_t tv = prefetch_toff(in, t);
-    for (uint32_t i = 0;; ++i) {
-      const int b = i & 1;
-      if (i >= 2) mbar_wait_parity_sleep(&S.in_empty[b], ((i >> 1) - 1) & 1u);
-      stage_tile(in, t, tv, S.in[b], &S.full[b]);
-      if (t >= ntiles) break;
-      t = __shfl_sync(kFull, ahead, 0);            // drawn one tile ago
-      tv = prefetch_toff(in, t);
-      if (lane == 0 && t < ntiles) ahead = draw();
-    }
-    return;
-  }
-
-  if (warp == kCompute / 32 + 1) {
-    // ==================== placement warp: look-back only ====================
-    // (the compute warps copy their own segments out, one tile later)
-    for (uint32_t kk = 0;; ++kk) {
-      const int p = kk & 1;
-      mbar_wait_parity_sleep(&S.st_full[p], (kk >> 1) & 1u);
-      const uint64_t cur = S.tile_of[p];
-      if (cur >= ntiles) break;
-      uint32_t ss[4], pp[4];
-      uint32_t ts = 0, tp = 0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        ss[q] = S.seg_s[p][q];
-        pp[q] = S.seg_p[p][q];
-        ts += ss[q];
-        tp += pp[q];
-      }
-      uint64_t es, ep;
-      lb_resolve(lb_words(out.ws), cur, epoch, ts, tp, &es, &ep, out.err);
-      if (lane == 0) {
-        const bool fits = es + ts <= out.sign_cap && ep + tp <= out.payload_cap;
-        out.toff[2 * cur] = es;
-        out.toff[2 * cur + 1] = ep;
-        if (cur == ntiles - 1) {
-          out.toff[2 * ntiles] = es + ts;
-          out.toff[2 * ntiles + 1] = ep + tp;
-        }
-        if (!fits) atomicOr(out.err, HSZ_ERR_CAPACITY);
-        uint64_t os = es, op = ep;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          S.xs[p][q] = fits ? os : ~0ull;
-          S.xp[p][q] = op;
-          os += ss[q];
-          op += pp[q];
-        }
-        __threadfence_block();
-        S.res_tile[p] = cur;                  // the tile's segments may be written now
-      }
-    }
-    return;
-  }
-
-  // =========================== compute warps ===========================
-  uint32_t flags = 0;
-  // the warp's staged segment of the previous tile, copied out once the
-  // placement warp resolved it (a tile later: the wait is almost never felt)
-  bool pend = false;
-  int pend_p = 0;
-  uint64_t pend_tile = 0;
-  uint32_t pend_ts = 0, pend_tp = 0;
-  auto wait_resolved = [&](int p, uint64_t tile) {
-    if (lane == 0) {
-      unsigned ns = 32;
-      while (S.res_tile[p] != tile) {
-        __nanosleep(ns);
-        ns = ns < 256 ? ns * 2 : 256;
-      }
-    }
-    __syncwarp();
-    __threadfence_block();
-  };
-  auto flush_pending = [&]() {
-    if (!pend) return;
-    wait_resolved(pend_p, pend_tile);
-    const uint64_t gs = S.xs[pend_p][warp], gp = S.xp[pend_p][warp];
-    if (gs != ~0ull)
-      copy_segment(S.sgn[pend_p][warp], S.pay[pend_p][warp], out, pend_ts, pend_tp, gs, gp);
-    __syncwarp();
-    pend = false;
-  };
-  for (uint32_t k = 0;; ++k) {
-    const int b = k & 1;      // input buffer
-    const int p = k & 1;      // output slot
-    mbar_wait_parity(&S.full[b], (k >> 1) & 1u);
-    const S4Tile& it = S.in[b];
-    const uint64_t cur = it.tile;
-    if (cur >= ntiles) {
-      flush_pending();
-      if (tid == 0) S.tile_of[p] = cur;
-      mbar_arrive_warp(&S.st_full[p]);
-      break;
-    }
-    // ---- this lane's block: in-tile input offsets without a CTA scan ---------
-    const int lb = warp * 32 + lane;
-    const uint64_t gb = cur * TB + lb;
-    const bool active = gb < nblocks;
-    const int len = !active ? 0 : (gb == nblocks - 1 ? static_cast<int>(in.tail_len) : K);
-    uint32_t w = it.w[lb];
-    const int32_t o = it.o[lb];
-    if (w > 64) {
-      flags |= HSZ_ERR_BAD_WIDTH;
-      w = 0;
-    }
-    const uint32_t isb = w ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
-    const uint32_t ipb = (static_cast<uint32_t>(len) * w + 7u) >> 3;
-    uint32_t base = 0;        // (sign | payload << 10) bytes of the preceding warps' blocks
-    for (int j = 0; j < warp; ++j) {   // blocks 32j + lane are full blocks (before ours)
-      const uint32_t wj = it.w[32 * j + lane];
-      base += (wj ? 4u : 0u) | ((4u * (wj > 64 ? 0u : wj)) << 10);
-    }
-    base = __reduce_add_sync(kFull, base);
-    uint32_t inc = isb | (ipb << 10);
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(kFull, inc, d);
-      if (lane >= d) inc += v;
-    }
-    const uint32_t iex = base + inc - (isb | (ipb << 10));
-    const uint32_t ies = iex & 1023u, iep = iex >> 10;
-    S.bes[lb] = ies;
-    S.bep[lb] = iep;
-    const bool fast_in = it.staged && w <= static_cast<uint32_t>(kFastW) && o > -(1 << 29) &&
-                         o < (1 << 29);
-    bool exact = __any_sync(kFull, !fast_in) || !sp.small_rs;      // warp-uniform
-    uint32_t qb[K];
-    if (!exact) {
-      bool ovf = false;
-      int32_t q[K];
-      decode_block<0, false>(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, o, len, q);
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        // bin * rs in one FMA from the biased bin (2^52 + 2^31 + bin): the
-        // exact product-sum is bin * rs (< 2^53), so the rounding is exact
-        const double pd = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(
-                                       static_cast<uint32_t>(q[i]) ^ 0x80000000u)),
-                                   sp.rsd, sp.negc);
-        const double tt = __dmul_rn(sp.d, pd);
-        // floor(RN(|t| + 1/2)) by one DADD rounding toward -inf against 2^52
-        const uint32_t mi = static_cast<uint32_t>(
-            __double2loint(__dadd_rd(__dadd_rn(fabs(tt), 0.5), 4503599627370496.0)));
-        ovf |= mi >= 1073741823u;
-        qb[i] = tt < 0.0 ? 0u - mi : mi;
-      }
-      exact = __any_sync(kFull, ovf);
-    }
-    if (!exact) {
-      mbar_arrive_warp(&S.in_empty[b]);               // every read of S.in[b] done
-      e32::BlockCode bc;
-      e32::block_code(qb, len, bc);
-      const uint32_t wmax = __reduce_max_sync(kFull, bc.w);
-      const uint32_t sb = (bc.w && active) ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
-      const uint32_t pb = (static_cast<uint32_t>(len) * bc.w + 7u) >> 3;
-      uint32_t oinc = sb | (pb << 10);
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t v = __shfl_up_sync(kFull, oinc, d);
-        if (lane >= d) oinc += v;
-      }
-      const uint32_t tot = __shfl_sync(kFull, oinc, 31);
-      const uint32_t ex = oinc - (sb | (pb << 10));
-      const uint32_t es = ex & 1023u, ep = ex >> 10;
-      const uint32_t ts = tot & 1023u, tp = tot >> 10;
-      if (active) {
-        out.widths[gb] = static_cast<uint8_t>(bc.w);
-        out.outliers[gb] = static_cast<int32_t>(qb[0]);
-      }
-      if (lane == 0) {
-        S.seg_s[p][warp] = ts;
-        S.seg_p[p][warp] = tp;
-        if (warp == 0) S.tile_of[p] = cur;
-        const unsigned long long mine = kAggCnt | (static_cast<unsigned long long>(ts) << 28) | tp;
-        const unsigned long long now = atomicAdd(&S.agg[p], mine) + mine;
-        if ((now >> 56) == 4) {               // the tile's last segment: publish its aggregate
-          S.agg[p] = 0;
-          lb_publish(lb_words(out.ws), cur, epoch, (now >> 28) & 0xFFFFFFFull, now & 0xFFFFFFFull);
-        }
-      }
-      // this warp's own staging region of slot p held tile k-2: copied out already
-      if (sb) S.sgn[p][warp][es >> 2] = bswap32(bc.sg);
-      e32::pack_block(bc, wmax, ep >> 2, reinterpret_cast<uint32_t*>(S.pay[p][warp]));
-      mbar_arrive_warp(&S.st_full[p]);
-      flush_pending();                                // tile k-1's segment (slot p ^ 1)
-      pend = true;
-      pend_p = p;
-      pend_tile = cur;
-      pend_ts = ts;
-      pend_tp = tp;
-      continue;
-    }
-    // ---- exact warp-per-block path for this warp's 32 blocks ----------------
-    flush_pending();
-    __syncwarp();                                     // S.bes / S.bep of the warp visible
-    SrcSmul4 src{in, &it, S.bes, S.bep, sp.rs, sp.d};
-    flags |= k32::fallback_sizes(src, out, cur, nblocks, in.tail_len, S.seg_s[p], S.seg_p[p]);
-    __syncwarp();
-    if (lane == 0) {
-      const uint32_t ts = S.seg_s[p][warp], tp = S.seg_p[p][warp];
-      if (warp == 0) S.tile_of[p] = cur;
-      const unsigned long long mine = kAggCnt | (static_cast<unsigned long long>(ts) << 28) | tp;
-      const unsigned long long now = atomicAdd(&S.agg[p], mine) + mine;
-      if ((now >> 56) == 4) {
-        S.agg[p] = 0;
-        lb_publish(lb_words(out.ws), cur, epoch, (now >> 28) & 0xFFFFFFFull, now & 0xFFFFFFFull);
-      }
-    }
-    mbar_arrive_warp(&S.st_full[p]);
-    wait_resolved(p, cur);                            // then write the blocks in place
-    const uint64_t gs = S.xs[p][warp], gp = S.xp[p][warp];
-    if (gs != ~0ull)
-      k32::fallback_pack(src, out, cur, nblocks, in.tail_len, gs, gp, S.xscratch[warp]);
-    mbar_arrive_warp(&S.in_empty[b]);
-  }
-  flags = __reduce_or_sync(kFull, flags);
-  if (lane == 0 && flags) atomicOr(out.err, flags);
-}
-
-// ---------------------------------------------------------------------------
 // Decode pipeline (moments, decompress to float32): persistent CTAs of 4
 // compute warps + 1 TMA warp; tiles by grid stride (no ordering needed),
 // input double-buffered.
@@ -1173,55 +822,6 @@ struct DecSmem {
 template <int kMode>
 constexpr uint32_t dec_smem_bytes() { return sizeof(DecSmem<kMode>) + 1024; }
 constexpr int kDecThreads = kCompute + 32;
-
-// Hand-offs between the TMA warp and the compute warps (HSZ_DEC_NAMED): the
-// TMA warp alone waits for a tile's bytes (mbarrier complete_tx), then
-// releases the compute warps through a NAMED barrier -- they block in
-// hardware instead of polling an mbarrier (the polls were ~12% of the
-// moment kernels' issued instructions).  Both hand-offs strictly alternate
-// per buffer (a buffer is restaged only after its release), which is what a
-// named barrier needs.  Barrier ids: 1 = the compute group, 2-3 full[b],
-// 4-5 empty[b].
-#ifndef HSZ_DEC_NAMED
-#define HSZ_DEC_NAMED 0
-#endif
-constexpr int kBarFull = 2, kBarEmpty = 4;
-
-// named barrier ops with IMMEDIATE ids (a register id makes ptxas reserve all
-// 16 barriers of the CTA)
-template <int kId>
-__device__ __forceinline__ void nbar_sync() {
-  asm volatile("bar.sync %0, %1;" ::"n"(kId), "n"(kDecThreads) : "memory");
-}
-template <int kId>
-__device__ __forceinline__ void nbar_arrive() {
-  asm volatile("bar.arrive %0, %1;" ::"n"(kId), "n"(kDecThreads) : "memory");
-}
-__device__ __forceinline__ void nbar_sync2(int base, int b) {   // base + b, b in {0, 1}
-  if (base == kBarFull) {
-    if (b) nbar_sync<kBarFull + 1>(); else nbar_sync<kBarFull>();
-  } else {
-    if (b) nbar_sync<kBarEmpty + 1>(); else nbar_sync<kBarEmpty>();
-  }
-}
-__device__ __forceinline__ void nbar_arrive2(int base, int b) {
-  if (base == kBarFull) {
-    if (b) nbar_arrive<kBarFull + 1>(); else nbar_arrive<kBarFull>();
-  } else {
-    if (b) nbar_arrive<kBarEmpty + 1>(); else nbar_arrive<kBarEmpty>();
-  }
-}
-
-__device__ __forceinline__ void dec_release(uint64_t* empty_bar, int b) {
-#if HSZ_DEC_NAMED
-  (void)empty_bar;
-  __syncwarp();
-  nbar_arrive2(kBarEmpty, b);
-#else
-  (void)b;
-  mbar_arrive_warp(empty_bar);
-#endif
-}
 
 // the 32-lane exact decode of one tile's blocks (any width up to 64, any
 // outlier), reading the sections in place; calls f(local block, lane, bin,
@@ -1342,22 +942,9 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
     for (uint64_t t = blockIdx.x;; t += gridDim.x, ++i) {
       const int b = i & 1;
       const uint64_t tvn = prefetch_toff(in, t + gridDim.x);   // consumed next iteration
-#if HSZ_DEC_NAMED
-      if (i >= 2) nbar_sync2(kBarEmpty, b);                    // compute done with tile i-2
-      stage_tile(in, t, tv, S.in[b], &S.full[b]);
-      mbar_wait_parity(&S.full[b], (i >> 1) & 1u);             // the bytes landed
-      nbar_arrive2(kBarFull, b);
-      if (t >= ntiles) {
-        // consume the compute warps' release of the last real tile, so no
-        // named barrier is left with pending arrivals
-        if (i >= 1) nbar_sync2(kBarEmpty, b ^ 1);
-        break;
-      }
-#else
       if (i >= 2) mbar_wait_parity_sleep(&S.empty[b], ((i >> 1) - 1) & 1u);
       stage_tile(in, t, tv, S.in[b], &S.full[b]);
       if (t >= ntiles) break;
-#endif
       tv = tvn;
     }
     return;
@@ -1371,11 +958,7 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
   uint32_t i = 0;
   for (;; ++i) {
     const int b = i & 1;
-#if HSZ_DEC_NAMED
-    nbar_sync2(kBarFull, b);                      // blocks without issuing (no polling)
-#else
     mbar_wait_parity(&S.full[b], (i >> 1) & 1u);
-#endif
     const auto& it = S.in[b];
     const uint64_t cur = it.tile;
     if (cur >= ntiles) break;
@@ -1404,7 +987,7 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
       int64_t sp;
       uint64_t sp2;
       decode_sum<kMode == 1>(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, len, &sp, &sp2);
-      dec_release(&S.empty[b], b);          // staged bytes consumed
+      mbar_arrive_warp(&S.empty[b]);          // staged bytes consumed
       if (len > 0) {
         const __int128 oo = o;
         acc.s += oo * len + sp;
@@ -1418,11 +1001,11 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
     } else if (fast && HSZ_F32_STREAM) {
       decode_f32(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, o, len, fs.d, S.out + tid * 128,
                  static_cast<uint32_t>(tid & 7), fs.may_overflow, &flags);
-      dec_release(&S.empty[b], b);          // staged bytes consumed
+      mbar_arrive_warp(&S.empty[b]);          // staged bytes consumed
     } else if (fast) {
       int32_t q[K];
       decode_block(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, o, len, q);
-      dec_release(&S.empty[b], b);          // staged bytes consumed
+      mbar_arrive_warp(&S.empty[b]);          // staged bytes consumed
       if (kMode == 2) {
         // f32 values = RN32(RN64(2eps * bin)) (codec.py:107-115), into the
         // swizzled 128-byte row of this block
@@ -1484,7 +1067,7 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
           if (live) acc.add(q, kMode == 1);
         });
       }
-      dec_release(&S.empty[b], b);
+      mbar_arrive_warp(&S.empty[b]);
     }
     if (kMode == 2) {
       // one TMA tensor store of the whole tile (the stream's partial last

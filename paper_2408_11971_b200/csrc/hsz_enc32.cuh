@@ -443,35 +443,6 @@ constexpr int kThreadsC = kCompute + 32;
 #define HSZ_CMP_CTAS 5
 #endif
 
-// "staged tile -> placement warp" hand-off of the ring kernels (compress,
-// scalar_mul v3): named barriers 2..5, one per ring slot (HSZ_PLACE_NAMED),
-// so the otherwise idle placement warp blocks instead of polling.  The slot
-// hand-off alternates strictly (slot s is refilled only after the placement
-// warp released it on st_empty[s]).
-#ifndef HSZ_PLACE_NAMED
-#define HSZ_PLACE_NAMED 0
-#endif
-constexpr int kBarSlot = 2;
-
-__device__ __forceinline__ void slot_staged(uint64_t* st_full, int slot) {   // compute warps
-#if HSZ_PLACE_NAMED
-  (void)st_full;
-  __syncwarp();
-  nbar_arrive4<kBarSlot, kThreadsC>(slot);
-#else
-  mbar_arrive_warp(st_full);
-#endif
-}
-__device__ __forceinline__ void slot_wait(uint64_t* st_full, int slot, uint32_t parity) {  // placement warp
-#if HSZ_PLACE_NAMED
-  (void)st_full;
-  (void)parity;
-  nbar_sync4<kBarSlot, kThreadsC>(slot);
-#else
-  mbar_wait_parity_sleep(st_full, parity);
-#endif
-}
-
 struct Smem7 {
   unsigned char in[kBufBytes];      // input tile (TMA 128B swizzle; 1024-aligned)
   unsigned char ring[kRingBytes];   // staged payloads (row-XOR word swizzle per 128 B row)
@@ -519,7 +490,7 @@ __global__ void __launch_bounds__(kThreadsC, HSZ_CMP_CTAS)
     // =========================== placement warp ===========================
     for (uint32_t kk = 0;; ++kk) {
       const int slot = kk % kSlots;
-      slot_wait(&S.st_full[slot], slot, (kk / kSlots) & 1u);
+      mbar_wait_parity_sleep(&S.st_full[slot], (kk / kSlots) & 1u);
       const RingRec r = S.rec[slot];
       if (r.ts == kDone) break;
       if (r.ts != kSelfPlaced) {
@@ -579,7 +550,7 @@ __global__ void __launch_bounds__(kThreadsC, HSZ_CMP_CTAS)
         S.rec[slot].ts = kDone;
         S.rec[slot].end = head;
       }
-      slot_staged(&S.st_full[slot], slot);
+      mbar_arrive_warp(&S.st_full[slot]);
       break;
     }
     unsigned char* in = S.in;
@@ -693,7 +664,7 @@ __global__ void __launch_bounds__(kThreadsC, HSZ_CMP_CTAS)
       }
       if (sb) S.sgn[slot][es >> 2] = bswap32(bc.sg);
       pack_block(bc, wmax, ep >> 2, reinterpret_cast<uint32_t*>(S.ring + pos));
-      slot_staged(&S.st_full[slot], slot);
+      mbar_arrive_warp(&S.st_full[slot]);
     } else {
       // exact path: sizes and publish first; the tile then resolves and
       // places itself (the placement warp resolves the previous tiles)
@@ -709,7 +680,7 @@ __global__ void __launch_bounds__(kThreadsC, HSZ_CMP_CTAS)
         S.rec[slot].end = head;
         S.rec[slot].ts = kSelfPlaced;
       }
-      slot_staged(&S.st_full[slot], slot);
+      mbar_arrive_warp(&S.st_full[slot]);
       if (warp == 0) {
         uint64_t es, ep;
         resolve6(out, cur, epoch, ntiles, ts, tp, &es, &ep);
