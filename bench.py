@@ -65,6 +65,20 @@ def _traffic(config, op):
         return None
 
 
+def _issue(config, op):
+    """Issue-side numbers of `op`'s kernel from the committed ncu --set full
+    capture of this config (profiles/issue.json): thread-instructions per
+    element, issue-slot utilisation, IPC -- the ceiling this block format
+    actually runs into (tools/ncu_issue.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "issue.json")) as f:
+            v = json.load(f).get(f"config{config}", {}).get(op)
+        return {k: v[k] for k in ("thread_inst_per_element", "issue_slots_busy_pct", "ipc")} \
+            if v else None
+    except Exception:
+        return None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -547,6 +561,7 @@ def measure(args, config, world, rank, local, coll, light=False):
             "kernel_gbps_uncompressed": round(4.0 * n / (kern[op] * 1e-3) / 1e9, 2),
             "algorithmic_bytes": int(abytes[op]),
             "roofline_frac": round(abytes[op] / (kern[op] * 1e-3) / 1e9 / peak, 4),
+            "ncu_issue": _issue(config, op),
         }
     ops_json["minmax"] = {"kernel_ms": round(kern["minmax"], 4),
                           "algorithmic_bytes": int(abytes["minmax"]),
@@ -561,7 +576,8 @@ def measure(args, config, world, rank, local, coll, light=False):
                         "traffic": traffic,
                         "traffic_source": f"profiles/traffic.json config{config} (ncu --set full)"
                         if traffic is not None else None,
-                        "algorithmic_bytes": int(abytes[dom])}
+                        "algorithmic_bytes": int(abytes[dom]),
+                        "issue": _issue(config, dom)}
     del abytes
 
     # ---- e2e through the public API from pinned host memory
@@ -899,7 +915,7 @@ def main():
     ap.add_argument("--digest", action="store_true",
                     help="add digests of the whole-field streams / values (sharding check)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--ref-budget", type=float, default=150.0,
+    ap.add_argument("--ref-budget", type=float, default=200.0,
                     help="seconds of CPU work for the whole --impl reference run")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -357,20 +357,34 @@ __global__ void __launch_bounds__(kThreads) negate_kernel(
 }
 
 // ---- K5: scalar add (ops.py:112-118) -----------------------------------------
-__device__ __forceinline__ int32_t sadd1(int32_t o, int64_t rs, uint32_t& flags) {
-  // numpy int64 addition wraps; any wrapped or true sum outside int32 is
-  // rejected by the int32 guard, so the exact test is equivalent
-  const __int128 v = static_cast<__int128>(o) + rs;
-  if (v < INT32_MIN || v > INT32_MAX) flags |= HSZ_ERR_OUTLIER_OVERFLOW;
-  return static_cast<int32_t>(static_cast<int64_t>(v));
+// outlier + rs in int64 (numpy wraps), then the int32 guard (model.py:182-191).
+// A wrapped int64 sum can never land back inside int32 (|rs| < 2^63), so the
+// guard on the wrapped value is the exact test.  kSmall (rs fits int32): the
+// same result from a 32-bit add, overflow iff the operands agree in sign and
+// the sum does not -- 3 instructions an element instead of ~30 for the int128
+// form, which made this streaming kernel issue-bound.
+template <bool kSmall>
+__device__ __forceinline__ int32_t sadd1(int32_t o, int64_t rs, uint32_t& bad) {
+  if constexpr (kSmall) {
+    const int32_t r = static_cast<int32_t>(rs);
+    const int32_t v = static_cast<int32_t>(static_cast<uint32_t>(o) + static_cast<uint32_t>(r));
+    bad |= static_cast<uint32_t>((o ^ v) & (r ^ v));          // sign bit: signed overflow
+    return v;
+  } else {
+    const int64_t v = static_cast<int64_t>(static_cast<uint64_t>(static_cast<int64_t>(o)) +
+                                           static_cast<uint64_t>(rs));
+    bad |= (static_cast<uint64_t>(v) + 0x80000000ull) > 0xFFFFFFFFull ? 0x80000000u : 0u;
+    return static_cast<int32_t>(v);
+  }
 }
 
+template <bool kSmall>
 __global__ void __launch_bounds__(kStreamThreads) sadd_kernel(const int32_t* oin, int32_t* oout,
                                                               uint64_t nblocks, int64_t rs,
                                                               uint32_t* err) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  uint32_t flags = 0;
+  uint32_t bad = 0;
   const bool vec = ((reinterpret_cast<uintptr_t>(oin) | reinterpret_cast<uintptr_t>(oout)) & 15u) == 0;
   const uint64_t nv = vec ? nblocks / 4 : 0;
   const int4* in4 = reinterpret_cast<const int4*>(oin);
@@ -387,12 +401,13 @@ __global__ void __launch_bounds__(kStreamThreads) sadd_kernel(const int32_t* oin
     for (int u = 0; u < kStreamU; ++u) {
       const uint64_t c = c0 + u * stride;
       if (c < nv)
-        out4[c] = make_int4(sadd1(v[u].x, rs, flags), sadd1(v[u].y, rs, flags),
-                            sadd1(v[u].z, rs, flags), sadd1(v[u].w, rs, flags));
+        out4[c] = make_int4(sadd1<kSmall>(v[u].x, rs, bad), sadd1<kSmall>(v[u].y, rs, bad),
+                            sadd1<kSmall>(v[u].z, rs, bad), sadd1<kSmall>(v[u].w, rs, bad));
     }
   }
-  for (uint64_t j = nv * 4 + tid; j < nblocks; j += stride) oout[j] = sadd1(oin[j], rs, flags);
-  if (flags) atomicOr(err, flags);
+  for (uint64_t j = nv * 4 + tid; j < nblocks; j += stride) oout[j] = sadd1<kSmall>(oin[j], rs, bad);
+  if (__any_sync(kFull, (bad >> 31) != 0) && (threadIdx.x & 31) == 0)
+    atomicOr(err, HSZ_ERR_OUTLIER_OVERFLOW);
 }
 
 }  // namespace ops
@@ -1051,7 +1066,11 @@ int hsz_scalar_add(const int32_t* oin, int32_t* oout, uint64_t nblocks, int64_t 
   if (!oin || !oout || !err || nblocks == 0) return HSZ_EINVAL;
   const unsigned g = static_cast<unsigned>(
       grid_for(nblocks, 4 * ops::kStreamU, ops::kStreamThreads, stream_wave()));
-  ops::sadd_kernel<<<g, ops::kStreamThreads, 0, static_cast<cudaStream_t>(stream)>>>(oin, oout, nblocks, rs, err);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (rs >= INT32_MIN && rs <= INT32_MAX)
+    ops::sadd_kernel<true><<<g, ops::kStreamThreads, 0, st>>>(oin, oout, nblocks, rs, err);
+  else
+    ops::sadd_kernel<false><<<g, ops::kStreamThreads, 0, st>>>(oin, oout, nblocks, rs, err);
   return launch_status();
 }
 
