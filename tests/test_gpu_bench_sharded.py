@@ -52,3 +52,28 @@ def test_config5_two_ranks_equal_one():
     assert d1["config"]["global_elements"] == d2["config"]["global_elements"] == 1 << 33
     assert d2["config"]["elements_per_gpu"] == 1 << 32
     assert d1["digests"] == d2["digests"]
+
+
+def test_config5_nccl_collectives_world1():
+    """The NCCL code paths of C1-C3 (device tensors, all_reduce MIN /
+    all_gather / all_reduce SUM on a real NCCL communicator) under torchrun
+    with one rank: same digests as the plain single-GPU run (the pool has
+    one GPU per box, so this is the NCCL world this machine can form)."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    args = ["bench.py", "--config", "5", "--quick", "--steps", "1", "--warmup", "1"]
+    one = subprocess.run([sys.executable] + args, cwd=ROOT, capture_output=True, text=True,
+                         timeout=900)
+    assert one.returncode == 0, one.stderr[-3000:]
+    env = dict(os.environ, HSZ_FORCE_COLL="1")
+    nccl = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                           "--nproc-per-node", "1", "--master-addr", "127.0.0.1",
+                           "--master-port", str(_free_port())] + args,
+                          cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert nccl.returncode == 0, nccl.stderr[-3000:]
+    d1, dn = _line(one.stdout), _line(nccl.stdout)
+    assert "nccl" in dn["config"]["parallelism"]
+    assert d1["digests"] == dn["digests"]
+
