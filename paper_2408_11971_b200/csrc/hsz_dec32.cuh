@@ -811,12 +811,21 @@ constexpr uint32_t kSmulSmemBytes = recode_smem_bytes<kOpSmul>();
 #define HSZ_SUM_CTAS 8
 #endif
 
+// staged input tiles in flight per CTA (the moment kernels hold 8 KB of
+// payload per tile: 3 buffers still fit 8 CTAs per SM)
+#ifndef HSZ_SUM_NBUF
+#define HSZ_SUM_NBUF 2
+#endif
+#ifndef HSZ_F32_NBUF
+#define HSZ_F32_NBUF 2
+#endif
 template <int kMode>
 struct DecSmem {
+  static constexpr int kNB = kMode == 2 ? HSZ_F32_NBUF : HSZ_SUM_NBUF;
   using Tile = InTileT<kMode == 2 ? HSZ_F32_PAYCAP : HSZ_SUM_PAYCAP>;
-  Tile in[2];
+  Tile in[kNB];
   alignas(1024) unsigned char out[kMode == 2 ? e32::kBufBytes : 16];   // decompress: value tile
-  uint64_t full[2], empty[2];
+  uint64_t full[kNB], empty[kNB];
   uint32_t scan[4];
 };
 template <int kMode>
@@ -927,8 +936,9 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
   DecSmem<kMode>& S = *reinterpret_cast<DecSmem<kMode>*>(smraw + (((a0 + 1023u) & ~1023u) - a0));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t ntiles = in.ntiles, nblocks = in.nblocks;
+  constexpr int kNB = DecSmem<kMode>::kNB;
   if (tid == kCompute) {
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kNB; ++b) {
       mbar_init(&S.full[b], 1);
       mbar_init(&S.empty[b], kCompute / 32);
     }
@@ -940,9 +950,9 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
     uint32_t i = 0;
     uint64_t tv = prefetch_toff(in, blockIdx.x);
     for (uint64_t t = blockIdx.x;; t += gridDim.x, ++i) {
-      const int b = i & 1;
+      const int b = i % kNB;
       const uint64_t tvn = prefetch_toff(in, t + gridDim.x);   // consumed next iteration
-      if (i >= 2) mbar_wait_parity_sleep(&S.empty[b], ((i >> 1) - 1) & 1u);
+      if (i >= kNB) mbar_wait_parity_sleep(&S.empty[b], ((i / kNB) - 1) & 1u);
       stage_tile(in, t, tv, S.in[b], &S.full[b]);
       if (t >= ntiles) break;
       tv = tvn;
@@ -957,8 +967,8 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
   acc.q2 = 0;
   uint32_t i = 0;
   for (;; ++i) {
-    const int b = i & 1;
-    mbar_wait_parity(&S.full[b], (i >> 1) & 1u);
+    const int b = i % kNB;
+    mbar_wait_parity(&S.full[b], (i / kNB) & 1u);
     const auto& it = S.in[b];
     const uint64_t cur = it.tile;
     if (cur >= ntiles) break;
