@@ -457,23 +457,25 @@ struct SrcSmulExact {
   }
 };
 
-// element-wise: bin_a (+|-) bin_b modulo 2^64 -- the fallback encoder's
-// residuals are then the operands' residual sums (ops.py:171-176)
+// element-wise: residual_a (+|-) residual_b exactly in 128 bits, outliers
+// o_a (+|-) o_b -- the reference's residual-domain fold (ops.py:163-182): no
+// bins are formed, so operands of any width up to 64 combine exactly (a
+// combined magnitude of 2^64 or more is flagged, where the reference's
+// uint64 conversion fails)
 template <int kOp>
 struct SrcEwExact {
+  static constexpr bool kResid = true;
   StreamIn a, b;
   const RecodeSmem<kOp>* S;
-  __device__ __forceinline__ int64_t lane_bin(int lb, int lane, int len, uint32_t* flags) {
-    uint32_t f = 0;
-    const int64_t qa = k32::decode_lane(a.signs, a.payload, S->in.w[lb], S->in.o[lb],
-                                        S->in.gs0 + S->bes[lb], S->in.gp0 + S->bep[lb], len, lane, &f);
-    const int64_t qb = k32::decode_lane(b.signs, b.payload, S->in2.w[lb], S->in2.o[lb],
-                                        S->in2.gs0 + S->bes2[lb], S->in2.gp0 + S->bep2[lb], len,
-                                        lane, &f);
-    *flags |= f;
-    if (f || lane >= len) return 0;
-    const uint64_t ua = static_cast<uint64_t>(qa), ub = static_cast<uint64_t>(qb);
-    return static_cast<int64_t>(kOp == kOpSub ? ua - ub : ua + ub);
+  __device__ __forceinline__ __int128 lane_resid(int lb, int lane, int len, uint32_t* flags) {
+    (void)flags;
+    const __int128 ra = k32::decode_lane_resid(a.signs, a.payload, S->in.w[lb], S->in.o[lb],
+                                               S->in.gs0 + S->bes[lb], S->in.gp0 + S->bep[lb], len,
+                                               lane);
+    const __int128 rb = k32::decode_lane_resid(b.signs, b.payload, S->in2.w[lb], S->in2.o[lb],
+                                               S->in2.gs0 + S->bes2[lb], S->in2.gp0 + S->bep2[lb],
+                                               len, lane);
+    return kOp == kOpSub ? ra - rb : ra + rb;
   }
 };
 

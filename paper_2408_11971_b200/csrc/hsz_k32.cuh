@@ -280,6 +280,64 @@ __device__ __forceinline__ int64_t decode_lane(const unsigned char* sgn, const u
   return static_cast<int64_t>(r);
 }
 
+// the lane's signed residual (lane 0: the outlier; 0 past len) without the
+// prefix sum -- the residual-domain element-wise ops combine streams here
+// (ops.py:163-182), so operands whose BINS would leave int64 (widths 62-64)
+// are combined exactly, like the reference's Python-int path
+__device__ __forceinline__ __int128 decode_lane_resid(const unsigned char* sgn,
+                                                      const unsigned char* pay, uint32_t w,
+                                                      int64_t o, uint64_t soff, uint64_t poff,
+                                                      int len, int lane) {
+  if (lane == 0) return o;
+  if (w == 0 || lane >= len) return 0;
+  const uint32_t sw = bswap32(*reinterpret_cast<const uint32_t*>(sgn + soff));
+  const bool neg = (__brev(sw) >> lane) & 1u;
+  const uint32_t* pw = reinterpret_cast<const uint32_t*>(pay + poff);
+  const uint32_t start = lane * w;
+  const uint32_t a = start >> 5, sh = start & 31;
+  const uint32_t w0 = bswap32(pw[a]);
+  const uint32_t w1 = bswap32(pw[a + 1]);
+  const uint32_t w2 = (sh + w > 64) ? bswap32(pw[a + 2]) : 0u;
+  const unsigned __int128 cat = (static_cast<unsigned __int128>(w0) << 64) |
+                                (static_cast<unsigned __int128>(w1) << 32) | w2;
+  const uint64_t mag = static_cast<uint64_t>((cat << (32 + sh)) >> (128 - w));
+  return neg ? -static_cast<__int128>(mag) : static_cast<__int128>(mag);
+}
+
+// sources that deliver residuals (lane_resid) instead of bins (lane_bin)
+template <class S, class = void>
+struct ResidSrc : std::false_type {};
+template <class S>
+struct ResidSrc<S, std::void_t<decltype(S::kResid)>> : std::bool_constant<S::kResid> {};
+
+// (first = outlier of the block, neg / mag = this lane's residual) from a
+// source of either kind; residual magnitudes of 2^64 or more are flagged
+template <class Src>
+__device__ __forceinline__ void lane_code(Src& src, int lb, int lane, int len, uint32_t* flags,
+                                          int64_t* first, bool* neg, uint64_t* mag) {
+  if constexpr (ResidSrc<Src>::value) {
+    const __int128 r = src.lane_resid(lb, lane, len, flags);
+    const uint64_t lo = static_cast<uint64_t>(r);
+    *first = static_cast<int64_t>(__shfl_sync(kFull, lo, 0));
+    *neg = false;
+    *mag = 0;
+    if (lane > 0 && lane < len) {
+      *neg = r < 0;
+      const unsigned __int128 u = *neg ? static_cast<unsigned __int128>(-r)
+                                       : static_cast<unsigned __int128>(r);
+      if (u >> 64) *flags |= HSZ_ERR_PREFIX_OVERFLOW;   // beyond the 64-bit field width
+      *mag = static_cast<uint64_t>(u);
+    }
+  } else {
+    const int64_t q = src.lane_bin(lb, lane, len, flags);
+    *first = __shfl_sync(kFull, q, 0);
+    const int64_t prev = __shfl_up_sync(kFull, q, 1);
+    *neg = false;
+    *mag = 0;
+    if (lane > 0 && lane < len) *mag = absdiff64(q, prev, neg);
+  }
+}
+
 // fallback helper: broadcast block j's metadata (held by lane j) to the warp
 struct LaneBlock {
   uint32_t w;
@@ -544,12 +602,10 @@ __device__ __noinline__ uint32_t fallback_sizes(Src src, EncodeOut out, uint64_t
     const uint64_t b = blk0 + j;
     if (b >= nblocks) break;
     const int len = (b == nblocks - 1) ? static_cast<int>(tail_len) : K;
-    const int64_t q = src.lane_bin(warp * BPW + j, lane, len, &flags);
-    const int64_t first = __shfl_sync(kFull, q, 0);
-    const int64_t prev = __shfl_up_sync(kFull, q, 1);
-    bool neg = false;
-    uint64_t mag = 0;
-    if (lane > 0 && lane < len) mag = absdiff64(q, prev, &neg);
+    int64_t first;
+    bool neg;
+    uint64_t mag;
+    lane_code(src, warp * BPW + j, lane, len, &flags, &first, &neg, &mag);
     const int wl = mag ? 64 - __clzll(static_cast<long long>(mag)) : 0;
     const int w = __reduce_max_sync(kFull, wl);
     if (lane == j) {
@@ -582,11 +638,11 @@ __device__ __noinline__ void fallback_pack(Src src, EncodeOut out, uint64_t tile
     if (b >= nblocks) break;
     const int len = (b == nblocks - 1) ? static_cast<int>(tail_len) : K;
     uint32_t f = 0;
-    const int64_t q = src.lane_bin(warp * BPW + j, lane, len, &f);
-    const int64_t prev = __shfl_up_sync(kFull, q, 1);
-    bool neg = false;
-    uint64_t mag = 0;
-    if (lane > 0 && lane < len) mag = absdiff64(q, prev, &neg);
+    int64_t first;
+    bool neg;
+    uint64_t mag;
+    lane_code(src, warp * BPW + j, lane, len, &f, &first, &neg, &mag);
+    (void)first;
     const unsigned sbits = __ballot_sync(kFull, neg);
     const int wl = mag ? 64 - __clzll(static_cast<long long>(mag)) : 0;
     const int w = __reduce_max_sync(kFull, wl);

@@ -148,3 +148,39 @@ def test_bivariate_device_resident(H):
     assert H.covariance(sa, sb) == O.covariance(oa, ob)
     assert H.ssim_global(sa, sb) == O.ssim_global(oa, ob)
     assert H.block_means(sa).cpu().numpy().tobytes() == O.block_means(oa).tobytes()
+
+
+def _wide_bins(case, n, rng):
+    """Operand bins whose residuals are ~2^63 (widths 63-64): their BIN sums
+    leave int64, their residual sums do not fit 63 bits."""
+    A = (1 << 62) - 1
+    a = np.where(np.arange(n) % 2 == 0, A, -A).astype(np.int64)
+    a[::32] = rng.integers(-1000, 1000, a[::32].size)
+    if case == "self":
+        b = a.copy()                      # residual sums ~2^64 - 4: width 64
+    elif case == "neg":
+        b = -a                            # everything cancels: width 0
+    else:
+        b = a.copy()
+        b[1::2] = rng.integers(-(1 << 40), 1 << 40, b[1::2].size)
+    return a, b
+
+
+@pytest.mark.parametrize("case", ["self", "neg", "mixed"])
+@pytest.mark.parametrize("sub", [False, True])
+def test_elementwise_wide_operands_residual_domain(H, case, sub):
+    """the element-wise exact path combines RESIDUALS (128-bit),
+    like the reference (ops.py:163-182, Python ints past int64), instead of
+    bins modulo 2^64 -- operands of width 62-64 give the reference's stream,
+    not a spurious QuantOverflow or a wrapped sign."""
+    rng = np.random.default_rng(7)
+    n = 32 * 4 * 3 + 5
+    a, b = _wide_bins(case, n, rng)
+    if sub:
+        b = -b
+    oa = O.encode_bins(a, 0.5, (n,), 32, "f32")
+    ob = O.encode_bins(b, 0.5, (n,), 32, "f32")
+    want = O.elementwise_sub(oa, ob) if sub else O.elementwise_add(oa, ob)
+    ha, hb = H.deserialize(O.serialize(oa)), H.deserialize(O.serialize(ob))
+    got = H.elementwise_sub(ha, hb) if sub else H.elementwise_add(ha, hb)
+    assert H.serialize(got) == O.serialize(want)
