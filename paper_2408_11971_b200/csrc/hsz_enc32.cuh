@@ -192,24 +192,6 @@ __device__ __forceinline__ uint32_t cta_scan(uint32_t v, uint32_t* s_scan, uint3
   return pre + inc - v;
 }
 
-// cta_scan fused with an OR-reduction of `p` in the same barrier (bar.red.or)
-__device__ __forceinline__ uint32_t cta_scan_or(uint32_t v, uint32_t* s_scan, uint32_t* total,
-                                                bool p, bool* any) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t inc = v;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t o = __shfl_up_sync(kFull, inc, d);
-    if (lane >= d) inc += o;
-  }
-  if (lane == 31) s_scan[warp] = inc;
-  *any = bar_or_compute(p);
-  const uint32_t a0 = s_scan[0], a1 = s_scan[1], a2 = s_scan[2], a3 = s_scan[3];
-  const uint32_t pre = (warp > 0 ? a0 : 0u) + (warp > 1 ? a1 : 0u) + (warp > 2 ? a2 : 0u);
-  *total = a0 + a1 + a2 + a3;
-  return pre + inc - v;
-}
-
 // ---------------------------------------------------------------------------
 // per-thread block encoding
 
@@ -474,18 +456,10 @@ struct Smem7 {
   uint64_t epoch;
   uint32_t alloc_off;
   uint32_t scan[4];
-  uint32_t scan2[2][4];             // HSZ_CMP_FUSED: by tile parity (no barrier between tiles)
   uint32_t wsb[4], wpb[4];
   uint32_t xscratch[4][64];         // exact path: one block's packed words per warp
 };
 constexpr uint32_t kSmem7Bytes = sizeof(Smem7) + 1024;
-
-// HSZ_CMP_FUSED: the "wide tile" decision rides on the sizes scan's barrier
-// (one CTA barrier per tile instead of two); the next tile's TMA load is
-// issued after that barrier
-#ifndef HSZ_CMP_FUSED
-#define HSZ_CMP_FUSED 0
-#endif
 
 template <bool kTma>
 __global__ void __launch_bounds__(kThreadsC, HSZ_CMP_CTAS)
@@ -637,7 +611,6 @@ __global__ void __launch_bounds__(kThreadsC, HSZ_CMP_CTAS)
 #pragma unroll
         for (int i = 0; i < K; ++i) qb[i] = *reinterpret_cast<const uint32_t*>(in + swz_elem(tid, i));
       }
-#if !HSZ_CMP_FUSED
       wide = bar_or_compute(wide);    // ... and every read of the input buffer is done
       if (tid == kTmaThread) {        // refill it: the next tile's load overlaps this tile
         const uint64_t nx = ahead;
@@ -645,30 +618,11 @@ __global__ void __launch_bounds__(kThreadsC, HSZ_CMP_CTAS)
         issue(nx);
         if (nx < ntiles) ahead = draw_raw();
       }
-#endif
     }
-    const uint64_t gb = cur * TB + tid;
-    const bool active = gb < nblocks;
-    const int len = !active ? 0 : (gb == nblocks - 1 ? static_cast<int>(tail_len) : K);
-#if HSZ_CMP_FUSED
-    BlockCode bc;
-    block_code(qb, len, bc);           // garbage on a wide tile: not used then
-    const uint32_t wmax = __reduce_max_sync(kFull, bc.w);
-    const uint32_t sb = (bc.w && active) ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
-    const uint32_t pb = (static_cast<uint32_t>(len) * bc.w + 7u) >> 3;
-    uint32_t tot;
-    bool wide_any;
-    const uint32_t ex = cta_scan_or(sb | (pb << 10), S.scan2[k & 1u], &tot, wide, &wide_any);
-    wide = wide_any;                   // ... and every read of the input buffer is done
-    if (tid == kTmaThread) {
-      const uint64_t nx = ahead;
-      consume(nx);
-      issue(nx);
-      if (nx < ntiles) ahead = draw_raw();
-    }
-#endif
     if (!wide) {
-#if !HSZ_CMP_FUSED
+      const uint64_t gb = cur * TB + tid;
+      const bool active = gb < nblocks;
+      const int len = !active ? 0 : (gb == nblocks - 1 ? static_cast<int>(tail_len) : K);
       BlockCode bc;
       block_code(qb, len, bc);
       const uint32_t wmax = __reduce_max_sync(kFull, bc.w);
@@ -676,7 +630,6 @@ __global__ void __launch_bounds__(kThreadsC, HSZ_CMP_CTAS)
       const uint32_t pb = (static_cast<uint32_t>(len) * bc.w + 7u) >> 3;
       uint32_t tot;
       const uint32_t ex = cta_scan(sb | (pb << 10), S.scan, &tot);   // sb <= 512, pb <= 15872
-#endif
       const uint32_t es = ex & 1023u, ep = ex >> 10;
       const uint32_t ts = tot & 1023u, tp = tot >> 10;
       if (tid == 0) lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
