@@ -545,6 +545,28 @@ static bool make_rows_map_f32_uncached(const float* x, uint64_t n, CUtensorMap* 
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D tensor map over int64 bins viewed as [half][block][16 bins] (dims
+// reordered: the block stride is 256 B, the half stride 128 B), 128-row boxes
+// of both halves, 128-byte swizzle -- the staged image puts block r's two
+// 128-byte rows at r and 128 + r, so the swizzle spreads a wavefront's 8
+// threads over 8 bank groups (e32::bins_off)
+static bool make_bins_map(const int64_t* b, uint64_t n, CUtensorMap* map) {
+  std::memset(map, 0, sizeof(*map));
+  const uint64_t rows = n / 32;
+  if ((reinterpret_cast<uintptr_t>(b) & 15u) != 0 || rows < static_cast<uint64_t>(kTileBlocks) ||
+      rows >= (1ull << 31))
+    return false;
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {16, rows, 2};
+  cuuint64_t strides[2] = {256, 128};
+  cuuint32_t box[3] = {16, static_cast<cuuint32_t>(kTileBlocks), 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, const_cast<int64_t*>(b), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int kMode>
 static int launch_decode_pipe(const d32::StreamIn& in, float* out, double d, uint64_t* mout,
                               void* ws, uint32_t* err, cudaStream_t st, Mailbox mb = Mailbox{nullptr, 0}) {
@@ -601,8 +623,41 @@ static int launch_compress_f32(const float* x, uint64_t n, const QuantConst& c,
   }
   const uint64_t grid = nt < static_cast<uint64_t>(resident[tma]) ? nt : static_cast<uint64_t>(resident[tma]);
   kern<<<static_cast<unsigned>(grid), e32::kThreadsC, smem, st>>>(map, x, n, qf, c, out, nb, nt,
-                                                                tail_len_of(n, 32));
+                                                                tail_len_of(n, 32), nullptr);
   return launch_status();
+}
+
+// encode_from_quant, block_len 32: the compressor's register-resident
+// encoder fed by a 3-D TMA tile of int64 bins; false if the bins do not allow
+// the tensor map (the caller then takes the first-generation encoder)
+static bool launch_encode_bins32(const int64_t* bins, uint64_t n, const k32::EncodeOut& out,
+                                 cudaStream_t st, int* rc) {
+  CUtensorMap map;
+  if (!make_bins_map(bins, n, &map)) return false;
+  const uint64_t nb = ceil_div(n, 32);
+  const uint64_t nt = ceil_div(nb, kTileBlocks);
+  constexpr int smem = static_cast<int>(e32::kSmem7BinsBytes);
+  auto kern = e32::compress_f32_kernel<true, true>;
+  static int resident = 0, resident_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (resident_dev != dev) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, e32::kThreadsC, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    resident = (per_sm > 0 ? per_sm : 1) * sms;
+    resident_dev = dev;
+  }
+  const uint64_t grid = nt < static_cast<uint64_t>(resident) ? nt : static_cast<uint64_t>(resident);
+  const e32::QuantF32 qf{0.f, 0.f, -1.f};
+  const QuantConst qc = make_quant_const(1.0);
+  kern<<<static_cast<unsigned>(grid), e32::kThreadsC, smem, st>>>(map, nullptr, n, qf, qc, out, nb, nt,
+                                                                tail_len_of(n, 32), bins);
+  *rc = launch_status();
+  return true;
 }
 
 template <class G>
@@ -712,6 +767,10 @@ static int launch_recode(const d32::StreamIn& a, const d32::StreamIn& b, const d
   kern<<<static_cast<unsigned>(grid), e32::kThreadsWS, smem, st>>>(a, b, sp, out);
   return launch_status();
 }
+
+#ifndef HSZ_BINS_REGISTER_PATH
+#define HSZ_BINS_REGISTER_PATH 1
+#endif
 
 namespace hsz {
 namespace ops {
@@ -926,6 +985,10 @@ int hsz_encode_bins(const int64_t* bins, uint64_t n, uint32_t k, uint8_t* widths
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (k == 32) {
     const k32::EncodeOut out{widths, outliers, signs, sign_cap, payload, payload_cap, toff, err, ws};
+#if HSZ_BINS_REGISTER_PATH
+    int rc = HSZ_OK;
+    if (launch_encode_bins32(bins, n, out, st, &rc)) return rc;
+#endif
     return launch_encode32(k32::SrcBins{bins, n}, out, n, st);
   }
   return launch_encode_generic(gen::GBins{bins}, n, k, widths, outliers, signs, sign_cap, payload,

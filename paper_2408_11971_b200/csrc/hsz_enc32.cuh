@@ -443,8 +443,9 @@ constexpr int kThreadsC = kCompute + 32;
 #define HSZ_CMP_CTAS 5
 #endif
 
-struct Smem7 {
-  unsigned char in[kBufBytes];      // input tile (TMA 128B swizzle; 1024-aligned)
+template <uint32_t kInBytes>
+struct Smem7T {
+  unsigned char in[kInBytes];       // input tile (TMA 128B swizzle; 1024-aligned)
   unsigned char ring[kRingBytes];   // staged payloads (row-XOR word swizzle per 128 B row)
   alignas(16) uint32_t sgn[kSlots][TB];
   uint64_t full;
@@ -459,16 +460,59 @@ struct Smem7 {
   uint32_t wsb[4], wpb[4];
   uint32_t xscratch[4][64];         // exact path: one block's packed words per warp
 };
+using Smem7 = Smem7T<kBufBytes>;
 constexpr uint32_t kSmem7Bytes = sizeof(Smem7) + 1024;
+// encode_from_quant: an int64 bin tile is 32 KB
+using Smem7Bins = Smem7T<2 * kBufBytes>;
+constexpr uint32_t kSmem7BinsBytes = sizeof(Smem7Bins) + 1024;
+#ifndef HSZ_BINS_CTAS
+#define HSZ_BINS_CTAS 4
+#endif
 
-template <bool kTma>
-__global__ void __launch_bounds__(kThreadsC, HSZ_CMP_CTAS)
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <class Src>
+__device__ __forceinline__ Src make_exact_src(const float* x, const int64_t* xb, uint64_t n,
+                                              const QuantConst& qc, uint64_t tile) {
+  if constexpr (std::is_same_v<Src, k32::SrcBins>) {
+    (void)x;
+    (void)qc;
+    return k32::SrcBins{xb, n, tile};
+  } else {
+    (void)xb;
+    return Src{x, n, qc, tile};
+  }
+}
+
+// byte offset of bin i of tile block r in the staged int64 tile: the TMA
+// view is [half][block][16 bins] (3-D map, dims reordered), 128-byte rows
+// swizzled by (row & 7) = (block & 7), so the 8 threads of a wavefront read
+// 8 distinct bank groups
+__device__ __forceinline__ uint32_t bins_off(uint32_t r, uint32_t i) {
+  const uint32_t h = i >> 4, e = i & 15u;
+  return (h * TB + r) * 128u + ((((e >> 1) ^ (r & 7u)) << 4) | ((e & 1u) << 3));
+}
+
+// kBins = false: compress of a float32 field (codec.py:495-498);
+// kBins = true:  encode_from_quant of int64 bins (codec.py:523-525) -- the
+// same encoder with the bins staged by a 3-D TMA load instead of quantized
+template <bool kTma, bool kBins = false>
+__global__ void __launch_bounds__(kThreadsC, kBins ? HSZ_BINS_CTAS : HSZ_CMP_CTAS)
     compress_f32_kernel(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ x,
                         uint64_t n, QuantF32 qf, QuantConst qc, k32::EncodeOut out,
-                        uint64_t nblocks, uint64_t ntiles, uint32_t tail_len) {
+                        uint64_t nblocks, uint64_t ntiles, uint32_t tail_len,
+                        const int64_t* __restrict__ xb = nullptr) {
+  using SM = std::conditional_t<kBins, Smem7Bins, Smem7>;
   extern __shared__ unsigned char smraw[];
   const uint32_t a0 = smem_u32(smraw);
-  Smem7& S = *reinterpret_cast<Smem7*>(smraw + (((a0 + 1023u) & ~1023u) - a0));
+  SM& S = *reinterpret_cast<SM*>(smraw + (((a0 + 1023u) & ~1023u) - a0));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   LookbackWs lw = LookbackWs::bind(out.ws, ntiles);
   const uint64_t last_draw = ntiles + gridDim.x - 1;   // every CTA draws once past the end
@@ -521,8 +565,13 @@ __global__ void __launch_bounds__(kThreadsC, HSZ_CMP_CTAS)
     S.cur = t;
     if (t < ntiles && kTma) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect_tx(&S.full, kBufBytes);
-      tma_load_2d(S.in, &tmap, 0, static_cast<int>(t * TB), &S.full);
+      if constexpr (kBins) {
+        mbar_arrive_expect_tx(&S.full, 2 * kBufBytes);
+        tma_load_3d(S.in, &tmap, 0, static_cast<int>(t * TB), 0, &S.full);
+      } else {
+        mbar_arrive_expect_tx(&S.full, kBufBytes);
+        tma_load_2d(S.in, &tmap, 0, static_cast<int>(t * TB), &S.full);
+      }
     } else {
       mbar_arrive(&S.full);
     }
@@ -562,11 +611,19 @@ __global__ void __launch_bounds__(kThreadsC, HSZ_CMP_CTAS)
       if ((n % K) != 0 && full_rows >= row0 && full_rows < row0 + TB) {
         if (tid < K) {
           const uint32_t r = static_cast<uint32_t>(n % K);
-          const float v = static_cast<uint32_t>(tid) < r ? x[full_rows * K + tid] : 0.0f;
-          *reinterpret_cast<float*>(in + swz_elem(static_cast<uint32_t>(full_rows - row0), tid)) = v;
+          const uint32_t rr = static_cast<uint32_t>(full_rows - row0);
+          if constexpr (kBins) {
+            const int64_t v = static_cast<uint32_t>(tid) < r ? xb[full_rows * K + tid] : 0;
+            *reinterpret_cast<int64_t*>(in + bins_off(rr, tid)) = v;
+          } else {
+            const float v = static_cast<uint32_t>(tid) < r ? x[full_rows * K + tid] : 0.0f;
+            *reinterpret_cast<float*>(in + swz_elem(rr, tid)) = v;
+          }
         }
         bar_sync_n(1, kCompute);
       }
+    } else if constexpr (kBins) {
+      __trap();                        // the host launches the bins variant with TMA only
     } else {
       const uint64_t e0 = row0 * K;
       for (uint32_t i = tid; i < TB * K; i += kCompute) {
@@ -576,6 +633,29 @@ __global__ void __launch_bounds__(kThreadsC, HSZ_CMP_CTAS)
       }
       bar_sync_n(1, kCompute);
     }
+    if constexpr (kBins) {
+      // ---- this thread's 32 bins: the register path needs |bin| < 2^30 ------
+      bool big = false;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(
+              in + (h * TB + tid) * 128 + ((j ^ (tid & 7)) << 4));
+          big |= (v.x + static_cast<uint64_t>(kWide) >= 2ull * kWide) |
+                 (v.y + static_cast<uint64_t>(kWide) >= 2ull * kWide);
+          qb[16 * h + 2 * j] = static_cast<uint32_t>(v.x) + kMagicBits;
+          qb[16 * h + 2 * j + 1] = static_cast<uint32_t>(v.y) + kMagicBits;
+        }
+      }
+      wide = bar_or_compute(big);     // ... and every read of the input buffer is done
+      if (tid == kTmaThread) {        // refill it: the next tile's load overlaps this tile
+        const uint64_t nx = ahead;
+        consume(nx);
+        issue(nx);
+        if (nx < ntiles) ahead = draw_raw();
+      }
+    } else
     // ---- quantize this thread's row ----------------------------------------
     {
       const unsigned char* row = in + tid * 128;
@@ -668,7 +748,8 @@ __global__ void __launch_bounds__(kThreadsC, HSZ_CMP_CTAS)
     } else {
       // exact path: sizes and publish first; the tile then resolves and
       // places itself (the placement warp resolves the previous tiles)
-      k32::SrcQuant<float> src{x, n, qc, cur};
+      using Src = std::conditional_t<kBins, k32::SrcBins, k32::SrcQuant<float>>;
+      Src src = make_exact_src<Src>(x, xb, n, qc, cur);
       flags |= k32::fallback_sizes(src, out, cur, nblocks, tail_len, S.wsb, S.wpb);
       bar_sync_n(1, kCompute);
       const uint32_t ts = S.wsb[0] + S.wsb[1] + S.wsb[2] + S.wsb[3];

@@ -236,3 +236,35 @@ def test_prefetch_totals_matches_fetch(H):
         d._totals = None
         d.prefetch_totals()
     assert first.totals() == want[0] and d.totals() == want[1]
+
+
+@pytest.mark.parametrize("n,kind", [(4096, "small"), (4096 * 3 + 17, "small"), (4096 * 64 + 31, "edge"),
+                                    (4096 * 40 + 5, "mixed"), (32 * 5000, "huge"),
+                                    (4096 * 8, "tailless_wide")])
+def test_encode_from_quant_register_path(H, n, kind):
+    """encode_from_quant for block_len 32 runs on the compressor's register
+    encoder (int64 bin tiles by a 3-D TMA load); tiles holding a bin with
+    |bin| >= 2^30 take the exact path.  Bytes against the oracle's
+    encode_bins (codec.py:523-525), round trip through decode_to_quant."""
+    rng = np.random.default_rng(n)
+    if kind == "small":
+        bins = np.cumsum(rng.integers(-40, 41, n)).astype(np.int64)
+    elif kind == "edge":               # |bin| right at the register-path limit 2^30
+        bins = rng.integers(-(2 ** 30 - 1), 2 ** 30, n).astype(np.int64)
+        bins[rng.integers(0, n, 20)] = 2 ** 30 - 1
+        bins[rng.integers(0, n, 20)] = -(2 ** 30 - 1)
+    elif kind == "mixed":              # a few wide tiles among narrow ones
+        bins = rng.integers(-1000, 1000, n).astype(np.int64)
+        for t in (3, 17, 31):
+            bins[t * 4096 + 7] = 2 ** 30
+            bins[t * 4096 + 100] = -(2 ** 40)
+    elif kind == "huge":               # 62-bit bins: widths 63-64, the exact path everywhere
+        bins = rng.integers(-(2 ** 62), 2 ** 62, n).astype(np.int64)
+        bins[::32] = rng.integers(-1000, 1000, bins[::32].size)   # outliers stay int32
+    else:
+        bins = rng.integers(-(2 ** 31), 2 ** 31, n).astype(np.int64)
+    p = H.QuantParams(0.5, (n,), 32, "f32")
+    s = H.encode_from_quant(H.QuantArray(bins, p))
+    ref = O.encode_bins(bins, p.eps, p.dims, p.block_len, p.dtype)
+    assert H.serialize(s) == O.serialize(ref)
+    assert np.array_equal(H.decode_to_quant(s).bins, bins)
