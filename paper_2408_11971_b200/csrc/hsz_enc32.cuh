@@ -723,16 +723,21 @@ __global__ void __launch_bounds__(kThreadsC, kBins ? HSZ_BINS_CTAS : HSZ_CMP_CTA
       if (k >= kSlots) mbar_wait_parity(&S.st_empty[slot], ((k / kSlots) - 1) & 1u);
       const uint32_t need = (tp + 127u) & ~127u;
       uint32_t pos = static_cast<uint32_t>(head % kRingBytes);
+      const uint64_t prev_end = head;   // end of the last tile this CTA allocated
       if (pos + need > kRingBytes) {   // no wrap inside a tile: skip to the ring start
         head += kRingBytes - pos;
         pos = 0;
       }
-      if (head + need - S.ring_tail > kRingBytes) {
-        unsigned ns = 32;
-        while (head + need - S.ring_tail > kRingBytes) {
-          __nanosleep(ns);
-          ns = ns < 256 ? ns * 2 : 256;
-        }
+      // [head, head + need) must be free.  The skipped bytes belong to no tile,
+      // so ring_tail (the end of the last PLACED tile) never covers them: once
+      // every earlier tile is placed (tail == prev_end) the ring is empty and the
+      // tile fits -- without this test a skip of more than kRingBytes - need
+      // bytes (a small tile followed by a large one) waited forever.
+      for (unsigned ns = 32;;) {
+        const uint64_t tail = S.ring_tail;
+        if (tail >= prev_end || head + need - tail <= kRingBytes) break;
+        __nanosleep(ns);
+        ns = ns < 256 ? ns * 2 : 256;
       }
       head += need;
       if (tid == 0) {

@@ -268,3 +268,48 @@ def test_encode_from_quant_register_path(H, n, kind):
     ref = O.encode_bins(bins, p.eps, p.dims, p.block_len, p.dtype)
     assert H.serialize(s) == O.serialize(ref)
     assert np.array_equal(H.decode_to_quant(s).bins, bins)
+
+
+def _alternating_width_bins(n, w_small, w_big, seed):
+    """Bins whose tiles alternate between residual widths w_small and w_big:
+    residuals of exactly w bits with alternating signs, so |bin| stays below
+    1000 + 2^w."""
+    rng = np.random.default_rng(seed)
+    bins = np.empty(n, dtype=np.int64)
+    for t in range(-(-n // 4096)):
+        w = w_big if t % 2 else w_small
+        seg = bins[t * 4096:(t + 1) * 4096]
+        mag = rng.integers(2 ** (w - 1), 2 ** w, seg.size)
+        d = np.where(np.arange(seg.size) % 2 == 0, mag, -mag)
+        d[::32] = 0
+        seg[:] = rng.integers(-1000, 1000)
+        full = seg.size // 32 * 32
+        seg[:full].reshape(-1, 32)[:] += np.cumsum(d[:full].reshape(-1, 32), axis=1)
+        seg[full:] += np.cumsum(d[full:])
+    return bins
+
+
+@pytest.mark.parametrize("w_small,w_big", [(12, 24), (10, 27), (12, 21), (11, 22)])
+def test_encoder_ring_small_then_large_tile(H, w_small, w_big):
+    """Staging-ring regression: a CTA that packs a small tile and then a large
+    one skips the rest of its 16 KB ring; the skipped bytes belong to no tile,
+    and the free-space wait used to count them as occupied forever (a tile
+    followed by a larger one of more than the space left hung compress and
+    encode_from_quant: 128 * 4 * (w_small + w_big) > 16384).  Tiles alternate
+    between the two residual widths; bytes against the oracle for
+    encode_from_quant and, where float32 holds the bins exactly, compress."""
+    n = 4096 * 1600 + 11        # more tiles than resident CTAs: every CTA packs several
+    bins = _alternating_width_bins(n, w_small, w_big, w_small * 100 + w_big)
+    assert np.abs(bins).max() < 2 ** 30
+    p = H.QuantParams(0.5, (n,), 32, "f32")
+    ref = O.encode_bins(bins, p.eps, p.dims, p.block_len, p.dtype)
+    assert {w_small, w_big} <= set(int(v) for v in ref["widths"])
+    s = H.encode_from_quant(H.QuantArray(bins, p))
+    assert H.serialize(s) == O.serialize(ref)
+    if w_big <= 22:
+        # x = bin exactly (|bin| < 2^24); eps 0.5: floor((x + 0.5) / 1) = bin
+        x = bins.astype(np.float32)
+        assert np.array_equal(x.astype(np.int64), bins)
+        sc = H.compress(H.RawArray(x, (n,), "f32"), p)
+        assert H.serialize(sc) == O.serialize(O.compress(x, 0.5, (n,), 32, "f32"))
+        assert H.serialize(sc) == O.serialize(ref)
