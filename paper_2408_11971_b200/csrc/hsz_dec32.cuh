@@ -431,11 +431,17 @@ struct RecodeSmem {
   uint32_t agg_ts[2], agg_tp[2];
   uint64_t tile_of[2];
   uint64_t epoch;
+  // scalar_mul releases S.in right after the decode; a tile that then turns
+  // out to need the exact path (a rescaled bin beyond 2^30) re-decodes from
+  // global memory and finds its block headers here
+  uint64_t xgs0, xgp0;
+  int32_t xo[TB];
+  uint8_t xw[TB];
   // three scan buffers: the two operands' in-tile offset scans run back to
   // back with no barrier between the first one's reads and the second one's
   // writes, so they must not share one (a shared buffer let a fast warp
   // overwrite a total a slow warp had not read yet: wrong offsets)
-  uint32_t scan[4], scan_in[4], scan_in2[4];
+  alignas(16) uint32_t scan[4], scan_in[4], scan_in2[4];
   uint32_t wsb[4], wpb[4];
 };
 using SmulSmem = RecodeSmem<kOpSmul>;
@@ -449,8 +455,13 @@ struct SrcSmulExact {
   double d;
   __device__ __forceinline__ int64_t lane_bin(int lb, int lane, int len, uint32_t* flags) {
     uint32_t f = 0;
+#if HSZ_SCAN_OR >= 2
+    const int64_t q = k32::decode_lane(in.signs, in.payload, S->xw[lb], S->xo[lb],
+                                       S->xgs0 + S->bes[lb], S->xgp0 + S->bep[lb], len, lane, &f);
+#else
     const int64_t q = k32::decode_lane(in.signs, in.payload, S->in.w[lb], S->in.o[lb],
                                        S->in.gs0 + S->bes[lb], S->in.gp0 + S->bep[lb], len, lane, &f);
+#endif
     *flags |= f;
     if (f || lane >= len) return 0;
     return rescale1(product_rn(q, rs), d, flags);
@@ -542,6 +553,18 @@ __device__ __forceinline__ void block_offsets(uint32_t w, int len, uint32_t* sca
   const uint32_t iex = e32::cta_scan(isb | (ipb << 10), scan, &itot);
   *es = iex & 1023u;
   *ep = iex >> 10;
+}
+// ... with a CTA-wide OR of `flag` on the same barrier
+__device__ __forceinline__ bool block_offsets_or(uint32_t w, int len, bool flag, uint32_t* scan,
+                                                 uint32_t* es, uint32_t* ep) {
+  const uint32_t isb = w ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
+  const uint32_t ipb = (static_cast<uint32_t>(len) * w + 7u) >> 3;
+  uint32_t itot;
+  bool any;
+  const uint32_t iex = e32::cta_scan_or(isb | (ipb << 10), flag, scan, &itot, &any);
+  *es = iex & 1023u;
+  *ep = iex >> 10;
+  return any;
 }
 
 // Persistent, warp-specialised like the compressor: warps 0-3 decode +
@@ -652,11 +675,30 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
       flags |= HSZ_ERR_BAD_WIDTH;
       w = 0;
     }
+#if HSZ_SCAN_OR >= 2
+    if constexpr (!kTwo) {
+      S.xw[tid] = static_cast<uint8_t>(w);
+      S.xo[tid] = o;
+      if (tid == 0) {
+        S.xgs0 = S.in.gs0;
+        S.xgp0 = S.in.gp0;
+      }
+    }
+#endif
     uint32_t ies, iep;
-    block_offsets(w, len, S.scan_in, &ies, &iep);
+    bool fast_in = S.in.staged && w <= static_cast<uint32_t>(kFastW) && o > -(1 << 29) && o < (1 << 29);
+    bool exact;
+#if HSZ_SCAN_OR
+    if constexpr (!kTwo) {
+      // the CTA-uniform path choice rides on the offset scan's barrier
+      exact = block_offsets_or(w, len, !fast_in || !sp.small_rs, S.scan_in, &ies, &iep);
+    } else
+#endif
+    {
+      block_offsets(w, len, S.scan_in, &ies, &iep);
+    }
     S.bes[tid] = ies;
     S.bep[tid] = iep;
-    bool fast_in = S.in.staged && w <= static_cast<uint32_t>(kFastW) && o > -(1 << 29) && o < (1 << 29);
     uint32_t w2 = 0, ies2 = 0, iep2 = 0;
     int32_t o2 = 0;
     if constexpr (kTwo) {
@@ -666,20 +708,34 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
         flags |= HSZ_ERR_BAD_WIDTH;
         w2 = 0;
       }
-      block_offsets(w2, len, S.scan_in2, &ies2, &iep2);
-      S.bes2[tid] = ies2;
-      S.bep2[tid] = iep2;
       fast_in = fast_in && S.in2.staged && w2 <= static_cast<uint32_t>(kFastW) && o2 > -(1 << 29) &&
                 o2 < (1 << 29);
+#if HSZ_SCAN_OR
+      exact = block_offsets_or(w2, len, !fast_in, S.scan_in2, &ies2, &iep2);
+#else
+      block_offsets(w2, len, S.scan_in2, &ies2, &iep2);
+#endif
+      S.bes2[tid] = ies2;
+      S.bep2[tid] = iep2;
     }
     // CTA-uniform: the register decode is warp-collective (decode_block)
-    bool exact = e32::bar_or_compute(!fast_in || (kOp == kOpSmul && !sp.small_rs));
+#if !HSZ_SCAN_OR
+    exact = e32::bar_or_compute(!fast_in || (kOp == kOpSmul && !sp.small_rs));
+#endif
     trace_tile(cur, 2);
     uint32_t qb[K];
+    bool released = false;   // this warp's in_empty arrival of the tile is done
+    bool over = false;       // scalar_mul: a rescaled bin beyond the register path
     if (!exact) {
       int32_t q[K];
       decode_block<0, kTwo>(S.in.sgn + S.in.soff + ies, S.in.pay + S.in.poff + iep, w, o, len, q);
       if constexpr (kOp == kOpSmul) {
+#if HSZ_SCAN_OR >= 2
+        // this warp is done with the staged tile: the next one may load (a
+        // tile that still turns out exact re-decodes from the header copies)
+        mbar_arrive_warp(&S.in_empty);
+        released = true;
+#endif
         // rescale: |bin| < 2^30, |rs| < 2^23 -> bin * rs exact in float64;
         // then ops.py:199-208 verbatim
 #pragma unroll
@@ -694,7 +750,7 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
           // adding 2^52 rounding toward -inf leaves floor() in the low word
           const uint32_t mi = static_cast<uint32_t>(
               __double2loint(__dadd_rd(__dadd_rn(fabs(tt), 0.5), 4503599627370496.0)));
-          exact |= mi >= 1073741823u;
+          over |= mi >= 1073741823u;
           qb[i] = tt < 0.0 ? 0u - mi : mi;
         }
       } else {
@@ -706,13 +762,21 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
         for (int i = 0; i < K; ++i) qb[i] = static_cast<uint32_t>(q[i]);
       }
     }
-    if (kOp == kOpSmul) exact = e32::bar_or_compute(exact);   // ... every read of S.in's staged bytes is done
+#if HSZ_SCAN_OR < 2
+    if (kOp == kOpSmul) exact = e32::bar_or_compute(exact || over);   // ... every read of S.in's staged bytes is done
     else e32::bar_sync_n(1, kCompute);
+#endif
     trace_tile(cur, 3);
-    if (!exact) mbar_arrive_warp(&S.in_empty);
-    if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);
     uint32_t ts = 0, tp = 0;
+    bool do_exact = exact;   // CTA-uniform
     if (!exact) {
+      if (!released) {       // (per warp: in_empty counts warps, no CTA barrier needed)
+        mbar_arrive_warp(&S.in_empty);
+        released = true;
+      }
+#if HSZ_SCAN_OR < 2
+      if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);
+#endif
       e32::BlockCode bc;
       if constexpr (kTwo)
         e32::block_code_resid(qb, bc);   // qb already holds the outlier and residuals
@@ -721,26 +785,41 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
       const uint32_t wmax = __reduce_max_sync(kFull, bc.w);
       const uint32_t sb = (bc.w && active) ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
       const uint32_t pb = (static_cast<uint32_t>(len) * bc.w + 7u) >> 3;
-      uint32_t tot;
-      const uint32_t ex = e32::cta_scan(sb | (pb << 10), S.scan, &tot);
-      const uint32_t es = ex & 1023u, ep = ex >> 10;
-      ts = tot & 1023u;
-      tp = tot >> 10;
-      if (tid == 0) {
-        lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
-        S.agg_ts[par] = ts;
-        S.agg_tp[par] = tp;
-        S.tile_of[par] = cur;
+      uint32_t tot, ex;
+#if HSZ_SCAN_OR >= 2
+      if constexpr (kOp == kOpSmul) {
+        // the overflow report rides on the output scan's barrier
+        ex = e32::cta_scan_or(sb | (pb << 10), over, S.scan, &tot, &do_exact);
+      } else {
+        ex = e32::cta_scan(sb | (pb << 10), S.scan, &tot);
       }
-      if (active) {
-        out.widths[gb] = static_cast<uint8_t>(bc.w);
-        out.outliers[gb] = static_cast<int32_t>(qb[0]);
+      if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);
+#else
+      ex = e32::cta_scan(sb | (pb << 10), S.scan, &tot);
+#endif
+      if (!do_exact) {
+        const uint32_t es = ex & 1023u, ep = ex >> 10;
+        ts = tot & 1023u;
+        tp = tot >> 10;
+        if (tid == 0) {
+          lb_publish(lb_words(out.ws), cur, epoch, ts, tp);
+          S.agg_ts[par] = ts;
+          S.agg_tp[par] = tp;
+          S.tile_of[par] = cur;
+        }
+        if (active) {
+          out.widths[gb] = static_cast<uint8_t>(bc.w);
+          out.outliers[gb] = static_cast<int32_t>(qb[0]);
+        }
+        if (sb) S.sgn[par][es >> 2] = bswap32(bc.sg);
+        trace_tile(cur, 4);
+        e32::pack_block(bc, wmax, ep >> 2, reinterpret_cast<uint32_t*>(S.pk[par]));
+        trace_tile(cur, 5);
       }
-      if (sb) S.sgn[par][es >> 2] = bswap32(bc.sg);
-      trace_tile(cur, 4);
-      e32::pack_block(bc, wmax, ep >> 2, reinterpret_cast<uint32_t*>(S.pk[par]));
-      trace_tile(cur, 5);
     } else {
+      if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);
+    }
+    if (do_exact) {
       // exact warp-per-block path, decoding from global memory; places itself
       if constexpr (kOp == kOpSmul) {
         SrcSmulExact src{in, &S, sp.rs, sp.d};
@@ -778,7 +857,8 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
         }
       }
       e32::bar_sync_n(1, kCompute);
-      mbar_arrive_warp(&S.in_empty);   // the per-block offsets in S.bes/bep are no longer needed
+      // the per-block offsets in S.bes/bep are no longer needed
+      if (!released) mbar_arrive_warp(&S.in_empty);
     }
     mbar_arrive_warp(&S.st_full[par]);
     par ^= 1;
@@ -812,6 +892,9 @@ constexpr uint32_t kSmulSmemBytes = recode_smem_bytes<kOpSmul>();
 #ifndef HSZ_SUM_CTAS
 #define HSZ_SUM_CTAS 8
 #endif
+#ifndef HSZ_DEC_SCAN_OR
+#define HSZ_DEC_SCAN_OR 0
+#endif
 
 // staged input tiles in flight per CTA (the moment kernels hold 8 KB of
 // payload per tile: 3 buffers still fit 8 CTAs per SM)
@@ -828,7 +911,7 @@ struct DecSmem {
   Tile in[kNB];
   alignas(1024) unsigned char out[kMode == 2 ? e32::kBufBytes : 16];   // decompress: value tile
   uint64_t full[kNB], empty[kNB];
-  uint32_t scan[4];
+  alignas(16) uint32_t scan[2][4];   // by tile parity: one CTA barrier per tile (cta_scan_or)
 };
 template <int kMode>
 constexpr uint32_t dec_smem_bytes() { return sizeof(DecSmem<kMode>) + 1024; }
@@ -986,10 +1069,19 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
     const uint32_t isb = w ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
     const uint32_t ipb = (static_cast<uint32_t>(len) * w + 7u) >> 3;
     uint32_t itot;
-    const uint32_t iex = e32::cta_scan(isb | (ipb << 10), S.scan, &itot);
+    const bool slow = !(it.staged && w <= static_cast<uint32_t>(kFastW) && o > -(1 << 29) && o < (1 << 29));
+#if HSZ_DEC_SCAN_OR
+    // the in-tile offsets and the CTA-uniform path choice on ONE barrier
+    // (measured: no gain for the moment kernels, 3-4% slower for variance and
+    // decompress on config 4 -- off by default)
+    bool any_slow;
+    const uint32_t iex = e32::cta_scan_or(isb | (ipb << 10), slow, S.scan[i & 1u], &itot, &any_slow);
+    const bool fast = !any_slow;
+#else
+    const uint32_t iex = e32::cta_scan(isb | (ipb << 10), S.scan[0], &itot);
+    const bool fast = e32::bar_or_compute(slow) == false;
+#endif
     const uint32_t ies = iex & 1023u, iep = iex >> 10;
-    const bool fast = e32::bar_or_compute(!(it.staged && w <= static_cast<uint32_t>(kFastW) &&
-                                            o > -(1 << 29) && o < (1 << 29))) == false;
     if (kMode == 2 && i > 0 && tid == 0) {
       // the previous tile's TMA store has finished reading S.out
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

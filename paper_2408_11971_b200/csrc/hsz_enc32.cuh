@@ -192,6 +192,34 @@ __device__ __forceinline__ uint32_t cta_scan(uint32_t v, uint32_t* s_scan, uint3
   return pre + inc - v;
 }
 
+// the same scan with a CTA-wide OR of `flag` riding on its one barrier: each
+// warp's total carries any(flag) of the warp in bit 31 (the sums stay below
+// 2^26).  Callers whose next use of `s_scan` is not separated from this one
+// by another barrier alternate between two buffers.
+#ifndef HSZ_SCAN_OR
+#define HSZ_SCAN_OR 2
+#endif
+__device__ __forceinline__ uint32_t cta_scan_or(uint32_t v, bool flag, uint32_t* s_scan,
+                                                uint32_t* total, bool* any) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t inc = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t o = __shfl_up_sync(kFull, inc, d);
+    if (lane >= d) inc += o;
+  }
+  const bool wany = __any_sync(kFull, flag);
+  if (lane == 31) s_scan[warp] = inc | (wany ? 0x80000000u : 0u);
+  bar_sync_n(1, kCompute);
+  const uint4 a = *reinterpret_cast<const uint4*>(s_scan);
+  *any = ((a.x | a.y | a.z | a.w) >> 31) != 0;
+  const uint32_t a0 = a.x & 0x7fffffffu, a1 = a.y & 0x7fffffffu, a2 = a.z & 0x7fffffffu,
+                 a3 = a.w & 0x7fffffffu;
+  const uint32_t pre = (warp > 0 ? a0 : 0u) + (warp > 1 ? a1 : 0u) + (warp > 2 ? a2 : 0u);
+  *total = a0 + a1 + a2 + a3;
+  return pre + inc - v;
+}
+
 // ---------------------------------------------------------------------------
 // per-thread block encoding
 
@@ -456,7 +484,7 @@ struct Smem7T {
   volatile uint64_t ring_tail;      // bytes of the ring freed (placement warp)
   uint64_t epoch;
   uint32_t alloc_off;
-  uint32_t scan[4];
+  alignas(16) uint32_t scan[4];
   uint32_t wsb[4], wpb[4];
   uint32_t xscratch[4][64];         // exact path: one block's packed words per warp
 };
