@@ -457,7 +457,7 @@ __device__ __forceinline__ void lb_publish(uint64_t* words, uint64_t tile, uint6
 }
 
 #ifndef HSZ_LB2_PER_LANE
-#define HSZ_LB2_PER_LANE 2
+#define HSZ_LB2_PER_LANE 1
 #endif
 
 #ifdef HSZ_TRACE

@@ -13,19 +13,25 @@ import torch  # noqa: E402
 import paper_2408_11971_b200 as H  # noqa: E402
 from paper_2408_11971_b200 import _native, workloads as W  # noqa: E402
 
-x = W.config2(device="cuda").contiguous()
-cfg = W.CONFIGS[2]
+CONFIG = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+x = torch.from_numpy(W.field(CONFIG)).cuda().contiguous()
+cfg = W.CONFIGS[CONFIG]
 raw = H.RawArray(x, cfg["dims"], "f32")
 lo, hi = raw.value_range()
 p = H.QuantParams(cfg["rel_eps"] * (hi - lo), cfg["dims"], 32, "f32")
-s = H.scalar_add(H.negate(H.compress(raw, p)), 3.5)
+s = H.scalar_add(H.negate(H.compress(raw, p)), cfg["sadd"])
 lib = _native.load()
 for _ in range(3):
-    z = H.scalar_mul(s, -1.25)
+    z = H.scalar_mul(s, cfg["smul"])
 torch.cuda.synchronize()
 lib.hsz_trace_read(None, 0, 1)
-z = H.scalar_mul(s, -1.25)
+lib.hsz_trace_lookback(None)
+z = H.scalar_mul(s, cfg["smul"])
 torch.cuda.synchronize()
+lb = (ctypes.c_uint * 3)()
+lib.hsz_trace_lookback(lb)
+print("look-back: rounds %d sleeps %d resolves %d -> %.2f rounds, %.2f sleeps per resolve" %
+      (lb[0], lb[1], lb[2], lb[0] / max(lb[2], 1), lb[1] / max(lb[2], 1)))
 buf = (ctypes.c_ulonglong * (1 << 20))()
 n = lib.hsz_trace_read(buf, 1 << 20, 1)
 a = np.frombuffer(buf, dtype=np.uint64, count=n)
