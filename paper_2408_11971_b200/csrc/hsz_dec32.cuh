@@ -411,6 +411,9 @@ __device__ __forceinline__ void decode_f32(const unsigned char* sgn, const unsig
 // decode front (one or two staged input tiles), per-element transform in
 // registers, the encoder back half of hsz_enc32.cuh.
 
+#ifndef HSZ_LATE_DRAW
+#define HSZ_LATE_DRAW 1
+#endif
 constexpr int kOpSmul = 0, kOpAdd = 1, kOpSub = 2;
 constexpr uint32_t kEwPayCap = 8192;   // per operand (two staged tiles: 4 CTAs per SM)
 
@@ -619,11 +622,20 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
     uint64_t tv2 = kTwo ? prefetch_toff(in2, ahead) : 0ull;
     for (uint32_t k = 0; t < ntiles; ++k) {
       const uint64_t nx = ahead;
+#if !HSZ_LATE_DRAW
       if (lane == 0 && nx < ntiles) ahead = draw();
       ahead = __shfl_sync(kFull, ahead, 0);
+#endif
       mbar_wait_parity_sleep(&S.in_empty, k & 1u);
       stage_tile(in, nx, tv, S.in, &S.bar);
       if constexpr (kTwo) stage_tile(in2, nx, tv2, S.in2, &S.bar);
+#if HSZ_LATE_DRAW
+      // draw the ticket after the wait, not before it: a tile period less
+      // between a ticket and its tile's aggregate, so fewer look-backs find a
+      // predecessor that has not published yet
+      if (lane == 0 && nx < ntiles) ahead = draw();
+      ahead = __shfl_sync(kFull, ahead, 0);
+#endif
       tv = prefetch_toff(in, ahead);
       if (kTwo) tv2 = prefetch_toff(in2, ahead);
       t = nx;
