@@ -466,11 +466,24 @@ __device__ unsigned long long g_lb_cycles_round, g_lb_cycles_total;
 #endif
 
 // one full warp: exclusive prefix of `tile` (its aggregate already published);
-// publishes the tile's inclusive prefix.  Each round inspects 32 * L tiles.
+// publishes the tile's inclusive prefix.
+//
+// Each round lane i reads the record of tile base - i (one L2 round trip for
+// the warp) and the warp accepts the records from the nearest one up to the
+// first inclusive prefix -- or up to the first record that is not published
+// yet, in which case the next round resumes AT that record (no re-read of
+// what was accepted, the window slides 32 tiles further back behind it).
+// Accepted values stay in per-lane partial sums; the one cross-lane
+// reduction happens at the end.  (The placement warp of a CTA spends most of
+// a tile period here, competing for issue slots with the compute warps: the
+// round is ~30 instructions instead of the ~100 of the reduce-every-round
+// form, which measured 3.8 us per resolve on config 4.)
+#if HSZ_LB2_PER_LANE != 1
+#error "lb_resolve reads one record per lane"
+#endif
 __device__ __forceinline__ void lb_resolve(uint64_t* words, uint64_t tile, uint64_t epoch,
                                            uint64_t agg_s, uint64_t agg_p, uint64_t* excl_s,
                                            uint64_t* excl_p, uint32_t* err) {
-  constexpr int L = HSZ_LB2_PER_LANE;
   const int lane = threadIdx.x & 31;
   if (tile == 0) {
     *excl_s = 0;
@@ -478,15 +491,13 @@ __device__ __forceinline__ void lb_resolve(uint64_t* words, uint64_t tile, uint6
     return;
   }
   const uint64_t tag = lb_tag(epoch);
-  uint64_t sum_s = 0, sum_p = 0;
+  uint64_t acc_s = 0, acc_p = 0;   // this lane's accepted records
   int64_t base = static_cast<int64_t>(tile) - 1;
   unsigned backoff = 16;
   const unsigned max_sleeps = g_lb_max_sleeps;
   unsigned nsleep = 0;
 #ifdef HSZ_TRACE
   unsigned rounds = 0, sleeps = 0;
-#endif
-#ifdef HSZ_TRACE
   const long long c_start = clock64();
   long long c_round = 0;
 #endif
@@ -495,38 +506,33 @@ __device__ __forceinline__ void lb_resolve(uint64_t* words, uint64_t tile, uint6
     ++rounds;
     const long long c0 = clock64();
 #endif
-    // lane covers tiles base - lane*L - j, j = 0..L-1 (nearest first).  All
-    // loads are issued before any is consumed (one L2 round trip per round).
-    uint64_t ra[L], rb[L];
-#pragma unroll
-    for (int j = 0; j < L; ++j) {
-      const int64_t idx = base - (lane * L + j);
-      ld_relaxed_v2(words + kLbStride * (idx >= 0 ? idx : 0), &ra[j], &rb[j]);
-    }
-    uint64_t s = 0, p = 0;
-    bool found = false, invalid = false;
-#pragma unroll
-    for (int j = 0; j < L; ++j) {
-      const bool real = base - (lane * L + j) >= 0;   // else: virtual inclusive 0 before tile 0
-      const uint64_t ta = ra[j] >> kLbValBits, tb = rb[j] >> kLbValBits;
-      const bool ok = !real || ((ta == tb) & ((ta & ~kLbIncBit) == tag));
-      const bool inc = !real || (ta & kLbIncBit) != 0;
-      const bool take = !found;
-      invalid |= take & !ok;
-      s += (take & real) ? (ra[j] & kLbValMask) : 0ull;
-      p += (take & real) ? (rb[j] & kLbValMask) : 0ull;
-      found |= ok & inc;
-    }
-    const unsigned fm = __ballot_sync(kFull, found);
+    const int64_t idx = base - lane;
+    const bool real = idx >= 0;      // else: the virtual inclusive 0 before tile 0
+    uint64_t ra, rb;
+    ld_relaxed_v2(words + kLbStride * (real ? idx : 0), &ra, &rb);
+    const uint64_t ta = ra >> kLbValBits, tb = rb >> kLbValBits;
+    const bool ok = !real || ((ta == tb) & ((ta & ~kLbIncBit) == tag));
+    const bool inc = !real || (ta & kLbIncBit) != 0;
+    const unsigned fm = __ballot_sync(kFull, ok & inc);   // inclusive prefixes
+    const unsigned vm = __ballot_sync(kFull, !ok);        // not published yet
 #ifdef HSZ_TRACE
     c_round += clock64() - c0;
 #endif
-    const int first = fm ? (__ffs(fm) - 1) : 32;
-    // lanes up to and including the first one holding an inclusive must have
-    // read only valid records before (or at) their inclusive one
-    const bool bad = lane <= first && invalid;
-    if (__any_sync(kFull, bad)) {
-      if (++nsleep > max_sleeps) {     // watchdog (warp-uniform): give up, flagged
+    const int first = fm ? (__ffs(fm) - 1) : 32;          // nearest inclusive prefix
+    const int hole = vm ? (__ffs(vm) - 1) : 32;           // nearest unpublished record
+    const int take = hole < first ? hole : first + 1;     // lanes [0, take) are accepted
+    if (lane < take && real) {
+      acc_s += ra & kLbValMask;
+      acc_p += rb & kLbValMask;
+    }
+    if (hole > first) break;        // reached an inclusive prefix with no hole before it
+    if (hole == 32) {               // 32 aggregates, no inclusive prefix yet: further back
+      base -= 32;
+      continue;
+    }
+    base -= hole;                   // resume at the unpublished record
+    if (hole == 0) {                // no progress this round: back off
+      if (++nsleep > max_sleeps) {  // watchdog (warp-uniform): give up, flagged
         if (lane == 0) atomicOr(err, HSZ_ERR_LOOKBACK_TIMEOUT);
         break;
       }
@@ -535,25 +541,18 @@ __device__ __forceinline__ void lb_resolve(uint64_t* words, uint64_t tile, uint6
 #ifdef HSZ_TRACE
       ++sleeps;
 #endif
-      continue;
+    } else {
+      backoff = 16;
     }
-    if (lane > first) {
-      s = 0;
-      p = 0;
-    }
+  }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      s += __shfl_xor_sync(kFull, s, o);
-      p += __shfl_xor_sync(kFull, p, o);
-    }
-    sum_s += s;
-    sum_p += p;
-    if (first < 32) break;
-    base -= 32 * L;
+  for (int o = 16; o > 0; o >>= 1) {
+    acc_s += __shfl_xor_sync(kFull, acc_s, o);
+    acc_p += __shfl_xor_sync(kFull, acc_p, o);
   }
   if (lane == 0) {
     const uint64_t t = (tag | kLbIncBit) << kLbValBits;
-    st_relaxed_v2(words + kLbStride * tile, t | (sum_s + agg_s), t | (sum_p + agg_p));
+    st_relaxed_v2(words + kLbStride * tile, t | (acc_s + agg_s), t | (acc_p + agg_p));
 #ifdef HSZ_TRACE
     atomicAdd(&g_lb_rounds, rounds);
     atomicAdd(&g_lb_sleeps, sleeps);
@@ -562,8 +561,8 @@ __device__ __forceinline__ void lb_resolve(uint64_t* words, uint64_t tile, uint6
     atomicAdd(&g_lb_cycles_total, static_cast<unsigned long long>(clock64() - c_start));
 #endif
   }
-  *excl_s = sum_s;
-  *excl_p = sum_p;
+  *excl_s = acc_s;
+  *excl_p = acc_p;
 }
 
 // ---------------------------------------------------------------------------
