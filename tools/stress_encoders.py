@@ -29,13 +29,19 @@ import paper_2408_11971_b200 as H  # noqa: E402
 
 
 def _field(rng, n):
-    kind = int(rng.integers(0, 3))
+    kind = int(rng.integers(0, 4))
     if kind == 0:
         x = np.cumsum(rng.normal(0, rng.uniform(0.1, 3), n))
     elif kind == 1:
         x = np.exp(rng.normal(0, 1.5, n))
-    else:
+    elif kind == 2:
         x = np.sin(np.arange(n) / rng.uniform(10, 500)) * rng.uniform(1, 50)
+    else:
+        # tiles alternating between quiet and very noisy data: packed tile
+        # sizes jump between a few hundred bytes and most of the staging ring
+        # (the pattern behind the round-2 ring deadlock)
+        amp = np.where((np.arange(n) // 4096) % 2 == 0, 1e-3, 1.0) * rng.uniform(0.5, 2)
+        x = rng.normal(0, 1, n) * amp
     return torch.from_numpy(x.astype(np.float32)).cuda()
 
 
