@@ -411,6 +411,9 @@ __device__ __forceinline__ void decode_f32(const unsigned char* sgn, const unsig
 // decode front (one or two staged input tiles), per-element transform in
 // registers, the encoder back half of hsz_enc32.cuh.
 
+#ifndef HSZ_SMUL_I2F
+#define HSZ_SMUL_I2F 1
+#endif
 #ifndef HSZ_LATE_DRAW
 #define HSZ_LATE_DRAW 1
 #endif
@@ -754,9 +757,14 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
         for (int i = 0; i < K; ++i) {
           // bin * rs in one FMA from the biased bin (2^52 + 2^31 + bin): the
           // exact product-sum is bin * rs (< 2^53), so the one rounding is exact
+#if HSZ_SMUL_I2F
+          // (int -> double by the conversion unit, then the exact product)
+          const double pd = __dmul_rn(__int2double_rn(q[i]), sp.rsd);
+#else
           const double pd = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(
                                          static_cast<uint32_t>(q[i]) ^ 0x80000000u)),
                                      sp.rsd, sp.negc);
+#endif
           const double tt = __dmul_rn(sp.d, pd);
           // floor(RN(|t| + 1/2)): RN(|t| + 1/2) is exact here (|t| < 2^31), and
           // adding 2^52 rounding toward -inf leaves floor() in the low word
