@@ -313,3 +313,26 @@ def test_encoder_ring_small_then_large_tile(H, w_small, w_big):
         sc = H.compress(H.RawArray(x, (n,), "f32"), p)
         assert H.serialize(sc) == O.serialize(O.compress(x, 0.5, (n,), 32, "f32"))
         assert H.serialize(sc) == O.serialize(ref)
+
+
+def test_scalar_mul_overflow_detected_after_input_release(H):
+    """scalar_mul releases the staged input tile right after the decode; a tile
+    whose RESCALED bins leave the register range (|bin'| >= 2^30) is only
+    detected afterwards and re-decodes from global memory with the header
+    copies kept outside the staged tile.  Tiles alternate between bins that
+    stay in range and bins that leave it; many more tiles than resident CTAs,
+    so every CTA meets both kinds back to back.  Bytes against the oracle."""
+    ntiles = 1500
+    n = 4096 * ntiles + 5
+    rng = np.random.default_rng(77)
+    bins = np.cumsum(rng.integers(-3, 4, n)).astype(np.int64)
+    big = (np.arange(n) // 4096) % 3 == 1
+    bins[big] += 40_000_000                       # x 30 -> 1.2e9 >= 2^30
+    s, ref = _bins_stream(H, bins, n)
+    scalar = 30.0                                  # eps 0.01: rs = 1500 (< 2^23), bin' = round(0.02 * 1500 * bin)
+    want = O.scalar_mul(ref, scalar)
+    got = H.scalar_mul(s, scalar)
+    assert H.serialize(got) == O.serialize(want)
+    # and the same stream device-resident (asynchronous path)
+    ds = H.DeviceStream.from_host(s)
+    assert H.serialize(H.scalar_mul(ds, scalar).to_host()) == O.serialize(want)
