@@ -1157,7 +1157,6 @@ int hsz_scalar_mul(const uint8_t* widths, const int32_t* outliers, const uint8_t
     sp.d = d;
     sp.rsd = static_cast<double>(rs);
     sp.small_rs = (rs > -(1ll << 23) && rs < (1ll << 23)) ? 1 : 0;
-    sp.negc = -4503601774854144.0 * sp.rsd;   // exact when small_rs (register path only)
     const k32::EncodeOut out{ow, oo, os, sign_cap, op, payload_cap, otoff, err, ws};
     return launch_recode<d32::kOpSmul>(in, in, sp, out, nt, st);
   }
@@ -1191,7 +1190,7 @@ int hsz_elementwise(const uint8_t* wa, const int32_t* oa, const uint8_t* sa, con
     const uint32_t tl = tail_len_of(n, 32);
     const d32::StreamIn A{wa, oa, sa, pa, ta, n, nb, nt, tl};
     const d32::StreamIn B{wb, ob, sb, pb, tb, n, nb, nt, tl};
-    const d32::SmulParams sp{0, 0.0, 0.0, 0, 0.0};
+    const d32::SmulParams sp{0, 0.0, 0.0, 0};
     const k32::EncodeOut out{ow, oo, os, sign_cap, op, payload_cap, otoff, err, ws};
     return sub ? launch_recode<d32::kOpSub>(A, B, sp, out, nt, st)
                : launch_recode<d32::kOpAdd>(A, B, sp, out, nt, st);

@@ -411,12 +411,6 @@ __device__ __forceinline__ void decode_f32(const unsigned char* sgn, const unsig
 // decode front (one or two staged input tiles), per-element transform in
 // registers, the encoder back half of hsz_enc32.cuh.
 
-#ifndef HSZ_SMUL_I2F
-#define HSZ_SMUL_I2F 1
-#endif
-#ifndef HSZ_LATE_DRAW
-#define HSZ_LATE_DRAW 1
-#endif
 constexpr int kOpSmul = 0, kOpAdd = 1, kOpSub = 2;
 constexpr uint32_t kEwPayCap = 8192;   // per operand (two staged tiles: 4 CTAs per SM)
 
@@ -461,13 +455,8 @@ struct SrcSmulExact {
   double d;
   __device__ __forceinline__ int64_t lane_bin(int lb, int lane, int len, uint32_t* flags) {
     uint32_t f = 0;
-#if HSZ_SCAN_OR >= 2
     const int64_t q = k32::decode_lane(in.signs, in.payload, S->xw[lb], S->xo[lb],
                                        S->xgs0 + S->bes[lb], S->xgp0 + S->bep[lb], len, lane, &f);
-#else
-    const int64_t q = k32::decode_lane(in.signs, in.payload, S->in.w[lb], S->in.o[lb],
-                                       S->in.gs0 + S->bes[lb], S->in.gp0 + S->bep[lb], len, lane, &f);
-#endif
     *flags |= f;
     if (f || lane >= len) return 0;
     return rescale1(product_rn(q, rs), d, flags);
@@ -547,7 +536,6 @@ struct SmulParams {
   double d;      // 2 eps
   double rsd;    // (double) rs
   int small_rs;  // |rs| < 2^23: every register-path product is exact in float64
-  double negc;   // -(2^52 + 2^31) * rs, exact (45 significant bits)
 };
 
 // in-tile (sign, payload) byte offsets of this thread's block: one CTA scan
@@ -625,20 +613,14 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
     uint64_t tv2 = kTwo ? prefetch_toff(in2, ahead) : 0ull;
     for (uint32_t k = 0; t < ntiles; ++k) {
       const uint64_t nx = ahead;
-#if !HSZ_LATE_DRAW
-      if (lane == 0 && nx < ntiles) ahead = draw();
-      ahead = __shfl_sync(kFull, ahead, 0);
-#endif
       mbar_wait_parity_sleep(&S.in_empty, k & 1u);
       stage_tile(in, nx, tv, S.in, &S.bar);
       if constexpr (kTwo) stage_tile(in2, nx, tv2, S.in2, &S.bar);
-#if HSZ_LATE_DRAW
       // draw the ticket after the wait, not before it: a tile period less
       // between a ticket and its tile's aggregate, so fewer look-backs find a
       // predecessor that has not published yet
       if (lane == 0 && nx < ntiles) ahead = draw();
       ahead = __shfl_sync(kFull, ahead, 0);
-#endif
       tv = prefetch_toff(in, ahead);
       if (kTwo) tv2 = prefetch_toff(in2, ahead);
       t = nx;
@@ -690,7 +672,6 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
       flags |= HSZ_ERR_BAD_WIDTH;
       w = 0;
     }
-#if HSZ_SCAN_OR >= 2
     if constexpr (!kTwo) {
       S.xw[tid] = static_cast<uint8_t>(w);
       S.xo[tid] = o;
@@ -699,16 +680,13 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
         S.xgp0 = S.in.gp0;
       }
     }
-#endif
     uint32_t ies, iep;
     bool fast_in = S.in.staged && w <= static_cast<uint32_t>(kFastW) && o > -(1 << 29) && o < (1 << 29);
     bool exact;
-#if HSZ_SCAN_OR
     if constexpr (!kTwo) {
       // the CTA-uniform path choice rides on the offset scan's barrier
       exact = block_offsets_or(w, len, !fast_in || !sp.small_rs, S.scan_in, &ies, &iep);
     } else
-#endif
     {
       block_offsets(w, len, S.scan_in, &ies, &iep);
     }
@@ -725,18 +703,11 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
       }
       fast_in = fast_in && S.in2.staged && w2 <= static_cast<uint32_t>(kFastW) && o2 > -(1 << 29) &&
                 o2 < (1 << 29);
-#if HSZ_SCAN_OR
       exact = block_offsets_or(w2, len, !fast_in, S.scan_in2, &ies2, &iep2);
-#else
-      block_offsets(w2, len, S.scan_in2, &ies2, &iep2);
-#endif
       S.bes2[tid] = ies2;
       S.bep2[tid] = iep2;
     }
     // CTA-uniform: the register decode is warp-collective (decode_block)
-#if !HSZ_SCAN_OR
-    exact = e32::bar_or_compute(!fast_in || (kOp == kOpSmul && !sp.small_rs));
-#endif
     trace_tile(cur, 2);
     uint32_t qb[K];
     bool released = false;   // this warp's in_empty arrival of the tile is done
@@ -745,26 +716,17 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
       int32_t q[K];
       decode_block<0, kTwo>(S.in.sgn + S.in.soff + ies, S.in.pay + S.in.poff + iep, w, o, len, q);
       if constexpr (kOp == kOpSmul) {
-#if HSZ_SCAN_OR >= 2
         // this warp is done with the staged tile: the next one may load (a
         // tile that still turns out exact re-decodes from the header copies)
         mbar_arrive_warp(&S.in_empty);
         released = true;
-#endif
         // rescale: |bin| < 2^30, |rs| < 2^23 -> bin * rs exact in float64;
         // then ops.py:199-208 verbatim
 #pragma unroll
         for (int i = 0; i < K; ++i) {
-          // bin * rs in one FMA from the biased bin (2^52 + 2^31 + bin): the
-          // exact product-sum is bin * rs (< 2^53), so the one rounding is exact
-#if HSZ_SMUL_I2F
-          // (int -> double by the conversion unit, then the exact product)
+          // int -> double by the conversion unit, then the exact product
+          // (|bin * rs| < 2^53)
           const double pd = __dmul_rn(__int2double_rn(q[i]), sp.rsd);
-#else
-          const double pd = __fma_rn(__hiloint2double(0x43300000, static_cast<int>(
-                                         static_cast<uint32_t>(q[i]) ^ 0x80000000u)),
-                                     sp.rsd, sp.negc);
-#endif
           const double tt = __dmul_rn(sp.d, pd);
           // floor(RN(|t| + 1/2)): RN(|t| + 1/2) is exact here (|t| < 2^31), and
           // adding 2^52 rounding toward -inf leaves floor() in the low word
@@ -782,10 +744,6 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
         for (int i = 0; i < K; ++i) qb[i] = static_cast<uint32_t>(q[i]);
       }
     }
-#if HSZ_SCAN_OR < 2
-    if (kOp == kOpSmul) exact = e32::bar_or_compute(exact || over);   // ... every read of S.in's staged bytes is done
-    else e32::bar_sync_n(1, kCompute);
-#endif
     trace_tile(cur, 3);
     uint32_t ts = 0, tp = 0;
     bool do_exact = exact;   // CTA-uniform
@@ -794,9 +752,6 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
         mbar_arrive_warp(&S.in_empty);
         released = true;
       }
-#if HSZ_SCAN_OR < 2
-      if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);
-#endif
       e32::BlockCode bc;
       if constexpr (kTwo)
         e32::block_code_resid(qb, bc);   // qb already holds the outlier and residuals
@@ -806,7 +761,6 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
       const uint32_t sb = (bc.w && active) ? ((static_cast<uint32_t>(len) + 7u) >> 3) : 0u;
       const uint32_t pb = (static_cast<uint32_t>(len) * bc.w + 7u) >> 3;
       uint32_t tot, ex;
-#if HSZ_SCAN_OR >= 2
       if constexpr (kOp == kOpSmul) {
         // the overflow report rides on the output scan's barrier
         ex = e32::cta_scan_or(sb | (pb << 10), over, S.scan, &tot, &do_exact);
@@ -814,9 +768,6 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
         ex = e32::cta_scan(sb | (pb << 10), S.scan, &tot);
       }
       if (k >= 2) mbar_wait_parity(&S.st_empty[par], ((k >> 1) - 1) & 1u);
-#else
-      ex = e32::cta_scan(sb | (pb << 10), S.scan, &tot);
-#endif
       if (!do_exact) {
         const uint32_t es = ex & 1023u, ep = ex >> 10;
         ts = tot & 1023u;

@@ -196,9 +196,6 @@ __device__ __forceinline__ uint32_t cta_scan(uint32_t v, uint32_t* s_scan, uint3
 // warp's total carries any(flag) of the warp in bit 31 (the sums stay below
 // 2^26).  Callers whose next use of `s_scan` is not separated from this one
 // by another barrier alternate between two buffers.
-#ifndef HSZ_SCAN_OR
-#define HSZ_SCAN_OR 2
-#endif
 __device__ __forceinline__ uint32_t cta_scan_or(uint32_t v, bool flag, uint32_t* s_scan,
                                                 uint32_t* total, bool* any) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
