@@ -12,7 +12,7 @@ import torch  # noqa: E402
 import paper_2408_11971_b200 as H  # noqa: E402
 from paper_2408_11971_b200 import distsim, hszio  # noqa: E402
 
-n = 32 * 128 * 3 + 21
+n = 32 * 128 * int(os.environ.get("HSZ_SAN_TILES", "3")) + 21
 i = np.arange(n)
 xa = (np.sin(i / 50.0) * 30 + np.random.default_rng(0).normal(0, 0.1, n)).astype(np.float32)
 xb = (np.cos(i / 70.0) * 10).astype(np.float32)
