@@ -86,10 +86,18 @@ __device__ __forceinline__ bool quantize_fast(double x, const QuantConst& c, int
   return (fabs(y) < 0x1p30 - 2.0) & (fabs(g) < 0.5 - 0x1p-20) & (c.fast_div != 0);
 }
 
-// exact int32 -> double without a conversion instruction
+// exact int32 -> double: the conversion unit (one instruction), or without a
+// conversion instruction (biased mantissa minus 2^52 + 2^31: three)
+#ifndef HSZ_I2F_CVT
+#define HSZ_I2F_CVT 1
+#endif
 __device__ __forceinline__ double i32_to_double(int32_t v) {
+#if HSZ_I2F_CVT
+  return __int2double_rn(v);
+#else
   return __dsub_rn(__hiloint2double(0x43300000, static_cast<int>(static_cast<uint32_t>(v) ^ 0x80000000u)),
                    4503601774854144.0);   // 2^52 + 2^31
+#endif
 }
 
 // Reconstruction RN(d * f64(bin)) (codec.py:107-109); int64 -> f64 is RN.
