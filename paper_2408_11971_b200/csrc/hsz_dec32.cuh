@@ -784,7 +784,7 @@ __global__ void __launch_bounds__(e32::kThreadsWS, HSZ_ENC_CTAS)
         }
         if (sb) S.sgn[par][es >> 2] = bswap32(bc.sg);
         trace_tile(cur, 4);
-        e32::pack_block(bc, wmax, ep >> 2, reinterpret_cast<uint32_t*>(S.pk[par]));
+        e32::pack_block<true>(bc, wmax, ep >> 2, reinterpret_cast<uint32_t*>(S.pk[par]));
         trace_tile(cur, 5);
       }
     } else {

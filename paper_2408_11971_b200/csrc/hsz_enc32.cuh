@@ -293,16 +293,18 @@ __device__ __forceinline__ void pack_fields(const BlockCode& bc, uint32_t a, uin
 }
 
 // wmax = __reduce_max_sync over the warp (warp-uniform grouping; computed by
-// the caller early so its latency overlaps other work)
+// the caller early so its latency overlaps other work).  kG3: three-field
+// groups for widths 8-10 -- the recode kernels gain 2-4% from them (their
+// outputs are a few bits wider than a compressor's), the compressor, at its
+// register limit, loses 1%
+template <bool kG3 = (HSZ_PACK_G3 != 0)>
 __device__ __forceinline__ void pack_block(const BlockCode& bc, uint32_t wmax, uint32_t a,
                                            uint32_t* pbuf) {
   if (bc.w == 0) return;
   if (wmax <= 7) {
     pack_fields<4>(bc, a, pbuf);
-#if HSZ_PACK_G3
-  } else if (wmax <= 10) {
+  } else if (kG3 && wmax <= 10) {
     pack_fields<3>(bc, a, pbuf);
-#endif
   } else if (wmax <= 15) {
     pack_fields<2>(bc, a, pbuf);
   } else {
@@ -459,13 +461,15 @@ __device__ __forceinline__ void resolve6(const k32::EncodeOut& out, uint64_t til
   *ep_out = ep;
 }
 
-// v7: 4 compute warps + 1 placement warp (160 threads, 5 CTAs per SM).  The
+// v7: 4 compute warps + 1 placement warp (160 threads, 4 CTAs per SM).  The
 // compute warps' thread 0 issues the next tile's TMA load as soon as the CTA
 // has read the current tile (single input buffer) and draws tickets one tile
 // ahead; placement and the staging ring are as described above.
 constexpr int kThreadsC = kCompute + 32;
+// (4 CTAs per SM at 96 registers, no spills: 178 us on config 4 against 183
+// at 5 CTAs / 72 registers with ~100 B of spills, 195 at 3)
 #ifndef HSZ_CMP_CTAS
-#define HSZ_CMP_CTAS 5
+#define HSZ_CMP_CTAS 4
 #endif
 
 template <uint32_t kInBytes>
