@@ -900,6 +900,9 @@ constexpr uint32_t kSmulSmemBytes = recode_smem_bytes<kOpSmul>();
 #ifndef HSZ_DEC_SCAN_OR
 #define HSZ_DEC_SCAN_OR 0
 #endif
+#ifndef HSZ_ACC64
+#define HSZ_ACC64 1
+#endif
 
 // staged input tiles in flight per CTA (the moment kernels hold 8 KB of
 // payload per tile: 3 buffers still fit 8 CTAs per SM)
@@ -1098,6 +1101,28 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
       decode_sum<kMode == 1>(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, len, &sp, &sp2);
       mbar_arrive_warp(&S.empty[b]);          // staged bytes consumed
       if (len > 0) {
+#if HSZ_ACC64
+        // block sums in 64 bits where they provably fit (|o| < 2^29 on this
+        // path): S_b = len o + sum P, |S_b| < 2^36; and for widths <= 16
+        // (|P| < 2^21, |sum P| < 2^26) Q_b = sum (o + P)^2 <= 32 (2^29 + 2^21)^2
+        // < 2^64, so its three terms add exactly modulo 2^64.  The 128-bit
+        // products cost ~40 instructions a block.
+        acc.s += static_cast<int64_t>(o) * len + sp;
+        if (kMode == 1) {
+          unsigned __int128 tot;
+          if (w <= 16u) {
+            const uint64_t o2 = static_cast<uint64_t>(static_cast<int64_t>(o) * o);
+            tot = o2 * static_cast<uint64_t>(len) +
+                  static_cast<uint64_t>(2 * static_cast<int64_t>(o) * sp) + sp2;
+          } else {
+            const __int128 oo = o;
+            tot = static_cast<unsigned __int128>(oo * oo * len + 2 * oo * sp + static_cast<__int128>(sp2));
+          }
+          const unsigned __int128 nq = acc.q + tot;
+          acc.q2 += nq < acc.q ? 1u : 0u;
+          acc.q = nq;
+        }
+#else
         const __int128 oo = o;
         acc.s += oo * len + sp;
         if (kMode == 1) {
@@ -1106,6 +1131,7 @@ __global__ void __launch_bounds__(kDecThreads, kMode == 2 ? HSZ_DEC_CTAS : HSZ_S
           acc.q2 += nq < acc.q ? 1u : 0u;
           acc.q = nq;
         }
+#endif
       }
     } else if (fast && HSZ_F32_STREAM) {
       decode_f32(it.sgn + it.soff + ies, it.pay + it.poff + iep, w, o, len, fs.d, S.out + tid * 128,
