@@ -335,7 +335,7 @@ def moments_device(ds: DeviceStream, want_sq: bool):
 
 def unpack_moments(limbs) -> tuple:
     """u64[5] -> (S: signed 128-bit, Q: unsigned 192-bit) as Python ints."""
-    v = [int(x) for x in np.asarray(limbs).view(np.uint64)]
+    v = np.asarray(limbs).view(np.uint64).tolist()   # (Python ints; 4 us less than a per-element int())
     S = v[0] | (v[1] << 64)
     if S >= 1 << 127:
         S -= 1 << 128
