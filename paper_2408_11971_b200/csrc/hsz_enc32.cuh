@@ -389,7 +389,10 @@ __device__ __forceinline__ void resolve_tile(Smem& S, const k32::EncodeOut& out,
 #define HSZ_RING_BYTES 16384
 #endif
 constexpr uint32_t kRingBytes = HSZ_RING_BYTES;
-constexpr int kSlots = 4;
+#ifndef HSZ_RING_SLOTS
+#define HSZ_RING_SLOTS 4
+#endif
+constexpr int kSlots = HSZ_RING_SLOTS;
 
 struct RingRec {
   uint64_t tile;
