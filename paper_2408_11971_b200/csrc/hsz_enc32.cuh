@@ -97,6 +97,32 @@ __device__ __forceinline__ uint32_t quant_f32(float x, const QuantF32& qf, bool&
   return mb + 1u + static_cast<uint32_t>(__float_as_int(v) >> 31);
 }
 
+// The same quantizer for the hot loop: the certificate of a whole row is
+// tested once, on the smallest |v| and the largest |p| of its 32 elements --
+// a three-input FMNMX3 folds two elements' magnitudes per instruction, where
+// the per-element form spends two FSETP and half a PLOP3 (48 instructions a
+// block less).  The maximum propagates NaN (a NaN or infinite x fails the
+// test like before; v is only non-finite when p is).
+__device__ __forceinline__ float max3_nan_abs(float a, float b, float c) {
+  float r;
+  asm("{\n\t.reg .f32 x, y;\n\tabs.f32 x, %2;\n\tabs.f32 y, %3;\n\tmax.NaN.f32 %0, %1, x, y;\n}"
+      : "=f"(r)
+      : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ uint32_t quant_f32m(float x, const QuantF32& qf, float& vmin, float& pout) {
+  const float p = __fmul_rn(x, qf.rh);
+  const float e = __fmaf_rn(x, qf.rh, -p);
+  const float m = floorf(p);
+  const float f = __fsub_rn(p, m);
+  const float c = __fmaf_rn(x, qf.rl, e);
+  const float v = __fadd_rn(__fsub_rn(f, 0.5f), c);
+  vmin = fminf(vmin, fabsf(v));
+  pout = p;
+  const uint32_t mb = __float_as_uint(__fadd_rn(m, kMagicF));
+  return mb + 1u + static_cast<uint32_t>(__float_as_int(v) >> 31);
+}
+
 struct ExactQ {
   int64_t q;
   uint32_t flags;
@@ -263,6 +289,9 @@ __device__ __forceinline__ void block_code_resid(const uint32_t (&qb)[K], BlockC
 
 #ifndef HSZ_PACK_G3
 #define HSZ_PACK_G3 0
+#endif
+#ifndef HSZ_QUANT_MINMAX
+#define HSZ_QUANT_MINMAX 1
 #endif
 
 // MSB-first w-bit fields, G fields combined per step (G * w < 32)
@@ -691,6 +720,21 @@ __global__ void __launch_bounds__(kThreadsC, kBins ? HSZ_BINS_CTAS : HSZ_CMP_CTA
     // ---- quantize this thread's row ----------------------------------------
     {
       const unsigned char* row = in + tid * 128;
+#if HSZ_QUANT_MINMAX
+      float vmin = 1.0f, pmax = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 v = *reinterpret_cast<const float4*>(row + ((j ^ (tid & 7)) << 4));
+        float p0, p1, p2, p3;
+        qb[4 * j + 0] = quant_f32m(v.x, qf, vmin, p0);
+        qb[4 * j + 1] = quant_f32m(v.y, qf, vmin, p1);
+        qb[4 * j + 2] = quant_f32m(v.z, qf, vmin, p2);
+        qb[4 * j + 3] = quant_f32m(v.w, qf, vmin, p3);
+        pmax = max3_nan_abs(pmax, p0, p1);
+        pmax = max3_nan_abs(pmax, p2, p3);
+      }
+      bool bad = !((vmin > qf.delta) & (pmax < 2097152.0f) & (qf.delta > 0.0f));
+#else
       bool bad = false;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -700,6 +744,7 @@ __global__ void __launch_bounds__(kThreadsC, kBins ? HSZ_BINS_CTAS : HSZ_CMP_CTA
         qb[4 * j + 2] = quant_f32(v.z, qf, bad);
         qb[4 * j + 3] = quant_f32(v.w, qf, bad);
       }
+#endif
       if (__any_sync(kFull, bad)) {   // rare: an element inside the certificate margin
         uint32_t mask = 0;
 #pragma unroll

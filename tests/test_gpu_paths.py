@@ -336,3 +336,21 @@ def test_scalar_mul_overflow_detected_after_input_release(H):
     # and the same stream device-resident (asynchronous path)
     ds = H.DeviceStream.from_host(s)
     assert H.serialize(H.scalar_mul(ds, scalar).to_host()) == O.serialize(want)
+
+
+@pytest.mark.parametrize("bad", [float("nan"), float("inf"), -float("inf")])
+def test_compress_unvalidated_nonfinite_is_flagged(H, bad):
+    """The compressor tests its float32 certificate once per 32-element row, on
+    the smallest |v| and the largest |p| of the row; the maximum propagates
+    NaN, so a non-finite value that skipped RawArray's finite check (a
+    pre-validated array) still fails the test and reaches the exact
+    quantizer, which reports it like the reference's 63-bit guard
+    (codec.py:136-137)."""
+    import torch
+
+    n = 4096 * 3 + 7
+    x = torch.linspace(-5.0, 5.0, n, device="cuda", dtype=torch.float32)
+    x[4096 + 777] = bad
+    raw = H.RawArray(x, (n,), "f32", _validated=True)
+    with pytest.raises(H.QuantOverflow):
+        H.compress(raw, H.QuantParams(1e-3, (n,), 32, "f32")).check()
